@@ -1,0 +1,115 @@
+"""Front end (reader/elaborator, Stage I, Stage II) against the reference's
+golden outputs: the functional oracle and the imperative interpreter must
+both reproduce the reference's eval_phrase result (reference tests
+TST/test_translate.py:47-55, TST/test_lower.py:192-197)."""
+import pytest
+
+from conftest import load_golden
+from oracle.dpia_eval import eval_phrase, from_json, to_json
+from oracle.imp_eval import RaceError, run_program
+from paper_1710_08332_b200.dtypes import AccT, Array, Num, array
+from paper_1710_08332_b200.reader import ElabError, ParseError, parse, parse_phrase
+from paper_1710_08332_b200.sizes import nat
+from paper_1710_08332_b200.stage1 import translate_program
+from paper_1710_08332_b200.stage2 import is_purely_imperative, stage2
+from paper_1710_08332_b200.terms import Prim, subtree_iter
+
+CASES = load_golden("programs.json") + load_golden("fuzz.json")
+
+
+def _id(c):
+    return c.get("name") or f"fuzz{c['seed']}"
+
+
+@pytest.mark.parametrize("case", CASES, ids=_id)
+def test_parse_and_eval_match_reference(case):
+    if not case.get("reparses", True):
+        # the reference's own parser rejects its printer's output here
+        with pytest.raises(ElabError):
+            parse(case["text"])
+        return
+    sp = parse(case["text"])
+    got = eval_phrase(sp.body, {k: from_json(v) for k, v in case["inputs"].items()},
+                      case.get("sigma", {}))
+    assert to_json(got) == case["expected"]
+
+
+def _count(p, names):
+    return sum(1 for s in subtree_iter(p) if isinstance(s, Prim) and s.name in names)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c.get("reparses", True)][::3], ids=_id)
+def test_stage2_coincidence(case):
+    sp = parse(case["text"])
+    inputs = {k: from_json(v) for k, v in case["inputs"].items()}
+    params = [("out", sp.body_type.data, "out")] + [(k, t.data, "in") for k, t in sp.params]
+    for space, acc in ((None, None), ("global", "private")):
+        s1 = translate_program(sp.body, sp.body_type.data, "out", space)
+        # strategy preservation: one intermediate per source combinator
+        for src, tgt in (("mapGlobal", "mapIGlobal"), ("mapWorkgroup", "mapIWorkgroup"),
+                         ("mapLocal", "mapILocal"), ("mapSeq", "mapISeq")):
+            assert _count(sp.body, {src}) == _count(s1, {tgt})
+        assert _count(sp.body, {"reduce"}) == _count(s1, {"reduceI", "reduceIInit"})
+        s2 = stage2(s1, acc)
+        assert is_purely_imperative(s2)
+        for rev in (False, True):
+            out = run_program(s2, params, inputs, case.get("sigma", {}), case.get("float", False), rev)
+            assert to_json(out["out"]) == case["expected"]
+
+
+def test_dot_file_answer():
+    case = [c for c in CASES if c.get("name") == "dot.dpia"][0]
+    assert case["expected"] == 120  # TST/test_cli.py:69-73
+
+
+def test_parse_errors_and_type_errors():
+    with pytest.raises(ParseError):
+        parse("(param xs (exp (array 4 num))) (map")
+    with pytest.raises(ElabError):
+        parse("(param xs (exp (array 4 num)))\n(zip xs (split 2 xs))")
+    with pytest.raises(ParseError):
+        parse("(param xs (exp (array 4 num)))")
+
+
+def test_transpose_and_abs_additions():
+    src = ("(param m (exp (array 2 (array 3 num))))\n"
+           "(map (lam (r (exp (array 2 num))) (reduce (lam (x (exp num)) (lam (a (exp num))"
+           " (+ (abs x) a))) 0 r)) (transpose m))")
+    sp = parse(src)
+    assert sp.body_type.data == array(3, Num())
+    m = [[1, -2, 3], [-4, 5, -6]]
+    assert eval_phrase(sp.body, {"m": m}) == [5, 7, 9]
+    s2 = stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private")
+    out = run_program(s2, [("out", sp.body_type.data, "out"), ("m", sp.params[0][1].data, "in")],
+                      {"m": m}, {})
+    assert out["out"] == [5, 7, 9]
+
+
+def test_reduce_local_is_reduce():
+    src = ("(param xs (exp (array 16 num)))\n"
+           "(reduceLocal (+) 3 (mapLocal (lam (x (exp num)) (* x x)) xs))")
+    sp = parse(src)
+    xs = list(range(-8, 8))
+    want = 3 + sum(x * x for x in xs)
+    assert eval_phrase(sp.body, {"xs": xs}) == want
+    s2 = stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private")
+    assert _count(s2, {"reduceILocal"}) == 1
+    out = run_program(s2, [("out", Num(), "out"), ("xs", array(16, Num()), "in")], {"xs": xs}, {})
+    assert out["out"] == want
+
+
+def test_seeded_race_is_reported():
+    racy, _ = parse_phrase("(parfor out (lam (i (exp (idx 4))) (lam (o (acc num)) (:= (idxAcc out 0) 1))))",
+                           {"out": AccT(array(4, Num()))})
+    with pytest.raises(RaceError):
+        run_program(racy, [("out", array(4, Num()), "out")], {}, {})
+
+
+def test_sizes_polynomials():
+    n = nat("n")
+    assert (n * 4 + 1) == (1 + 4 * n)
+    assert str(nat(3) * n * n) == "(* (* 3 n) n)"
+    assert (n * 1024).const is None and nat(7).const == 7
+    from paper_1710_08332_b200.sizes import nat_divide
+    assert nat_divide(n * 1024, 1024) == n
+    assert nat_divide(n * 1024 + 3, 1024) is None
