@@ -155,6 +155,8 @@ def _prim(name, targs, args, env, sigma):
         return ev(args[0])(ev(args[1]))
     if name == "idx" and k == 2:
         xs, i = ev(args[0]), ev(args[1])
+        if isinstance(xs, Vec):  # lane of a vector (shim)
+            xs = list(xs.items)
         if not 0 <= i < len(xs):
             raise EvalError(f"index {i} out of bounds {len(xs)}")
         return xs[i]

@@ -1,0 +1,53 @@
+"""Program-level convenience API: parse -> Stage I -> Stage II -> CUDA.
+
+The reference drives this pipeline from its CLI (`SRC/cli.py:122-134` for
+compilation, `:170-183` for `run --launch`): Stage I with
+default_space="global", Stage II with accum_space="private", then the kernel
+backend.  `compile_program` / `run_program_cuda` do the same with the CUDA
+backend in place of the OpenCL emitter and simulator.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+from .dtypes import DataType
+from .launcher import Executable, build, run_kernel
+from .reader import SourceProgram, parse
+from .stage1 import translate_program
+from .stage2 import stage2
+from .terms import Phrase
+
+
+@dataclass
+class Program:
+    source: SourceProgram
+    stage1: Phrase
+    imperative: Phrase
+    name: str = "KERNEL"
+
+    @property
+    def out_type(self) -> DataType:
+        return self.source.body_type.data
+
+    @property
+    def params(self) -> List[Tuple[str, DataType, str]]:
+        return [("out", self.out_type, "out")] + [(n, t.data, "in") for n, t in self.source.params]
+
+
+def compile_program(text: str, name: str = "KERNEL") -> Program:
+    sp = parse(text)
+    s1 = translate_program(sp.body, sp.body_type.data, out="out", default_space="global")
+    return Program(sp, s1, stage2(s1, accum_space="private"), name)
+
+
+def executable(prog: Program, launch, sigma: Optional[Dict[str, int]] = None,
+               float_mode: bool = True, device: int = 0) -> Executable:
+    return build(prog.imperative, prog.params, launch, sigma, float_mode, device, prog.name)
+
+
+def run_program_cuda(prog: Program, inputs: Dict[str, object], sigma=None, launch=(148, 256),
+                     float_mode: bool = True, device: int = 0, flat: bool = False):
+    out = run_kernel(prog.imperative, prog.params, inputs, launch, sigma, float_mode, device,
+                     prog.name, flat=flat)
+    return out["out"]

@@ -1,0 +1,171 @@
+// Device-side templates included by every kernel the DPIA CUDA backend emits.
+//
+// * dpia::vec<T,W>      -- the (vec W) data type: W lanes, naturally aligned so a
+//                          whole-vector access is one 64/128-bit LDG/STG/LDS/STS
+//                          (the backend's rendering of asVector/asScalar, which the
+//                          reference emits as OpenCL vloadW/vstoreW, SRC/codegen_c.py:482-493)
+// * dpia::block_combine -- the cooperative work-group combine behind reduceLocal:
+//                          warp-shuffle tree (__shfl_down_sync) + one shared-memory
+//                          hop per warp; absent from the reference, whose single
+//                          kernels stop at partial sums (programs/dotvec.dpia:4-5)
+// * dpia::grid_arrive   -- last-block-done detection used to fuse a single
+//                          work-group tail phase into the preceding grid phase
+//
+// Self-contained: NVRTC compiles it without any system header.
+#pragma once
+
+namespace dpia {
+
+template <class T, int W>
+struct alignas((sizeof(T) * W <= 16 && (W & (W - 1)) == 0) ? sizeof(T) * W
+               : (sizeof(T) * W > 16 && (W & (W - 1)) == 0) ? 16 : sizeof(T)) vec {
+  T v[W];
+};
+
+template <class T, int W>
+__device__ __forceinline__ vec<T, W> splat(T x) {
+  vec<T, W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.v[k] = x;
+  return r;
+}
+
+#define DPIA_VEC_BINOP(OP)                                                             \
+  template <class T, int W>                                                            \
+  __device__ __forceinline__ vec<T, W> operator OP(const vec<T, W>& a, const vec<T, W>& b) { \
+    vec<T, W> r;                                                                       \
+    _Pragma("unroll") for (int k = 0; k < W; ++k) r.v[k] = a.v[k] OP b.v[k];           \
+    return r;                                                                          \
+  }                                                                                    \
+  template <class T, int W>                                                            \
+  __device__ __forceinline__ vec<T, W> operator OP(const vec<T, W>& a, T b) {          \
+    vec<T, W> r;                                                                       \
+    _Pragma("unroll") for (int k = 0; k < W; ++k) r.v[k] = a.v[k] OP b;                \
+    return r;                                                                          \
+  }                                                                                    \
+  template <class T, int W>                                                            \
+  __device__ __forceinline__ vec<T, W> operator OP(T a, const vec<T, W>& b) {          \
+    vec<T, W> r;                                                                       \
+    _Pragma("unroll") for (int k = 0; k < W; ++k) r.v[k] = a OP b.v[k];                \
+    return r;                                                                          \
+  }
+DPIA_VEC_BINOP(+)
+DPIA_VEC_BINOP(-)
+DPIA_VEC_BINOP(*)
+DPIA_VEC_BINOP(/)
+#undef DPIA_VEC_BINOP
+
+template <class T, int W>
+__device__ __forceinline__ vec<T, W> operator-(const vec<T, W>& a) {
+  vec<T, W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.v[k] = -a.v[k];
+  return r;
+}
+
+__device__ __forceinline__ float abs_(float x) { return fabsf(x); }
+__device__ __forceinline__ double abs_(double x) { return fabs(x); }
+__device__ __forceinline__ long long abs_(long long x) { return x < 0 ? -x : x; }
+template <class T, int W>
+__device__ __forceinline__ vec<T, W> abs_(const vec<T, W>& a) {
+  vec<T, W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.v[k] = abs_(a.v[k]);
+  return r;
+}
+
+// whole-vector read of lanes p[i .. i+W) (i is a multiple of W by construction)
+template <class T, int W>
+__device__ __forceinline__ vec<T, W> vload(const T* p, long long i) {
+  return *reinterpret_cast<const vec<T, W>*>(p + i);
+}
+template <class T, int W>
+__device__ __forceinline__ void vstore(T* p, long long i, const vec<T, W>& x) {
+  *reinterpret_cast<vec<T, W>*>(p + i) = x;
+}
+
+// ------------------------------------------------------------ shuffles
+__device__ __forceinline__ float shfl_down(float x, int d) {
+  return __shfl_down_sync(0xffffffffu, x, d);
+}
+__device__ __forceinline__ double shfl_down(double x, int d) {
+  return __shfl_down_sync(0xffffffffu, x, d);
+}
+__device__ __forceinline__ long long shfl_down(long long x, int d) {
+  return __shfl_down_sync(0xffffffffu, x, d);
+}
+template <class T, int W>
+__device__ __forceinline__ vec<T, W> shfl_down(const vec<T, W>& x, int d) {
+  vec<T, W> r;
+#pragma unroll
+  for (int k = 0; k < W; ++k) r.v[k] = shfl_down(x.v[k], d);
+  return r;
+}
+
+// Fold (value, valid) pairs of one warp into lane 0.  op(x, acc) is the
+// reduction function f x acc of the program; it must be associative and
+// commutative (the contract of reduceLocal).
+template <class T, class Op>
+__device__ __forceinline__ void warp_fold(T& v, bool& has, Op op) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    T o = shfl_down(v, d);
+    bool oh = __shfl_down_sync(0xffffffffu, has, d);
+    if (oh) {
+      v = has ? op(o, v) : o;
+      has = true;
+    }
+  }
+}
+
+// Work-group combine.  Every thread passes its partial (valid iff `has`);
+// every thread receives the combination of all valid partials.  `scratch`
+// holds NWARP_MAX+1 slots of T in shared memory.  Two barriers; safe to call
+// repeatedly (slot ownership alternates between the partial slots and the
+// broadcast slot, so no trailing barrier is needed).
+template <class T, class Op>
+__device__ __forceinline__ T block_combine(T v, bool has, Op op, T* scratch, bool* scratch_has,
+                                           int tid, int nthreads, bool& has_out) {
+  warp_fold(v, has, op);
+  const int lane = tid & 31, warp = tid >> 5, nwarps = (nthreads + 31) >> 5;
+  if (nwarps == 1) {
+    if (lane == 0) { scratch[32] = v; scratch_has[32] = has; }
+    __syncthreads();
+    T r = scratch[32];
+    has_out = scratch_has[32];
+    __syncwarp();  // lane 0 may rewrite the slot in the next call
+    return r;
+  }
+  if (lane == 0) { scratch[warp] = v; scratch_has[warp] = has; }
+  __syncthreads();
+  if (warp == 0) {
+    bool h = lane < nwarps ? scratch_has[lane] : false;
+    T w = h ? scratch[lane] : v;
+    warp_fold(w, h, op);
+    if (lane == 0) { scratch[32] = w; scratch_has[32] = h; }
+  }
+  __syncthreads();
+  has_out = scratch_has[32];
+  return scratch[32];
+}
+
+// Last-block-done detection for a fused single-work-group tail phase.
+// Returns true in exactly one block: the last to finish the grid phase.
+__device__ __forceinline__ bool grid_arrive(unsigned int* counter, int tid, bool* flag) {
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int nblocks = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned int ticket = atomicAdd(counter, 1u);
+    *flag = (ticket == nblocks - 1);
+  }
+  __syncthreads();
+  if (*flag) __threadfence();
+  return *flag;
+}
+
+__device__ __forceinline__ void grid_reset(unsigned int* counter, int tid) {
+  if (tid == 0) *counter = 0u;
+}
+
+}  // namespace dpia

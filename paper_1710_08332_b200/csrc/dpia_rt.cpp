@@ -1,0 +1,471 @@
+// libdpia_rt: NVRTC + CUDA driver API + NCCL behind a C ABI (include/dpia_rt.h).
+#include "dpia_rt.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+// ---------------------------------------------------------------------------
+// The CUDA driver is loaded with dlopen so the library itself loads (and its
+// symbols can be inspected) on machines without a GPU driver.  Names go
+// through the cuda.h macros (e.g. cuMemAlloc -> cuMemAlloc_v2) before lookup.
+#define DPIA_STR2(x) #x
+#define DPIA_STR(x) DPIA_STR2(x)
+#define DPIA_DRIVER_FUNCS(X)                                                              \
+  X(cuInit) X(cuGetErrorString) X(cuDeviceGet) X(cuDeviceGetCount) X(cuDeviceGetAttribute)   \
+  X(cuDeviceGetName) X(cuDevicePrimaryCtxRetain) X(cuCtxSetCurrent) X(cuCtxSynchronize)      \
+  X(cuModuleLoadData) X(cuModuleUnload) X(cuModuleGetFunction) X(cuFuncSetAttribute)         \
+  X(cuFuncGetAttribute) X(cuMemAlloc) X(cuMemFree) X(cuMemAllocHost) X(cuMemFreeHost)        \
+  X(cuMemcpyHtoD) X(cuMemcpyDtoH) X(cuMemcpyHtoDAsync) X(cuMemcpyDtoHAsync)                  \
+  X(cuMemcpyDtoDAsync) X(cuMemsetD8Async) X(cuMemsetD32Async) X(cuLaunchKernel)              \
+  X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
+  X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)
+
+namespace drv {
+#define DPIA_DECL(f) decltype(&::f) f = nullptr;
+DPIA_DRIVER_FUNCS(DPIA_DECL)
+#undef DPIA_DECL
+}  // namespace drv
+
+namespace {
+
+thread_local std::string g_err;
+void* g_libcuda = nullptr;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code ? code : -1;
+}
+
+int load_driver() {
+  if (g_libcuda) return 0;
+  g_libcuda = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_libcuda) g_libcuda = dlopen("libcuda.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!g_libcuda) return fail(-1, "cannot load the CUDA driver (libcuda.so.1): %s", dlerror());
+#define DPIA_LOAD(f)                                                         \
+  drv::f = reinterpret_cast<decltype(drv::f)>(dlsym(g_libcuda, DPIA_STR(f))); \
+  if (!drv::f) return fail(-1, "CUDA driver lacks %s", DPIA_STR(f));
+  DPIA_DRIVER_FUNCS(DPIA_LOAD)
+#undef DPIA_LOAD
+  return 0;
+}
+
+int cu(CUresult r, const char* what) {
+  if (r == CUDA_SUCCESS) return 0;
+  const char* s = nullptr;
+  drv::cuGetErrorString(r, &s);
+  return fail(static_cast<int>(r), "%s: %s (%d)", what, s ? s : "?", static_cast<int>(r));
+}
+
+#define CU(call)                                \
+  do {                                          \
+    int _e = cu((call), #call);                 \
+    if (_e) return _e;                          \
+  } while (0)
+
+constexpr int kMaxDev = 64;
+CUcontext g_ctx[kMaxDev] = {};
+std::mutex g_mu;
+
+int bind(int dev) {
+  if (dev < 0 || dev >= kMaxDev) return fail(-1, "bad device %d", dev);
+  if (!g_ctx[dev]) {
+    int e = dpia_init(dev);
+    if (e) return e;
+  }
+  CU(drv::cuCtxSetCurrent(g_ctx[dev]));
+  return 0;
+}
+
+// ------------------------------------------------------------ hash filler
+const char* kFillSrc = R"(
+extern "C" __global__ void dpia_fill_hash_f32(float* out, unsigned long long n,
+    unsigned long long offset, unsigned int seed, float lo, float hi) {
+  unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    unsigned long long k = offset + i;
+    unsigned int h = (unsigned int)(k) * 0x9E3779B1u ^ (unsigned int)(k >> 32) * 0x85EBCA77u ^ seed;
+    h ^= h >> 16; h *= 0x7FEB352Du; h ^= h >> 15; h *= 0x846CA68Bu; h ^= h >> 16;
+    out[i] = __fadd_rn(lo, __fmul_rn(hi - lo, (float)(h >> 8) * (1.0f / 16777216.0f)));
+  }
+}
+)";
+CUmodule g_fill_mod[kMaxDev] = {};
+CUfunction g_fill_fn[kMaxDev] = {};
+CUdeviceptr g_flush_buf[kMaxDev] = {};
+size_t g_flush_bytes[kMaxDev] = {};
+
+// ------------------------------------------------------------------ NCCL
+typedef struct { char internal[128]; } ncclUniqueId_t;
+typedef void* ncclComm_t;
+typedef int (*nccl_get_id_fn)(ncclUniqueId_t*);
+typedef int (*nccl_init_rank_fn)(ncclComm_t*, int, ncclUniqueId_t, int);
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, CUstream);
+typedef int (*nccl_destroy_fn)(ncclComm_t);
+typedef const char* (*nccl_err_fn)(int);
+void* g_nccl = nullptr;
+nccl_get_id_fn p_get_id = nullptr;
+nccl_init_rank_fn p_init_rank = nullptr;
+nccl_allreduce_fn p_allreduce = nullptr;
+nccl_destroy_fn p_destroy = nullptr;
+nccl_err_fn p_errstr = nullptr;
+ncclComm_t g_comm = nullptr;
+
+int load_nccl() {
+  if (g_nccl) return 0;
+  const char* env = getenv("DPIA_NCCL_LIB");
+  const char* cands[] = {env, "libnccl.so.2", "libnccl.so",
+                         "/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2"};
+  for (const char* c : cands) {
+    if (!c) continue;
+    g_nccl = dlopen(c, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl) break;
+  }
+  if (!g_nccl) return fail(-1, "cannot dlopen libnccl.so.2 (set DPIA_NCCL_LIB)");
+  p_get_id = (nccl_get_id_fn)dlsym(g_nccl, "ncclGetUniqueId");
+  p_init_rank = (nccl_init_rank_fn)dlsym(g_nccl, "ncclCommInitRank");
+  p_allreduce = (nccl_allreduce_fn)dlsym(g_nccl, "ncclAllReduce");
+  p_destroy = (nccl_destroy_fn)dlsym(g_nccl, "ncclCommDestroy");
+  p_errstr = (nccl_err_fn)dlsym(g_nccl, "ncclGetErrorString");
+  if (!p_get_id || !p_init_rank || !p_allreduce || !p_destroy)
+    return fail(-1, "libnccl is missing required symbols");
+  return 0;
+}
+
+int nccl(int r, const char* what) {
+  if (r == 0) return 0;
+  return fail(r, "%s: %s", what, p_errstr ? p_errstr(r) : "nccl error");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dpia_last_error(void) { return g_err.c_str(); }
+
+int dpia_init(int device) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (device < 0 || device >= kMaxDev) return fail(-1, "bad device %d", device);
+  if (int e = load_driver()) return e;
+  CU(drv::cuInit(0));
+  if (!g_ctx[device]) {
+    CUdevice d;
+    CU(drv::cuDeviceGet(&d, device));
+    CU(drv::cuDevicePrimaryCtxRetain(&g_ctx[device], d));
+  }
+  CU(drv::cuCtxSetCurrent(g_ctx[device]));
+  return 0;
+}
+
+int dpia_device_count(int* count) {
+  if (int e = load_driver()) return e;
+  CU(drv::cuInit(0));
+  CU(drv::cuDeviceGetCount(count));
+  return 0;
+}
+
+int dpia_device_attribute(int device, int attr, int* value) {
+  if (int e = load_driver()) return e;
+  CU(drv::cuInit(0));
+  CUdevice d;
+  CU(drv::cuDeviceGet(&d, device));
+  CU(drv::cuDeviceGetAttribute(value, static_cast<CUdevice_attribute>(attr), d));
+  return 0;
+}
+
+int dpia_device_name(int device, char* buf, int len) {
+  if (int e = load_driver()) return e;
+  CU(drv::cuInit(0));
+  CUdevice d;
+  CU(drv::cuDeviceGet(&d, device));
+  CU(drv::cuDeviceGetName(buf, len, d));
+  return 0;
+}
+
+int dpia_compile(const char* source, const char* program_name, const char* arch,
+                 const char* options, void** image, size_t* size, char* log, size_t logcap) {
+  if (log && logcap) log[0] = 0;
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name, 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(r, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  std::vector<std::string> opts;
+  opts.push_back(std::string("--gpu-architecture=") + (arch && *arch ? arch : "sm_100a"));
+  opts.push_back("--std=c++17");
+  if (options) {
+    std::string all(options);
+    size_t pos = 0;
+    while (pos <= all.size()) {
+      size_t nl = all.find('\n', pos);
+      std::string o = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+      if (!o.empty()) opts.push_back(o);
+      if (nl == std::string::npos) break;
+      pos = nl + 1;
+    }
+  }
+  std::vector<const char*> cops;
+  for (auto& o : opts) cops.push_back(o.c_str());
+  r = nvrtcCompileProgram(prog, static_cast<int>(cops.size()), cops.data());
+  size_t lsz = 0;
+  nvrtcGetProgramLogSize(prog, &lsz);
+  if (log && logcap && lsz > 1) {
+    std::string l(lsz, '\0');
+    nvrtcGetProgramLog(prog, &l[0]);
+    size_t n = lsz < logcap ? lsz : logcap - 1;
+    memcpy(log, l.data(), n);
+    log[n] = 0;
+  }
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(r, "nvrtcCompileProgram: %s (see log)", nvrtcGetErrorString(r));
+  }
+  size_t n = 0;
+  r = nvrtcGetCUBINSize(prog, &n);
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return fail(r, "nvrtcGetCUBINSize: %s", nvrtcGetErrorString(r));
+  }
+  void* buf = malloc(n);
+  r = nvrtcGetCUBIN(prog, static_cast<char*>(buf));
+  nvrtcDestroyProgram(&prog);
+  if (r != NVRTC_SUCCESS) {
+    free(buf);
+    return fail(r, "nvrtcGetCUBIN: %s", nvrtcGetErrorString(r));
+  }
+  *image = buf;
+  *size = n;
+  return 0;
+}
+
+void dpia_free_host(void* ptr) { free(ptr); }
+
+int dpia_module_load(int device, const void* image, void** module) {
+  if (int e = bind(device)) return e;
+  CUmodule m;
+  CU(drv::cuModuleLoadData(&m, image));
+  *module = m;
+  return 0;
+}
+
+int dpia_module_unload(void* module) {
+  CU(drv::cuModuleUnload(static_cast<CUmodule>(module)));
+  return 0;
+}
+
+int dpia_get_kernel(void* module, const char* name, void** function) {
+  CUfunction f;
+  CU(drv::cuModuleGetFunction(&f, static_cast<CUmodule>(module), name));
+  *function = f;
+  return 0;
+}
+
+int dpia_kernel_set_smem(void* function, int bytes) {
+  CU(drv::cuFuncSetAttribute(static_cast<CUfunction>(function),
+                        CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, bytes));
+  return 0;
+}
+
+int dpia_kernel_attribute(void* function, int attr, int* value) {
+  CU(drv::cuFuncGetAttribute(value, static_cast<CUfunction_attribute>(attr),
+                        static_cast<CUfunction>(function)));
+  return 0;
+}
+
+int dpia_malloc(int device, size_t bytes, uint64_t* dptr) {
+  if (int e = bind(device)) return e;
+  CUdeviceptr p = 0;
+  CU(drv::cuMemAlloc(&p, bytes ? bytes : 16));
+  *dptr = static_cast<uint64_t>(p);
+  return 0;
+}
+
+int dpia_free(int device, uint64_t dptr) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuMemFree(static_cast<CUdeviceptr>(dptr)));
+  return 0;
+}
+
+int dpia_host_alloc(size_t bytes, void** ptr) {
+  CU(drv::cuMemAllocHost(ptr, bytes ? bytes : 16));
+  return 0;
+}
+
+int dpia_host_free(void* ptr) {
+  CU(drv::cuMemFreeHost(ptr));
+  return 0;
+}
+
+int dpia_memcpy_htod(int device, uint64_t dst, const void* src, size_t bytes, void* stream) {
+  if (int e = bind(device)) return e;
+  if (stream) CU(drv::cuMemcpyHtoDAsync(dst, src, bytes, static_cast<CUstream>(stream)));
+  else CU(drv::cuMemcpyHtoD(dst, src, bytes));
+  return 0;
+}
+
+int dpia_memcpy_dtoh(int device, void* dst, uint64_t src, size_t bytes, void* stream) {
+  if (int e = bind(device)) return e;
+  if (stream) CU(drv::cuMemcpyDtoHAsync(dst, src, bytes, static_cast<CUstream>(stream)));
+  else CU(drv::cuMemcpyDtoH(dst, src, bytes));
+  return 0;
+}
+
+int dpia_memcpy_dtod(int device, uint64_t dst, uint64_t src, size_t bytes, void* stream) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuMemcpyDtoDAsync(dst, src, bytes, static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_memset(int device, uint64_t dst, int value, size_t bytes, void* stream) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuMemsetD8Async(dst, static_cast<unsigned char>(value), bytes, static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_launch(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
+                unsigned smem, void** args, void* stream) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuLaunchKernel(static_cast<CUfunction>(function), gx, gy, 1, bx, by, 1, smem,
+                    static_cast<CUstream>(stream), args, nullptr));
+  return 0;
+}
+
+int dpia_stream_create(int device, void** stream) {
+  if (int e = bind(device)) return e;
+  CUstream s;
+  CU(drv::cuStreamCreate(&s, CU_STREAM_NON_BLOCKING));
+  *stream = s;
+  return 0;
+}
+
+int dpia_stream_destroy(void* stream) {
+  CU(drv::cuStreamDestroy(static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_stream_sync(void* stream) {
+  CU(drv::cuStreamSynchronize(static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_device_sync(int device) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuCtxSynchronize());
+  return 0;
+}
+
+int dpia_event_create(int device, void** event) {
+  if (int e = bind(device)) return e;
+  CUevent ev;
+  CU(drv::cuEventCreate(&ev, CU_EVENT_DEFAULT));
+  *event = ev;
+  return 0;
+}
+
+int dpia_event_destroy(void* event) {
+  CU(drv::cuEventDestroy(static_cast<CUevent>(event)));
+  return 0;
+}
+
+int dpia_event_record(void* event, void* stream) {
+  CU(drv::cuEventRecord(static_cast<CUevent>(event), static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_event_elapsed(void* start, void* stop, float* ms) {
+  CU(drv::cuEventSynchronize(static_cast<CUevent>(stop)));
+  CU(drv::cuEventElapsedTime(ms, static_cast<CUevent>(start), static_cast<CUevent>(stop)));
+  return 0;
+}
+
+int dpia_l2_flush(int device, void* stream) {
+  if (int e = bind(device)) return e;
+  if (!g_flush_buf[device]) {
+    int l2 = 0;
+    CUdevice d;
+    CU(drv::cuDeviceGet(&d, device));
+    CU(drv::cuDeviceGetAttribute(&l2, CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE, d));
+    g_flush_bytes[device] = static_cast<size_t>(l2 > 0 ? l2 : (128 << 20)) * 2;
+    CU(drv::cuMemAlloc(&g_flush_buf[device], g_flush_bytes[device]));
+  }
+  CU(drv::cuMemsetD32Async(g_flush_buf[device], 0x5a5a5a5a, g_flush_bytes[device] / 4,
+                      static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_fill_hash_f32(int device, uint64_t dptr, uint64_t count, uint64_t offset, uint32_t seed,
+                       float lo, float hi, void* stream) {
+  if (int e = bind(device)) return e;
+  if (!g_fill_fn[device]) {
+    void* img = nullptr;
+    size_t sz = 0;
+    char log[4096];
+    int major = 0, minor = 0;
+    CUdevice d;
+    CU(drv::cuDeviceGet(&d, device));
+    CU(drv::cuDeviceGetAttribute(&major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, d));
+    CU(drv::cuDeviceGetAttribute(&minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, d));
+    char arch[32];
+    snprintf(arch, sizeof arch, "sm_%d%d%s", major, minor, major >= 9 ? "a" : "");
+    if (int e = dpia_compile(kFillSrc, "dpia_fill.cu", arch, "", &img, &sz, log, sizeof log)) return e;
+    CUresult r = drv::cuModuleLoadData(&g_fill_mod[device], img);
+    free(img);
+    CU(r);
+    CU(drv::cuModuleGetFunction(&g_fill_fn[device], g_fill_mod[device], "dpia_fill_hash_f32"));
+  }
+  unsigned long long n = count, off = offset;
+  void* args[] = {&dptr, &n, &off, &seed, &lo, &hi};
+  CU(drv::cuLaunchKernel(g_fill_fn[device], 148 * 8, 1, 1, 256, 1, 1, 0,
+                    static_cast<CUstream>(stream), args, nullptr));
+  return 0;
+}
+
+int dpia_nccl_available(void) { return load_nccl() == 0 ? 1 : 0; }
+
+int dpia_nccl_unique_id(char out[128]) {
+  if (int e = load_nccl()) return e;
+  ncclUniqueId_t id;
+  if (int e = nccl(p_get_id(&id), "ncclGetUniqueId")) return e;
+  memcpy(out, id.internal, 128);
+  return 0;
+}
+
+int dpia_nccl_init(int device, int nranks, int rank, const char id[128]) {
+  if (int e = load_nccl()) return e;
+  if (int e = bind(device)) return e;
+  ncclUniqueId_t uid;
+  memcpy(uid.internal, id, 128);
+  return nccl(p_init_rank(&g_comm, nranks, uid, rank), "ncclCommInitRank");
+}
+
+int dpia_nccl_allreduce(uint64_t dptr, size_t count, int dtype, void* stream) {
+  if (!g_comm) return fail(-1, "NCCL communicator not initialised");
+  // ncclDataType_t: ncclFloat32 = 7, ncclFloat64 = 8, ncclInt64 = 4; ncclSum = 0
+  int nd = dtype == 0 ? 7 : dtype == 1 ? 8 : 4;
+  void* p = reinterpret_cast<void*>(dptr);
+  return nccl(p_allreduce(p, p, count, nd, 0, g_comm, static_cast<CUstream>(stream)),
+              "ncclAllReduce");
+}
+
+int dpia_nccl_destroy(void) {
+  if (g_comm && p_destroy) {
+    int r = p_destroy(g_comm);
+    g_comm = nullptr;
+    return nccl(r, "ncclCommDestroy");
+  }
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,1346 @@
+"""CUDA C emitter for purely imperative DPIA (Stage III for sm_100a).
+
+Replaces the reference's OpenCL backend (`SRC/opencl.py:124-314` with the
+opencl dialect of `SRC/codegen_c.py` / `SRC/c_ast.py`).  The input is a Stage
+II phrase (or the reference's hoisted form); the output is one CUDA
+translation unit with one `__global__` function per *phase*.
+
+Strategy preservation -- each hierarchy annotation becomes one CUDA construct:
+
+  parforGlobal        grid-stride loop over the linear global thread id
+  parforWorkgroup{,1} blockIdx.{x,y} loop (stride gridDim)
+  parforLocal{,1}     threadIdx.{x,y} loop (stride blockDim)
+  parfor (plain)      the innermost free level: global at kernel top level,
+                      all threads of the block at work-group level,
+                      sequential inside a work item
+  for                 sequential loop (#pragma unroll when small & constant)
+  newLocal            __shared__ staging (one arena, static offsets)
+  newPrivate          registers (per-thread arrays; thread-sliced, below)
+  newGlobal           device scratch buffer, one slice per parallel iteration
+  asVector/asScalar   whole-vector dpia::vec loads/stores (LDG/STG.128)
+  reduceILocal        dpia::block_combine (warp shuffles + one smem hop)
+
+Additions over the reference backend (SURVEY.md sections 0 and 7):
+  * access-path resolution with 64-bit-safe, range-simplified subscripts;
+  * barrier placement for RAW, WAR and loop-carried hazards on shared
+    buffers at work-group-uniform program points (the reference misses the
+    loop-carried case);
+  * shared buffers inside sequential loops are reused, not multiplied by the
+    trip count (SURVEY.md finding 4);
+  * thread slicing: a private buffer declared at work-group level whose every
+    access is indexed by this thread's local ids keeps only its own slice;
+  * writes to shared/global memory at work-group-uniform points are made by
+    one thread (the reference rejects such programs as not fully parallel);
+  * phase splitting at grid-wide dependences, with a single-work-group tail
+    phase fused into the preceding grid phase by last-block-done detection.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Set, Tuple, Union
+
+from ..dtypes import Array, DataType, Idx, Num, Pair, Vector
+from ..signatures import LOOP_LEVEL, NEW_SPACE, PARFOR_FAMILY
+from ..sizes import Nat, nat
+from ..terms import Lam, Lit, PairP, Phrase, Prim, Proj, Var, free_vars, subtree_iter, unapply
+from . import index as IX
+from .ctypes_map import CudaError, TypeTable, split_array
+from .index import Ix, div, ix, mod, render
+
+HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "dpia_device.cuh")
+UNROLL_LIMIT = 64
+
+
+class NeedLanes(Exception):
+    """A whole-vector access has to be split into lanes."""
+
+
+# ---------------------------------------------------------------- bindings
+
+@dataclass
+class Buffer:
+    key: str                 # phrase-level binder
+    cname: str
+    space: str               # in | out | global | local | private
+    dtype: DataType          # full type, hoisting dims included
+    prefix: List[Ix] = field(default_factory=list)
+    sliced: int = 0
+
+    @property
+    def dims(self):
+        return split_array(self.dtype)[0]
+
+    @property
+    def elem(self):
+        return split_array(self.dtype)[1]
+
+
+@dataclass
+class Val:
+    dtype: DataType
+    text: Optional[str] = None
+    ixv: Optional[Ix] = None
+
+
+@dataclass
+class Alias:
+    """The per-iteration acceptor `o` of a parfor: (idxAcc a i)."""
+    acc: Phrase
+    i: Ix
+
+
+@dataclass
+class Ref:
+    buf: Buffer
+    flat: Optional[Ix]
+    suffix: str
+    text: str
+
+
+@dataclass
+class VStore:
+    ref: Ref
+    width: int
+
+
+@dataclass
+class Loop:
+    level: str          # global workgroup local lin seq fold lambda
+    dim: int
+    var: str
+    trip: Optional[int]
+    trip_nat: Nat
+    single: bool = False
+
+
+Step = Tuple[str, object]   # ("i", Ix) | ("f", 1|2)
+
+
+# ------------------------------------------------------------ signatures
+
+@dataclass
+class KernelInfo:
+    name: str
+    grid: str                # "launch" (user launch) or "single" (one block)
+    args: List[Tuple[str, str]]   # (kind, name): kind in out/in/scratch/size/counter
+    smem: int
+    fused_tail: bool
+
+
+@dataclass
+class CudaSignature:
+    outputs: List[Tuple[str, DataType]]
+    inputs: List[Tuple[str, DataType]]
+    buffers: List[Tuple[str, DataType]]     # device scratch (global) buffers
+    sizes: List[str]                          # runtime size arguments (unspecialised)
+    kernels: List[KernelInfo]
+    scalar: str
+    launch: Optional[Tuple[Tuple[int, int], Tuple[int, int]]]
+    sigma: Optional[Dict[str, int]]
+
+    def params(self) -> List[str]:
+        out = [f"{self.scalar} *{n}" for n, _ in self.outputs]
+        out += [f"const {self.scalar} *__restrict__ {n}" for n, _ in self.inputs]
+        out += [f"{self.scalar} *{n}" for n, _ in self.buffers]
+        out += [f"long long {n}" for n in self.sizes]
+        return out
+
+
+def normalize_launch(launch):
+    """(G, L) | ((gx, gy), (lx, ly)) -> ((gx, gy), (lx, ly))."""
+    if launch is None:
+        return None
+    g, l = launch
+    g = (g, 1) if isinstance(g, int) else tuple(g)
+    l = (l, 1) if isinstance(l, int) else tuple(l)
+    if min(g + l) < 1:
+        raise ValueError("launch parameters must be positive")
+    return (g[0], g[1]), (l[0], l[1])
+
+
+# ----------------------------------------------------- syntactic analyses
+
+def _is_new(name):
+    return name in NEW_SPACE
+
+
+def acc_roots(a: Phrase, alias: Dict[str, Set[str]]) -> Set[str]:
+    if isinstance(a, Var):
+        return alias.get(a.name, {a.name})
+    if isinstance(a, Proj) and isinstance(a.target, Var):
+        return {a.target.name}
+    u = unapply(a)
+    if u is None or not u[2]:
+        return set()
+    return acc_roots(u[2][0], alias)
+
+
+def exp_names(e: Phrase) -> Set[str]:
+    out = set()
+    stack = [e]
+    while stack:
+        q = stack.pop()
+        if isinstance(q, Var):
+            out.add(q.name)
+        elif isinstance(q, Lam):
+            stack.append(q.body)
+        else:
+            u = unapply(q)
+            if u is not None:
+                stack.extend(u[2])
+            elif isinstance(q, PairP):
+                stack.extend([q.fst, q.snd])
+            elif isinstance(q, Proj):
+                stack.append(q.target)
+    return out
+
+
+def rw_sets(c: Phrase, alias=None) -> Tuple[Set[str], Set[str]]:
+    """Buffer names read / written anywhere inside command c."""
+    alias = dict(alias or {})
+    R: Set[str] = set()
+    W: Set[str] = set()
+
+    def walk(q):
+        u = unapply(q)
+        if u is None:
+            return
+        name, targs, args = u
+        if name == ";":
+            walk(args[0].fst)
+            walk(args[0].snd)
+        elif name == ":=":
+            W.update(acc_roots(args[0].fst, alias))
+            R.update(exp_names(args[0].snd))
+            R.update(_acc_index_names(args[0].fst))
+        elif _is_new(name) or name == "for":
+            walk(args[0].body)
+        elif name in PARFOR_FAMILY:
+            a, f = args
+            alias[f.body.binder] = acc_roots(a, alias)
+            walk(f.body.body)
+        elif name == "reduceILocal":
+            f, init, src, k = args
+            R.update(exp_names(init) | exp_names(src))
+            walk(f.body.body.body)
+            walk(k.body)
+
+    walk(c)
+    return R, W
+
+
+def _binders(p: Phrase) -> Set[str]:
+    return {q.binder for q in subtree_iter(p) if isinstance(q, Lam)}
+
+
+def _acc_index_names(a):
+    out = set()
+    u = unapply(a)
+    while u is not None and u[2]:
+        if u[0] == "idxAcc":
+            out |= exp_names(u[2][1])
+        u = unapply(u[2][0])
+    return out
+
+
+def contains_prim(p: Phrase, names) -> bool:
+    stack = [p]
+    while stack:
+        q = stack.pop()
+        if isinstance(q, Prim):
+            if q.name in names:
+                return True
+        elif isinstance(q, Lam):
+            stack.append(q.body)
+        else:
+            u = unapply(q)
+            if u is not None:
+                stack.append(Prim(u[0]))
+                stack.extend(u[2])
+            elif isinstance(q, PairP):
+                stack.extend([q.fst, q.snd])
+            elif isinstance(q, Proj):
+                stack.append(q.target)
+    return False
+
+
+# ---------------------------------------------------------------- planner
+
+class BarrierPlanner:
+    """Work-group barrier placement at uniform program points.
+
+    State = (buffers read, buffers written) by other threads since the last
+    barrier.  A unit that reads a pending write (RAW), writes a pending read
+    (WAR) or rewrites a pending write (WAW) gets a barrier before it.
+    Sequential loops are analysed twice so loop-carried hazards place a
+    barrier inside the body (the reference's insert_barriers,
+    SRC/opencl.py:209-244, handles only the straight-line RAW case)."""
+
+    def __init__(self, shared, skip=()):
+        self.shared = shared
+        self.skip = set(skip)
+        self.before: Set[int] = set()
+
+    def run(self, c: Phrase, loop: bool = False, alias=None):
+        st = self.visit(c, (frozenset(), frozenset()), dict(alias or {}))
+        if loop:  # the region repeats: find loop-carried hazards
+            self.visit(c, st, dict(alias or {}))
+        return self.before
+
+    def visit(self, c, st, alias):
+        u = unapply(c)
+        if u is None or id(c) in self.skip:
+            return st
+        name, targs, args = u
+        if name == ";":
+            st = self.visit(args[0].fst, st, alias)
+            return self.visit(args[0].snd, st, alias)
+        if _is_new(name):
+            return self.visit(args[0].body, st, alias)
+        if name == "barrier":
+            return (frozenset(), frozenset())
+        if name == "skip":
+            return st
+        uniform_loop = name == "for" or (name in PARFOR_FAMILY and LOOP_LEVEL[name][0] == "workgroup")
+        if uniform_loop:
+            if name == "for":
+                body = args[0].body
+            else:
+                body = args[1].body.body
+                alias = {**alias, args[1].body.binder: acc_roots(args[0], alias)}
+            s1 = self.visit(body, st, alias)
+            s2 = self.visit(body, s1, alias)
+            return s2
+        if name == "reduceILocal":
+            f, init, src, k = args
+            R = {n for n in exp_names(init) | exp_names(src) if self.shared(n)}
+            self._hazard(c, st, R, set())
+            # block_combine's internal barriers fence every earlier access
+            return self.visit(k.body, (frozenset(), frozenset()), alias)
+        R, W = rw_sets(c, alias)
+        R = {n for n in R if self.shared(n)}
+        W = {n for n in W if self.shared(n)}
+        st = self._hazard(c, st, R, W)
+        return (st[0] | R, st[1] | W)
+
+    def _hazard(self, c, st, R, W):
+        pr, pw = st
+        if (R & pw) or (W & pr) or (W & pw):
+            self.before.add(id(c))
+            return (frozenset(), frozenset())
+        return st
+
+
+# ------------------------------------------------------------------ emitter
+
+class KernelEmitter:
+    """Emits the body of one kernel (a grid phase and/or tail phases)."""
+
+    def __init__(self, prog: "ProgramEmitter", kname: str):
+        self.prog = prog
+        self.kname = kname
+        self.types = prog.types
+        self.scalar = prog.scalar
+        self.launch = prog.launch
+        self.sigma = prog.sigma
+        self.slices: Dict[str, int] = {}
+        self.reset()
+
+    def reset(self):
+        self.lines: List[str] = []
+        self.ind = 1
+        self.env: Dict[str, object] = dict(self.prog.base_env)
+        self.loops: List[Loop] = []
+        self.R: Dict[str, Optional[int]] = {}
+        self.records: Dict[str, List] = {}
+        self.recording = False
+        self.smem = 0
+        self.barriers: Set[int] = set()
+        self.single_thread = False
+        self.used_scratch: Set[str] = set()
+        self._k = 0
+        self.counter = False
+        self.uses_gid = False
+        self.uniform_decl: Dict[str, bool] = {}
+        self.hoisted: Dict[int, Buffer] = {}
+        self.hoisted_writes: Set[int] = set()
+
+    # ---------------------------------------------------------- helpers
+    def fresh(self, base: str) -> str:
+        self._k += 1
+        base = "".join(ch if ch.isalnum() or ch == "_" else "_" for ch in base) or "v"
+        return f"{base}_{self._k}"
+
+    def line(self, s: str):
+        self.lines.append("  " * self.ind + s)
+
+    def open(self, head: str):
+        self.line(head + " {")
+        self.ind += 1
+
+    def close(self):
+        self.ind -= 1
+        self.line("}")
+
+    def nat_int(self, n: Nat) -> Optional[int]:
+        c = n.const
+        if c is not None:
+            return c
+        if self.sigma is not None:
+            return n.evaluate(self.sigma)
+        return None
+
+    def nat_ix(self, n: Nat) -> Ix:
+        v = self.nat_int(n)
+        if v is not None:
+            return ix(v)
+        out = Ix()
+        for mono, c in n.terms:
+            t = ix(c)
+            for name in mono:
+                t = t * ix(name)
+            out = out + t
+        return out
+
+    def r(self, e: Ix) -> str:
+        return render(e, self.R)
+
+    @property
+    def per_thread(self) -> bool:
+        return self.single_thread or any(lp.level in ("global", "local", "lin", "fold", "lambda")
+                                         for lp in self.loops)
+
+    @property
+    def in_workgroup(self) -> bool:
+        return any(lp.level == "workgroup" for lp in self.loops)
+
+    def lit(self, v) -> str:
+        if self.scalar == "float":
+            f = float(v)
+            s = repr(f)
+            if "inf" in s or "nan" in s:
+                raise CudaError(f"non-finite literal {v}")
+            return f"({s}f)" if f < 0 else f"{s}f"
+        return f"({int(v)}LL)" if int(v) < 0 else f"{int(v)}LL"
+
+    # ---------------------------------------------------- access paths
+    def fold(self, buf: Buffer, steps: List[Step]) -> Ref:
+        dims, elem = split_array(buf.dtype)
+        steps = [("i", p) for p in buf.prefix] + list(steps)
+        k = len(dims)
+        if len(steps) < k or any(t != "i" for t, _ in steps[:k]):
+            raise CudaError(f"partial or malformed access to {buf.key}")
+        idxs = [s for _, s in steps[:k]]
+        if self.recording and buf.space == "private":
+            self.records.setdefault(buf.key, []).append((idxs, list(self.loops)))
+        idxs, dims = idxs[buf.sliced:], dims[buf.sliced:]
+        flat = None
+        if dims:
+            flat = Ix()
+            for d, i in zip(dims, idxs):
+                flat = flat * self.nat_ix(d) + i
+            base = f"{buf.cname}[{self.r(flat)}]"
+        else:
+            base = buf.cname if buf.space == "private" else f"{buf.cname}[0]"
+        suffix = ""
+        t = elem
+        for tag, s in steps[k:]:
+            if tag == "f":
+                if not isinstance(t, Pair):
+                    raise CudaError("field step on a non-pair")
+                suffix += f".x{s}"
+                t = t.fst if s == 1 else t.snd
+            elif isinstance(t, Vector):
+                suffix += f".v[{self.r(s)}]"
+                t = Num()
+            elif isinstance(t, Array):
+                suffix += f"[{self.r(s)}]"
+                t = t.elem
+            else:
+                raise CudaError(f"index step into scalar of {buf.key}")
+        return Ref(buf, flat, suffix, base + suffix)
+
+    def binding(self, name: str):
+        if name not in self.env:
+            raise CudaError(f"unbound identifier in kernel: {name}")
+        return self.env[name]
+
+    def index(self, p: Phrase) -> Ix:
+        if isinstance(p, Lit):
+            return ix(int(p.value))
+        if isinstance(p, Var):
+            b = self.binding(p.name)
+            if isinstance(b, Val) and b.ixv is not None:
+                return b.ixv
+        raise CudaError(f"index expression is not a loop index or literal: {p!r}")
+
+    def val_path(self, v: Val, steps) -> str:
+        if v.ixv is not None:
+            if steps:
+                raise CudaError("path into an index value")
+            return self.r(v.ixv)
+        text, t = v.text, v.dtype
+        for tag, s in steps:
+            if tag == "f":
+                text += f".x{s}"
+                t = t.fst if s == 1 else t.snd
+            elif isinstance(t, Vector):
+                text += f".v[{self.r(s)}]"
+                t = Num()
+            else:
+                raise CudaError("index step into a value")
+        return text
+
+    def resolve(self, p: Phrase, steps: List[Step]):
+        """Read p at path steps: a Ref (buffer-rooted) or C text."""
+        if isinstance(p, Proj) and p.index == 2 and isinstance(p.target, Var):
+            p = p.target
+        if isinstance(p, Var):
+            b = self.binding(p.name)
+            if isinstance(b, Buffer):
+                return self.fold(b, steps)
+            if isinstance(b, Val):
+                return self.val_path(b, steps)
+            raise CudaError(f"{p.name} is not readable here")
+        if isinstance(p, Lit):
+            if steps or not isinstance(p.dtype, Vector):
+                return self.lit(p.value)
+            return f"dpia::splat<{self.scalar}, {p.dtype.width}>({self.lit(p.value)})"
+        u = unapply(p)
+        if u is None:
+            raise CudaError(f"not an expression: {p!r}")
+        name, targs, args = u
+        R = self.R
+        if name in ("+", "-", "*", "/") and len(args) == 1:
+            return f"({self.exp(args[0].fst, steps)} {name} {self.exp(args[0].snd, steps)})"
+        if name == "negate":
+            return f"(-{self.exp(args[0], steps)})"
+        if name == "abs":
+            return f"dpia::abs_({self.exp(args[0], steps)})"
+        if name == "zip":
+            (t1, i), (t2, k), rest = steps[0], steps[1], steps[2:]
+            return self.resolve(args[k - 1], [("i", i)] + rest)
+        if name == "split":
+            n = self.nat_ix(targs[0])
+            (_, i), (_, j), rest = steps[0], steps[1], steps[2:]
+            return self.resolve(args[0], [("i", i * n + j)] + rest)
+        if name == "join":
+            m = self.nat_int(targs[1])
+            (_, k), rest = steps[0], steps[1:]
+            if m is None:
+                raise CudaError("join with a symbolic row size needs specialisation")
+            return self.resolve(args[0], [("i", div(k, m, R)), ("i", mod(k, m, R))] + rest)
+        if name == "transpose":
+            (_, j), (_, i), rest = steps[0], steps[1], steps[2:]
+            return self.resolve(args[0], [("i", i), ("i", j)] + rest)
+        if name == "pair":
+            (_, k), rest = steps[0], steps[1:]
+            return self.resolve(args[k - 1], rest)
+        if name in ("fst", "snd"):
+            return self.resolve(args[0], [("f", 1 if name == "fst" else 2)] + steps)
+        if name == "idx":
+            return self.resolve(args[0], [("i", self.index(args[1]))] + steps)
+        if name.startswith("asVector") and "Acc" not in name:
+            w = int(name[len("asVector"):])
+            (_, i) = steps[0]
+            ref = self.resolve(args[0], [("i", i * w)])
+            aligned = isinstance(ref, Ref) and ref.flat is not None and not ref.suffix \
+                and all(c % w == 0 for _, c in ref.flat.terms)
+            if len(steps) >= 2:
+                (_, lane), rest = steps[1], steps[2:]
+                if aligned and not rest:
+                    # whole-vector load + lane select: redundant loads of the
+                    # same vector CSE into one LDG.128/LDS.128
+                    return (f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, "
+                            f"{self.r(ref.flat)}).v[{self.r(lane)}]")
+                return self.resolve(args[0], [("i", i * w + lane)] + rest)
+            if aligned:
+                return f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, {self.r(ref.flat)})"
+            lanes = ", ".join(self.exp(args[0], [("i", i * w + k)]) for k in range(w))
+            return f"dpia::vec<{self.scalar}, {w}>{{{{{lanes}}}}}"
+        if name.startswith("asScalar") and "Acc" not in name:
+            w = int(name[len("asScalar"):])
+            (_, k), rest = steps[0], steps[1:]
+            return self.resolve(args[0], [("i", div(k, w, R)), ("i", mod(k, w, R))] + rest)
+        raise CudaError(f"no expression clause for {name!r}")
+
+    def exp(self, p: Phrase, steps: List[Step]) -> str:
+        r = self.resolve(p, steps)
+        return r.text if isinstance(r, Ref) else r
+
+    def acc(self, p: Phrase, steps: List[Step]) -> Union[Ref, VStore]:
+        if isinstance(p, Proj) and p.index == 1 and isinstance(p.target, Var):
+            p = p.target
+        if isinstance(p, Var):
+            b = self.binding(p.name)
+            if isinstance(b, Buffer):
+                if b.space == "in":
+                    raise CudaError(f"write to input {b.key}")
+                return self.fold(b, steps)
+            if isinstance(b, Alias):
+                return self.acc(b.acc, [("i", b.i)] + steps)
+            raise CudaError(f"{p.name} is not an acceptor")
+        u = unapply(p)
+        if u is None:
+            raise CudaError(f"not an acceptor: {p!r}")
+        name, targs, args = u
+        R = self.R
+        if name == "idxAcc":
+            return self.acc(args[0], [("i", self.index(args[1]))] + steps)
+        if name == "splitAcc":
+            n = self.nat_int(targs[0])
+            if n is None:
+                raise CudaError("splitAcc with a symbolic chunk size needs specialisation")
+            (_, k), rest = steps[0], steps[1:]
+            return self.acc(args[0], [("i", div(k, n, R)), ("i", mod(k, n, R))] + rest)
+        if name == "joinAcc":
+            m = self.nat_ix(targs[1])
+            (_, i), (_, j), rest = steps[0], steps[1], steps[2:]
+            return self.acc(args[0], [("i", i * m + j)] + rest)
+        if name == "transposeAcc":
+            (_, i), (_, j), rest = steps[0], steps[1], steps[2:]
+            return self.acc(args[0], [("i", j), ("i", i)] + rest)
+        if name in ("pairAcc1", "pairAcc2"):
+            return self.acc(args[0], [("f", int(name[-1]))] + steps)
+        if name in ("zipAcc1", "zipAcc2"):
+            (_, i), rest = steps[0], steps[1:]
+            return self.acc(args[0], [("i", i), ("f", int(name[-1]))] + rest)
+        if name.startswith("asVectorAcc"):
+            w = int(name[len("asVectorAcc"):])
+            (_, k), rest = steps[0], steps[1:]
+            return self.acc(args[0], [("i", div(k, w, R)), ("i", mod(k, w, R))] + rest)
+        if name.startswith("asScalarAcc"):
+            w = int(name[len("asScalarAcc"):])
+            (_, i) = steps[0]
+            if len(steps) >= 2:
+                (_, lane), rest = steps[1], steps[2:]
+                return self.acc(args[0], [("i", i * w + lane)] + rest)
+            ref = self.acc(args[0], [("i", i * w)])
+            if isinstance(ref, Ref) and ref.flat is not None and not ref.suffix \
+                    and all(c % w == 0 for _, c in ref.flat.terms):
+                return VStore(ref, w)
+            raise NeedLanes()
+        raise CudaError(f"no acceptor clause for {name!r}")
+
+    # ------------------------------------------------------- assignment
+    def assign(self, d: DataType, a: Phrase, e: Phrase, steps=()):
+        steps = list(steps)
+        if isinstance(d, Pair):
+            self.assign(d.fst, a, e, steps + [("f", 1)])
+            self.assign(d.snd, a, e, steps + [("f", 2)])
+            return
+        if isinstance(d, Array):
+            raise CudaError("assignment at array type (expected generalised assignment)")
+        if isinstance(d, Vector):
+            try:
+                target = self.acc(a, steps)
+            except NeedLanes:
+                for k in range(d.width):
+                    self.assign(Num(), a, e, steps + [("i", ix(k))])
+                return
+            rhs = self.exp(e, steps)
+        else:
+            target = self.acc(a, steps)
+            rhs = self.exp(e, steps)
+        buf = target.ref.buf if isinstance(target, VStore) else target.buf
+        if isinstance(target, VStore):
+            stmt = (f"dpia::vstore<{self.scalar}, {target.width}>({buf.cname}, "
+                    f"{self.r(target.ref.flat)}, {rhs});")
+        else:
+            stmt = f"{target.text} = {rhs};"
+        if buf.space != "private" and not self.per_thread:
+            stmt = f"if (dpia_tid == 0) {stmt}"
+        self.line(stmt)
+
+    # --------------------------------------------------------- commands
+    def comm(self, p: Phrase):
+        if id(p) in self.barriers and not self.per_thread:
+            self.line("__syncthreads();")
+        u = unapply(p)
+        if u is None:
+            raise CudaError(f"not a command: {p!r}")
+        name, targs, args = u
+        if name == "skip":
+            return
+        if name == "barrier":
+            if not self.per_thread:
+                self.line("__syncthreads();")
+            return
+        if name == ";":
+            self.comm(args[0].fst)
+            self.comm(args[0].snd)
+            return
+        if name == ":=":
+            self.assign(targs[0], args[0].fst, args[0].snd)
+            return
+        if _is_new(name):
+            self.new(name, targs[0], args[0], p)
+            return
+        if name == "for":
+            f = args[0]
+            self.loop("seq", 0, targs[0], f.binder, lambda: self.comm(f.body))
+            return
+        if name in PARFOR_FAMILY:
+            self.parfor(name, targs, args)
+            return
+        if name == "reduceILocal":
+            self.combine(targs, args)
+            return
+        raise CudaError(f"no command clause for {name!r}")
+
+    def _declare_local(self, binder: str, d: DataType) -> Buffer:
+        lp = [lp for lp in self.loops if lp.level in ("local", "lin")]
+        full = d
+        for lp_ in reversed(lp):
+            full = Array(lp_.trip_nat, full)
+        cname = self.fresh(binder)
+        buf = Buffer(binder, cname, "local", full, [ix(lp_.var) for lp_ in lp])
+        n = self._elements(full)
+        if n is None:
+            raise CudaError(f"local buffer {binder} needs a constant size (specialise sizes)")
+        off = self.alloc_smem(n * self._elem_bytes(split_array(full)[1]))
+        ct = self.types.c_elem(split_array(full)[1])
+        self.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
+        return buf
+
+    def new(self, prim: str, d: DataType, f: Lam, node: Phrase = None):
+        if node is not None and id(node) in self.hoisted:
+            old = self.env.get(f.binder)
+            self.env[f.binder] = self.hoisted[id(node)]
+            self.comm(unapply(f.body)[2][0].snd)   # the staging already ran
+            if old is None:
+                del self.env[f.binder]
+            else:
+                self.env[f.binder] = old
+            return
+        space = NEW_SPACE[prim] or "private"
+        cname = self.fresh(f.binder)
+        if space == "private":
+            sl = self.slices.get(f.binder, 0)
+            buf = Buffer(f.binder, cname, "private", d, [], sl)
+            dims, elem = split_array(d)
+            dims = dims[sl:]
+            n = 1
+            for x in dims:
+                v = self.nat_int(x)
+                if v is None:
+                    raise CudaError(f"private buffer {f.binder} needs constant sizes")
+                n *= v
+            ct = self.types.c_elem(elem)
+            self.line(f"{ct} {cname}" + (f"[{n}];" if dims else ";"))
+            if self.prog.init_new:
+                self._zero_private(buf, elem, n if dims else None)
+        elif space == "local":
+            buf = self._declare_local(f.binder, d)
+        else:
+            lp = [lp for lp in self.loops if lp.level in ("global", "workgroup", "local", "lin", "fold")]
+            full = d
+            for lp_ in reversed(lp):
+                full = Array(lp_.trip_nat, full)
+            buf = Buffer(f.binder, cname, "global", full, [ix(lp_.var) for lp_ in lp])
+            self.prog.add_scratch(self, buf)
+        old = self.env.get(f.binder)
+        self.env[f.binder] = buf
+        self.comm(f.body)
+        if old is None:
+            del self.env[f.binder]
+        else:
+            self.env[f.binder] = old
+
+    def _zero_private(self, buf, elem, n):
+        zero = self.lit(0)
+        if isinstance(elem, Vector):
+            zero = f"dpia::splat<{self.scalar}, {elem.width}>({zero})"
+        if isinstance(elem, Pair):
+            return
+        if n is None:
+            self.line(f"{buf.cname} = {zero};")
+        else:
+            self.line(f"#pragma unroll\n" + "  " * self.ind +
+                      f"for (int z = 0; z < {n}; ++z) {buf.cname}[z] = {zero};")
+
+    def _elements(self, d: DataType) -> Optional[int]:
+        n = 1
+        for x in split_array(d)[0]:
+            v = self.nat_int(x)
+            if v is None:
+                return None
+            n *= v
+        return n
+
+    def _elem_bytes(self, d: DataType) -> int:
+        s = 4 if self.scalar == "float" else 8
+        if isinstance(d, Num):
+            return s
+        if isinstance(d, Idx):
+            return 8
+        if isinstance(d, Vector):
+            return s * d.width
+        if isinstance(d, Pair):
+            return 2 * max(self._tree_bytes(d.fst), self._tree_bytes(d.snd))
+        raise CudaError(f"no size for {d}")
+
+    def _tree_bytes(self, d):
+        if isinstance(d, Array):
+            n = d.size.const or 1
+            return n * self._tree_bytes(d.elem)
+        return self._elem_bytes(d)
+
+    def alloc_smem(self, nbytes: int) -> int:
+        off = (self.smem + 15) // 16 * 16
+        self.smem = off + nbytes
+        return off
+
+    # ------------------------------------------------------------ loops
+    def _level_of(self, prim: str) -> Tuple[str, int]:
+        level, dim = LOOP_LEVEL[prim]
+        if level == "plain":
+            if self.per_thread:
+                return "seq", 0
+            if self.in_workgroup or self.prog.in_tail:
+                return "lin", 0
+            return "global", 0
+        return level, dim
+
+    def _geometry(self, level: str, dim: int):
+        """(start C text, stride C text, stride int or None)."""
+        L = self.launch
+        if level == "seq":
+            return "0", "1", 1
+        if level == "workgroup":
+            ax = "xy"[dim]
+            g = L[0][dim] if L else None
+            return f"(int)blockIdx.{ax}", f"(int)gridDim.{ax}", g
+        if level == "local":
+            ax = "xy"[dim]
+            b = L[1][dim] if L else None
+            return f"(int)threadIdx.{ax}", f"(int)blockDim.{ax}", b
+        if level in ("lin", "fold"):
+            b = L[1][0] * L[1][1] if L else None
+            return "dpia_tid", "dpia_nthreads", b
+        if level == "global":
+            self.uses_gid = True
+            g = L[0][0] * L[0][1] * L[1][0] * L[1][1] if L else None
+            return "dpia_gid", "dpia_gsize", g
+        raise CudaError(level)
+
+    def loop(self, level: str, dim: int, n: Nat, binder: str, body, bind=None):
+        trip = self.nat_int(n)
+        start, stride, S = self._geometry(level, dim)
+        v = self.fresh(binder)
+        wide = trip is None or trip > IX.INT32_MAX
+        ctype = "long long" if wide else "int"
+        self.R[v] = trip
+        single = trip is not None and S is not None and trip <= S
+        if level == "local" and self.launch and trip is not None and S is not None:
+            single = trip <= S
+        lp = Loop(level, dim, v, trip, n, single)
+        bound = str(trip) if trip is not None else f"({self.r(self.nat_ix(n))})"
+        if single and level != "seq":
+            if trip == S:
+                self.open("")
+            else:
+                self.open(f"if ({start} < {trip})")
+            self.line(f"const {ctype} {v} = {start};")
+        elif level == "seq" and trip == 1:
+            self.open("")
+            self.line(f"const int {v} = 0;")
+        else:
+            if level == "seq" and trip is not None and trip <= UNROLL_LIMIT and self._small_body(body):
+                self.line("#pragma unroll")
+            self.open(f"for ({ctype} {v} = {start}; {v} < {bound}; {v} += {stride})")
+        self.loops.append(lp)
+        old = {}
+        names = [binder] + ([bind[0]] if bind else [])
+        for nm in names:
+            old[nm] = self.env.get(nm)
+        self.env[binder] = Val(Idx(n), ixv=ix(v))
+        if bind:
+            self.env[bind[0]] = bind[1](ix(v))
+        body()
+        for nm, ov in old.items():
+            if ov is None:
+                self.env.pop(nm, None)
+            else:
+                self.env[nm] = ov
+        self.loops.pop()
+        self.close()
+
+    def _small_body(self, body) -> bool:
+        return True
+
+    def parfor(self, prim: str, targs, args):
+        n, d = targs
+        a, f = args
+        if not (isinstance(f, Lam) and isinstance(f.body, Lam)):
+            raise CudaError("parfor body must be a two-argument lambda")
+        level, dim = self._level_of(prim)
+        self.lint(prim, level, dim)
+        ivar, ovar, body = f.binder, f.body.binder, f.body.body
+        entering_wg = level == "workgroup"
+        if entering_wg and not self.per_thread:
+            binders = _binders(body) | {ivar, ovar}
+            for node, d0, fl, c1 in self.invariant_stagings(body, binders):
+                buf = self._declare_local(fl.binder, d0)
+                self.env[fl.binder] = buf
+                # block-uniform context (every thread of the work-group)
+                self.loops.append(Loop("workgroup", dim, "", 1, nat(1), True))
+                self.comm(c1)
+                self.loops.pop()
+                self.line("__syncthreads();")
+                del self.env[fl.binder]
+                self.hoisted[id(node)] = buf
+                self.hoisted_writes.add(id(c1))
+
+        def emit_body():
+            if entering_wg:
+                self.plan_uniform(body, loop=True, alias={ovar: acc_roots(a, {})})
+            self.comm(body)
+
+        self.loop(level, dim, n, ivar, emit_body, bind=(ovar, lambda i: Alias(a, i)))
+
+    def lint(self, prim, level, dim):
+        enclosing = [(lp.level, lp.dim) for lp in self.loops if lp.level not in ("seq",)]
+        lv = [e[0] for e in enclosing]
+        if level == "workgroup":
+            if "local" in lv or "lin" in lv or "fold" in lv or "global" in lv:
+                raise CudaError(f"{prim}: work-group loop nested inside a work-item loop")
+            if ("workgroup", dim) in enclosing:
+                raise CudaError(f"{prim}: nested work-group loops over the same dimension")
+        if level == "global" and enclosing:
+            raise CudaError(f"{prim}: global loop nested inside another parallel loop")
+        if level == "local":
+            if ("local", dim) in enclosing:
+                raise CudaError(f"{prim}: nested work-item loops over the same dimension")
+            if "global" in lv or "fold" in lv or "lin" in lv:
+                raise CudaError(f"{prim}: work-item loop nested inside a per-item loop")
+            if "workgroup" not in lv and not self.prog.in_tail:
+                raise CudaError(f"{prim}: work-item loop with no enclosing work-group loop")
+
+    def plan_uniform(self, c: Phrase, loop: bool = False, alias=None):
+        planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes)
+        self.barriers |= planner.run(c, loop, alias)
+
+    # ---------------------------------------------- loop-invariant staging
+    def invariant_stagings(self, body: Phrase, inner_binders: Set[str]):
+        """newLocal buffers at the top of a work-group loop body whose
+        initialising command reads nothing bound inside the loop: staged
+        once per block before the loop instead of once per iteration."""
+        found = []
+
+        def walk(q):
+            u = unapply(q)
+            if u is None:
+                return
+            name, targs, args = u
+            if name == ";":
+                walk(args[0].fst)
+                walk(args[0].snd)
+            elif _is_new(name) and isinstance(args[0], Lam):
+                f = args[0]
+                inner = unapply(f.body)
+                if name == "newLocal" and inner is not None and inner[0] == ";":
+                    c1, c2 = inner[2][0].fst, inner[2][0].snd
+                    R1, W1 = rw_sets(c1)
+                    _, W2 = rw_sets(c2)
+                    free = free_vars(c1) - {f.binder}
+                    if W1 == {f.binder} and f.binder not in W2 and not (free & inner_binders) \
+                            and all(nm in self.env for nm in free):
+                        found.append((q, targs[0], f, c1))
+                        return
+                walk(f.body)
+
+        walk(body)
+        return found
+
+    # ---------------------------------------------------------- combine
+    def combine(self, targs, args):
+        n, d = targs
+        f, init, src, k = args
+        if self.per_thread:
+            raise CudaError("reduceLocal must be at work-group level (not inside a work-item loop)")
+        if not isinstance(d, (Num, Vector)):
+            raise CudaError(f"reduceLocal combines num or vec values, not {d}")
+        if self.launch and (self.launch[1][0] * self.launch[1][1]) % 32:
+            raise CudaError("reduceLocal needs a work-group size that is a multiple of 32")
+        T = self.types.c_elem(d)
+        op = self.fresh("op")
+        x, y, o = f.binder, f.body.binder, f.body.body.binder
+        cx, cy, co = self.fresh("x"), self.fresh("y"), self.fresh("o")
+        saved = {nm: self.env.get(nm) for nm in (x, y, o)}
+        self.env[x] = Val(d, text=cx)
+        self.env[y] = Val(d, text=cy)
+        self.env[o] = Buffer(o, co, "private", d)
+        self.open(f"auto {op} = [&](const {T}& {cx}, const {T}& {cy}) -> {T}")
+        self.line(f"{T} {co};")
+        self.loops.append(Loop("lambda", 0, "", None, nat(1), True))
+        self.comm(f.body.body.body)
+        self.loops.pop()
+        self.line(f"return {co};")
+        self.ind -= 1
+        self.line("};")
+        for nm, ov in saved.items():
+            if ov is None:
+                self.env.pop(nm, None)
+            else:
+                self.env[nm] = ov
+        part, has = self.fresh("part"), self.fresh("has")
+        self.line(f"{T} {part}; bool {has} = false;")
+        sfx = self.fresh("e")
+
+        def fold_body():
+            self.line(f"const {T} {sfx} = {self.exp(src, [('i', ix(self.loops[-1].var))])};")
+            self.line(f"{part} = {has} ? {op}({sfx}, {part}) : {sfx}; {has} = true;")
+
+        self.loop("fold", 0, n, self.fresh("j"), fold_body)
+        off_v = self.alloc_smem(33 * self._elem_bytes(d))
+        off_h = self.alloc_smem(33)
+        tot, tot_h = self.fresh("tot"), self.fresh("tot_has")
+        self.line(f"bool {tot_h};")
+        self.line(f"const {T} {tot} = dpia::block_combine<{T}>({part}, {has}, {op}, "
+                  f"reinterpret_cast<{T}*>(dpia_smem + {off_v}), "
+                  f"reinterpret_cast<bool*>(dpia_smem + {off_h}), dpia_tid, dpia_nthreads, {tot_h});")
+        rv = self.fresh("r")
+        self.line(f"const {T} {rv} = {tot_h} ? {op}({tot}, {self.exp(init, [])}) : {self.exp(init, [])};")
+        saved_r = self.env.get(k.binder)
+        self.env[k.binder] = Val(d, text=rv)
+        self.comm(k.body)
+        if saved_r is None:
+            self.env.pop(k.binder, None)
+        else:
+            self.env[k.binder] = saved_r
+
+
+# -------------------------------------------------------------- program
+
+class ProgramEmitter:
+    def __init__(self, outputs, inputs, float_mode=True, name="KERNEL", sigma=None, launch=None,
+                 init_new=False):
+        self.outputs, self.inputs = list(outputs), list(inputs)
+        self.scalar = "float" if float_mode else "long long"
+        self.types = TypeTable(self.scalar)
+        self.name = "".join(ch if ch.isalnum() or ch == "_" else "_" for ch in name) or "KERNEL"
+        self.sigma = dict(sigma) if sigma is not None else None
+        self.launch = normalize_launch(launch)
+        self.init_new = init_new
+        self.base_env: Dict[str, object] = {}
+        self.spaces: Dict[str, str] = {}
+        for n, d in self.outputs:
+            self.base_env[n] = Buffer(n, n, "out", d)
+            self.spaces[n] = "out"
+        for n, d in self.inputs:
+            self.base_env[n] = Buffer(n, n, "in", d)
+            self.spaces[n] = "in"
+        self.scratch: List[Buffer] = []
+        self.scratch_names: Set[str] = set()
+        self.in_tail = False
+        self.size_names: Set[str] = set()
+
+    def is_shared(self, name: str) -> bool:
+        return self.spaces.get(name, "private") != "private"
+
+    def add_scratch(self, ke: KernelEmitter, buf: Buffer):
+        if buf.cname not in self.scratch_names:
+            self.scratch_names.add(buf.cname)
+            self.scratch.append(buf)
+        ke.used_scratch.add(buf.cname)
+
+    def collect_spaces(self, p: Phrase):
+        stack = [p]
+        while stack:
+            q = stack.pop()
+            u = unapply(q)
+            if u is not None:
+                if _is_new(u[0]) and u[2] and isinstance(u[2][0], Lam):
+                    self.spaces[u[2][0].binder] = NEW_SPACE[u[0]] or "private"
+                stack.extend(u[2])
+            elif isinstance(q, Lam):
+                stack.append(q.body)
+            elif isinstance(q, PairP):
+                stack.extend([q.fst, q.snd])
+            elif isinstance(q, Proj):
+                stack.append(q.target)
+
+    # ---------------------------------------------------------- phases
+    def items(self, p: Phrase, top: List):
+        u = unapply(p)
+        if u is not None and u[0] == ";" and len(u[2]) == 1:
+            return self.items(u[2][0].fst, top) + self.items(u[2][0].snd, top)
+        if u is not None and _is_new(u[0]) and len(u[2]) == 1 and isinstance(u[2][0], Lam):
+            top.append((u[0], u[1][0], u[2][0].binder))
+            return self.items(u[2][0].body, top)
+        return [p]
+
+    @staticmethod
+    def is_grid_item(c: Phrase) -> bool:
+        u = unapply(c)
+        if u is None:
+            return False
+        name = u[0]
+        if name in PARFOR_FAMILY and LOOP_LEVEL[name][0] in ("global", "workgroup", "plain"):
+            return True
+        if _is_new(name) and isinstance(u[2][0], Lam):
+            return ProgramEmitter.is_grid_item(u[2][0].body)
+        if name == ";":
+            return ProgramEmitter.is_grid_item(u[2][0].fst) or ProgramEmitter.is_grid_item(u[2][0].snd)
+        return contains_prim(c, {"parforGlobal", "parforWorkgroup", "parforWorkgroup1"})
+
+    @staticmethod
+    def is_cooperative(c: Phrase) -> bool:
+        return contains_prim(c, {"reduceILocal", "parforLocal", "parforLocal1", "parfor"})
+
+    def emit(self, p: Phrase) -> Tuple[str, CudaSignature]:
+        self.collect_spaces(p)
+        top: List = []
+        items = self.items(p, top)
+        for prim, d, binder in top:
+            self.spaces[binder] = NEW_SPACE[prim] or "private"
+        # group items into kernels: a grid item opens a kernel, the items
+        # after it (until the next grid item) form its fused tail
+        kernels: List[Tuple[Optional[Phrase], List[Phrase]]] = []
+        for it in items:
+            if self.is_grid_item(it):
+                kernels.append((it, []))
+            elif kernels:
+                kernels[-1][1].append(it)
+            else:
+                kernels.append((None, [it]))
+        # top-level buffers: place by use
+        use: Dict[str, Set[int]] = {}
+        for b_prim, d, binder in top:
+            use[binder] = {ki for ki, (g, tail) in enumerate(kernels)
+                           for it in ([g] if g is not None else []) + tail
+                           if binder in exp_names(it)}
+        top_global: List[Tuple[str, DataType]] = []
+        kernel_top: Dict[int, List[Tuple[str, str, DataType]]] = {}
+        for b_prim, d, binder in top:
+            space = NEW_SPACE[b_prim] or "private"
+            ks = use[binder]
+            if space == "global" or (space == "private" and (len(ks) > 1 or any(
+                    kernels[k][0] is not None and binder in exp_names(kernels[k][0]) for k in ks))):
+                top_global.append((binder, d))
+                self.spaces[binder] = "global"
+            elif space == "local" and len(ks) > 1:
+                # outside any work-group, local memory has no per-group
+                # meaning; a buffer shared by several phases lives in HBM
+                top_global.append((binder, d))
+                self.spaces[binder] = "global"
+            elif space == "local":
+                for k in ks:
+                    kernel_top.setdefault(k, []).append(("local", binder, d))
+            else:
+                for k in ks:
+                    kernel_top.setdefault(k, []).append(("private", binder, d))
+        for binder, d in top_global:
+            buf = Buffer(binder, "g_" + binder.replace("@", "_"), "global", d)
+            self.base_env[binder] = buf
+            self.scratch.append(buf)
+            self.scratch_names.add(buf.cname)
+
+        bodies, infos = [], []
+        for ki, (grid, tail) in enumerate(kernels):
+            text, info = self.emit_kernel(ki, grid, tail, kernel_top.get(ki, []))
+            bodies.append(text)
+            infos.append(info)
+
+        with open(HEADER_PATH) as f:
+            header = f.read()
+        size_names = sorted(self.size_names) if self.sigma is None else []
+        sig = CudaSignature(self.outputs, self.inputs,
+                            [(b.cname, b.dtype) for b in self.scratch], size_names, infos,
+                            self.scalar, self.launch, self.sigma)
+        src = ["// generated by the DPIA CUDA backend (paper_1710_08332_b200) for sm_100a",
+               header, self.types.struct_text()] + bodies
+        return "\n".join(s for s in src if s) + "\n", sig
+
+    def emit_kernel(self, ki, grid, tail, decls):
+        kname = f"{self.name}_k{ki}"
+        ke = KernelEmitter(self, kname)
+        body_lines = None
+        for attempt in ("record", "final"):
+            ke.reset()
+            ke.recording = attempt == "record"
+            self._kernel_body(ke, grid, tail, decls)
+            if attempt == "record":
+                ke.slices = self._decide_slices(ke)
+            body_lines = ke.lines
+        args: List[Tuple[str, str]] = [("out", n) for n, _ in self.outputs]
+        args += [("in", n) for n, _ in self.inputs]
+        args += [("scratch", b.cname) for b in self.scratch if b.cname in ke.used_scratch
+                 or b.key in self._kernel_names(grid, tail)]
+        sizes = []
+        if self.sigma is None:
+            sizes = sorted(self._size_vars())
+            self.size_names |= set(sizes)
+            args += [("size", s) for s in sizes]
+        if grid is not None and tail:
+            args.append(("counter", "dpia_counter"))
+        params, views = [], []
+        for kind, n in args:
+            if kind == "size":
+                params.append(f"long long {n}")
+                continue
+            if kind == "counter":
+                params.append("unsigned int *dpia_counter")
+                continue
+            ct = self.types.c_elem(split_array(self._arg_type(n))[1])
+            q = "const " if kind == "in" else ""
+            rs = " __restrict__" if kind in ("in", "out") else ""
+            if ct == self.scalar:
+                params.append(f"{q}{self.scalar} *{rs} {n}")
+            else:
+                params.append(f"{q}{self.scalar} *{rs} {n}_raw")
+                views.append(f"  {q}{ct}*{rs} {n} = reinterpret_cast<{q}{ct}*>({n}_raw);")
+        L = self.launch
+        bounds = f"__launch_bounds__({L[1][0] * L[1][1]}) " if L else ""
+        head = [f'extern "C" __global__ void {bounds}{kname}({", ".join(params)}) {{',
+                "  extern __shared__ __align__(16) unsigned char dpia_smem[];"]
+        head += views
+        if L:
+            head.append(f"  const int dpia_nthreads = {L[1][0] * L[1][1]};")
+        else:
+            head.append("  const int dpia_nthreads = (int)(blockDim.x * blockDim.y);")
+        head.append("  const int dpia_tid = (int)(threadIdx.y * blockDim.x + threadIdx.x);")
+        if ke.uses_gid:
+            wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
+            it = "long long" if wide else "int"
+            head.append(f"  const {it} dpia_gid = ({it})(blockIdx.y * gridDim.x + blockIdx.x) * "
+                        "dpia_nthreads + dpia_tid;")
+            head.append(f"  const {it} dpia_gsize = ({it})gridDim.x * gridDim.y * dpia_nthreads;")
+        text = "\n".join(head + body_lines + ["}"])
+        info = KernelInfo(kname, "launch" if grid is not None else "single", args, ke.smem,
+                          grid is not None and bool(tail))
+        return text, info
+
+    def _kernel_names(self, grid, tail):
+        names = set()
+        for it in ([grid] if grid is not None else []) + tail:
+            names |= exp_names(it)
+        return names
+
+    def _arg_type(self, n):
+        for nn, d in self.outputs + self.inputs:
+            if nn == n:
+                return d
+        for b in self.scratch:
+            if b.cname == n:
+                return b.dtype
+        raise KeyError(n)
+
+    def _size_vars(self):
+        out = set()
+        for _, d in self.outputs + self.inputs:
+            for x in split_array(d)[0]:
+                out |= set(x.free)
+        for b in self.scratch:
+            for x in split_array(b.dtype)[0]:
+                out |= set(x.free)
+        return out
+
+    def _kernel_body(self, ke: KernelEmitter, grid, tail, decls):
+        saved_env = {}
+        for space, binder, d in decls:
+            lam = Lam(binder, Prim("skip"))
+            # declare kernel-level buffers (top-level local / private)
+            if space == "local":
+                n = ke._elements(d)
+                if n is None:
+                    raise CudaError(f"local buffer {binder} needs a constant size")
+                off = ke.alloc_smem(n * ke._elem_bytes(split_array(d)[1]))
+                ct = self.types.c_elem(split_array(d)[1])
+                cname = ke.fresh(binder)
+                ke.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
+                saved_env[binder] = Buffer(binder, cname, "local", d)
+            del lam
+        ke.env.update(saved_env)
+        if grid is not None:
+            self.in_tail = False
+            if not self.is_grid_item(grid):
+                raise CudaError("internal: grid item expected")
+            ke.comm(grid)
+        if tail:
+            self.in_tail = True
+            if grid is not None:
+                ke.counter = True
+                ke.line("__shared__ bool dpia_last;")
+                ke.open("if (dpia::grid_arrive(dpia_counter, dpia_tid, &dpia_last))")
+            for space, binder, d in decls:
+                if space == "private":
+                    dims, elem = split_array(d)
+                    n = ke._elements(d)
+                    cname = ke.fresh(binder)
+                    ke.line(f"{self.types.c_elem(elem)} {cname}" + (f"[{n}];" if dims else ";"))
+                    ke.env[binder] = Buffer(binder, cname, "private", d)
+            for it in tail:
+                if self.is_cooperative(it):
+                    ke.plan_uniform(it)
+                    ke.comm(it)
+                else:
+                    ke.open("if (dpia_tid == 0)")
+                    ke.single_thread = True
+                    ke.comm(it)
+                    ke.single_thread = False
+                    ke.close()
+            if grid is not None:
+                ke.line("dpia::grid_reset(dpia_counter, dpia_tid);")
+                ke.close()
+            self.in_tail = False
+
+    def _decide_slices(self, ke: KernelEmitter) -> Dict[str, int]:
+        """Thread slicing of work-group-level private buffers (see module doc)."""
+        L = self.launch
+        if L is None:
+            return {}
+        one_d = L[1][1] == 1
+        out = {}
+        for key, recs in ke.records.items():
+            best = None
+            keys_at: List = []
+            for idxs, loops in recs:
+                m = 0
+                for j, e in enumerate(idxs):
+                    v = e.var_name()
+                    lp = next((lp for lp in loops if lp.var == v), None) if v else None
+                    if lp is None or not lp.single or lp.level not in ("local", "lin", "fold"):
+                        break
+                    if one_d and (lp.level != "local" or lp.dim == 0):
+                        kkey = ("thread", 0)
+                    elif lp.level == "local":
+                        kkey = ("local", lp.dim)
+                    else:
+                        kkey = ("lin", 0)
+                    if j < len(keys_at) and keys_at[j] != kkey:
+                        break
+                    if j == len(keys_at):
+                        keys_at.append(kkey)
+                    m += 1
+                best = m if best is None else min(best, m)
+                if best == 0:
+                    break
+            if best:
+                out[key] = best
+        return out
+
+
+# ------------------------------------------------------------------ API
+
+def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple[str, DataType]],
+              float_mode: bool = True, name: str = "KERNEL", init_new: bool = False,
+              simplify: bool = True, sigma: Optional[Dict[str, int]] = None,
+              launch=None) -> Tuple[str, CudaSignature]:
+    """Render an imperative DPIA command as CUDA C for sm_100a.
+
+    Drop-in for the reference's `emit_kernel(p, outputs, inputs, float_mode,
+    name, init_new, simplify)` (SRC/opencl.py:265-271).  Accepts the Stage II
+    phrase directly or the reference's hoisted form.  `sigma` and `launch`
+    optionally specialise sizes and the (G, L) launch geometry into the
+    source (run_kernel always does), which enables single-iteration loops,
+    thread slicing and compile-time index arithmetic."""
+    del simplify  # subscripts are always range-simplified
+    return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new).emit(p)
+
+
+def source_hash(src: str, opts: str = "") -> str:
+    return hashlib.sha256((src + "\0" + opts).encode()).hexdigest()[:24]

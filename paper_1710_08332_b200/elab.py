@@ -23,7 +23,7 @@ from .reader import (ParseError, SExp, Token, error_at, head_of, number_of,
 from .signatures import (ARITH_OPS, MAP_FAMILY, MAPI_FAMILY, NEW_SPACE,
                          PARFOR_FAMILY, PRIMITIVES, REDUCE_FAMILY, TO_SPACE,
                          UNARY_OPS, vector_prim)
-from .sizes import nat_divide
+from .sizes import nat, nat_divide
 from .terms import (App, Lam, Lit, PairP, Phrase, Prim, Proj, TApp, TLam, Var,
                     apply_prim, fresh_name)
 
@@ -424,6 +424,10 @@ def _r_arith(el, sx) -> Typed:
 def _r_idx(el, sx) -> Typed:
     _arity(sx, 3, "(idx E I)")
     e, et = el.infer(sx[1])
+    if isinstance(et, ExpT) and isinstance(et.data, Vector):
+        # lane of a vector (extension: vectors read as arrays of lanes)
+        w = nat(et.data.width)
+        return apply_prim("idx", [w, NUM], [e, el.check(sx[2], ExpT(Idx(w)))]), ExpT(NUM)
     n, d = _arr_exp(sx, et)
     return apply_prim("idx", [n, d], [e, el.check(sx[2], ExpT(Idx(n)))]), ExpT(d)
 

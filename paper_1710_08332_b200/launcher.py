@@ -1,0 +1,149 @@
+"""Execution of emitted kernels: the CUDA replacement of the reference's
+work-item simulator.
+
+`run_kernel` has the signature and result of `simulate_kernel`
+(SRC/opencl.py:397-402): params are (name, data type, "in"|"out"|"var"),
+inputs map names to values, launch is (G, L) -- or ((Gx, Gy), (Lx, Ly)) for
+the two-dimensional hierarchy -- and the result maps every out/var parameter
+to its final value.  Instead of interpreting the phrase it emits CUDA C
+(`cuda.emit`), compiles it with NVRTC for sm_100a and launches it through
+libdpia_rt.so.  `Executable` keeps the compiled program and device buffers
+for repeated launches (benchmarks, CUDA-event timing).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import layout as LY
+from . import runtime as RT
+from .cuda.emit import CudaSignature, emit_cuda, normalize_launch
+from .dtypes import DataType
+from .terms import Phrase
+
+
+@dataclass
+class Executable:
+    src: str
+    sig: CudaSignature
+    device: int
+    float_mode: bool
+    sigma: Dict[str, int]
+    module: RT.Module = None
+    buffers: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
+    counters: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
+    _args: List = field(default_factory=list)
+
+    @property
+    def launch_geom(self):
+        return self.sig.launch
+
+    def compile(self):
+        img = RT.get_cubin(self.src)
+        self.module = RT.Module(img, self.device)
+        for k in self.sig.kernels:
+            if k.smem > 48 * 1024:
+                RT.lib().dpia_kernel_set_smem(self.module.function(k.name), k.smem)
+        return self
+
+    # ----------------------------------------------------------- buffers
+    def allocate(self):
+        fm, sg = self.float_mode, self.sigma
+        for n, d in self.sig.outputs + self.sig.inputs:
+            if n not in self.buffers:
+                self.buffers[n] = RT.DeviceBuffer(LY.nbytes(d, sg, fm), self.device)
+        for n, d in self.sig.buffers:
+            if n not in self.buffers:
+                b = RT.DeviceBuffer(LY.nbytes(d, sg, fm), self.device)
+                b.zero()
+                self.buffers[n] = b
+        for k in self.sig.kernels:
+            if k.fused_tail and k.name not in self.counters:
+                c = RT.DeviceBuffer(16, self.device)
+                c.zero()
+                self.counters[k.name] = c
+        self._args = []
+        for k in self.sig.kernels:
+            vals = []
+            for kind, n in k.args:
+                if kind in ("out", "in", "scratch"):
+                    vals.append(RT.C.c_uint64(self.buffers[n].ptr))
+                elif kind == "size":
+                    vals.append(RT.C.c_longlong(int(self.sigma[n])))
+                else:
+                    vals.append(RT.C.c_uint64(self.counters[k.name].ptr))
+            self._args.append(vals)
+        return self
+
+    def bind(self, name: str, buf: RT.DeviceBuffer):
+        """Use an externally owned device buffer for parameter `name`."""
+        self.buffers[name] = buf
+        if self._args:
+            self.allocate()
+
+    def upload(self, name: str, value, stream=None):
+        d = dict(self.sig.outputs + self.sig.inputs)[name]
+        self.buffers[name].upload(LY.to_bytes(value, d, self.sigma, self.float_mode), stream)
+
+    def download(self, name: str, stream=None) -> np.ndarray:
+        d = dict(self.sig.outputs + self.sig.inputs)[name]
+        raw = np.empty(LY.nbytes(d, self.sigma, self.float_mode), np.uint8)
+        self.buffers[name].download(raw, stream)
+        return LY.from_bytes(raw, d, self.sigma, self.float_mode)
+
+    # ------------------------------------------------------------ launch
+    def launch(self, stream: Optional[RT.Stream] = None):
+        (g, l) = self.sig.launch
+        for k, vals in zip(self.sig.kernels, self._args):
+            grid = g if k.grid == "launch" else (1, 1)
+            fn = self.module.function(k.name)
+            RT.launch(fn, self.device, grid, l, k.smem, vals, stream)
+
+    def kernel_names(self) -> List[str]:
+        return [k.name for k in self.sig.kernels]
+
+
+def _split_params(params):
+    outs = [(n, d) for n, d, mode in params if mode in ("out", "var")]
+    ins = [(n, d) for n, d, mode in params if mode == "in"]
+    return outs, ins
+
+
+def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None,
+          float_mode: bool = False, device: int = 0, name: str = "KERNEL") -> Executable:
+    """Emit + compile + allocate (no data movement)."""
+    sigma = dict(sigma or {})
+    outs, ins = _split_params(params)
+    src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name, sigma=sigma,
+                         launch=normalize_launch(launch))
+    exe = Executable(src, sig, device, float_mode, sigma)
+    return exe.compile().allocate()
+
+
+def run_kernel(p: Phrase, params: List[Tuple[str, DataType, str]], inputs: Dict[str, object],
+               launch, sigma: Optional[Dict[str, int]] = None, float_mode: bool = False,
+               device: int = 0, name: str = "KERNEL", flat: bool = False) -> Dict[str, object]:
+    """Drop-in for `simulate_kernel(p, params, inputs, launch, sigma,
+    float_mode)` (SRC/opencl.py:397): same arguments, same result mapping,
+    executed on the GPU.  flat=True returns numpy arrays of scalar leaves."""
+    normalize_launch(launch)  # ValueError for non-positive launches, like the reference
+    exe = build(p, params, launch, sigma, float_mode, device, name)
+    stream = RT.Stream(device)
+    for n, d, mode in params:
+        if mode == "in":
+            exe.upload(n, inputs[n], stream)
+        elif mode == "var" and n in inputs:
+            exe.upload(n, inputs[n], stream)
+        else:
+            exe.buffers[n].zero(stream)
+    exe.launch(stream)
+    stream.sync()
+    out = {}
+    for n, d, mode in params:
+        if mode in ("out", "var"):
+            leaves = exe.download(n, stream)
+            out[n] = leaves if flat else LY.unflatten(d, leaves, exe.sigma)
+    stream.sync()
+    return out

@@ -1,0 +1,120 @@
+"""GPU parity: every program is emitted as CUDA, compiled with NVRTC for
+sm_100a, launched through libdpia_rt.so, and compared with the oracle.
+
+* golden programs: the reference's sample/test programs and 400 programs of
+  the reference's own fuzzer, with the reference's eval_phrase result; int
+  mode is bit-exact, float within 1e-5*max(1,|want|) (the reference's bound,
+  TST/test_acceptance.py:149-150);
+* the benchmark strategies at reduced sizes, int mode bit-exact against the
+  oracle interpreter, and at full BASELINE sizes in fp32 against the float64
+  NumPy oracle with |got-want| <= 1e-4 * sum|terms|.
+"""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import blas_np
+from oracle.dpia_eval import eval_phrase, flatten_value, from_json
+from paper_1710_08332_b200 import CudaError, compile_program, run_program_cuda
+from paper_1710_08332_b200.bench_programs import (asum_config, asum_program, dot_config,
+                                                  dot_program, gemv_config, gemv_program)
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = load_golden("programs.json")
+FUZZ = [c for c in load_golden("fuzz.json") if c["reparses"]]
+
+
+def _check(case, launch):
+    prog = compile_program(case["text"])
+    inputs = {k: from_json(v) for k, v in case["inputs"].items()}
+    fm = case.get("float", False)
+    got = run_program_cuda(prog, inputs, sigma=case.get("sigma", {}), launch=launch, float_mode=fm,
+                           flat=True)
+    want = flatten_value(from_json(case["expected"]))
+    if fm:
+        assert np.allclose(got, want, rtol=1e-5, atol=1e-5), (got, want)
+    else:
+        assert [int(v) for v in got] == want
+
+
+@pytest.mark.parametrize("launch", [(1, 1), (2, 2), (2, 4), (4, 8), (3, 32)])
+@pytest.mark.parametrize("case", GOLDEN, ids=lambda c: c["name"])
+def test_golden_programs(case, launch):
+    _check(case, launch)
+
+
+@pytest.mark.parametrize("case", FUZZ, ids=lambda c: f"seed{c['seed']}")
+def test_reference_fuzz_programs(case):
+    """Kernel-legal programs (the reference simulates them) must run; the
+    others run when the CUDA backend accepts their hierarchy."""
+    for launch in ((2, 2), (3, 5)):
+        try:
+            _check(case, launch)
+        except CudaError:
+            if case["opencl_legal"]:
+                raise
+            pytest.skip("hierarchy rejected by the backend (reference rejects it too)")
+
+
+# ------------------------------------------------------------ benchmarks
+
+def _ints(n, seed):
+    return np.random.default_rng(seed).integers(-9, 10, n).tolist()
+
+
+@pytest.mark.parametrize("L,K,n,blocks", [(32, 2, 3, 3), (64, 4, 5, 2), (256, 16, 8, 8), (256, 16, 9, 4)])
+def test_dot_strategy_int_exact(L, K, n, blocks):
+    prog = compile_program(dot_program(L, K))
+    N = n * 4 * K * L
+    xs, ys = _ints(N, 1), _ints(N, 2)
+    got = run_program_cuda(prog, {"xs": xs, "ys": ys}, sigma={"n": n}, launch=(blocks, L),
+                           float_mode=False)
+    assert got == eval_phrase(prog.source.body, {"xs": xs, "ys": ys}, {"n": n})
+
+
+@pytest.mark.parametrize("L,K,n,blocks", [(32, 2, 3, 3), (128, 8, 6, 4)])
+def test_asum_strategy_int_exact(L, K, n, blocks):
+    prog = compile_program(asum_program(L, K))
+    xs = _ints(n * 4 * K * L, 3)
+    got = run_program_cuda(prog, {"xs": xs}, sigma={"n": n}, launch=(blocks, L), float_mode=False)
+    assert got == sum(abs(x) for x in xs)
+    assert got == eval_phrase(prog.source.body, {"xs": xs}, {"n": n})
+
+
+@pytest.mark.parametrize("M,N,L,blocks", [(8, 256, 32, 3), (33, 512, 64, 7), (64, 1024, 256, 64)])
+def test_gemv_strategy_int_exact(M, N, L, blocks):
+    prog = compile_program(gemv_program(M, N, L))
+    A = np.random.default_rng(4).integers(-9, 10, (M, N))
+    x = np.random.default_rng(5).integers(-9, 10, N)
+    got = run_program_cuda(prog, {"A": A.tolist(), "x": x.tolist()}, launch=(blocks, L),
+                           float_mode=False, flat=True)
+    assert [int(v) for v in got] == (A @ x).tolist()
+
+
+def test_dot_full_size_fp32():
+    cfg = dot_config()
+    N = 1 << 24
+    xs, ys = blas_np.seeded(N, 0, 0.0, 1.0), blas_np.seeded(N, 1, 0.0, 1.0)
+    got = run_program_cuda(compile_program(cfg.text), {"xs": xs, "ys": ys}, sigma=cfg.sigma,
+                           launch=cfg.launch, flat=True)
+    want, absterms = blas_np.dot(xs, ys)
+    assert blas_np.within(got[0], want, absterms), (got[0], want)
+
+
+def test_asum_full_size_fp32():
+    cfg = asum_config()
+    xs = blas_np.seeded(1 << 26, 2, -1.0, 1.0)
+    got = run_program_cuda(compile_program(cfg.text), {"xs": xs}, sigma=cfg.sigma,
+                           launch=cfg.launch, flat=True)
+    want, absterms = blas_np.asum(xs)
+    assert blas_np.within(got[0], want, absterms), (got[0], want)
+
+
+def test_gemv_full_size_fp32():
+    cfg = gemv_config()
+    A = blas_np.seeded((8192, 8192), 3, -1.0, 1.0)
+    x = blas_np.seeded(8192, 4, -1.0, 1.0)
+    got = run_program_cuda(compile_program(cfg.text), {"A": A, "x": x}, launch=cfg.launch, flat=True)
+    want, absterms = blas_np.gemv(A, x)
+    assert blas_np.within(got, want, absterms)
