@@ -44,7 +44,8 @@ from typing import Dict, List, Optional, Set, Tuple, Union
 from ..dtypes import Array, DataType, Idx, Num, Pair, Vector
 from ..signatures import LOOP_LEVEL, NEW_SPACE, PARFOR_FAMILY
 from ..sizes import Nat, nat
-from ..terms import Lam, Lit, PairP, Phrase, Prim, Proj, Var, free_vars, subtree_iter, unapply
+from ..terms import (Lam, Lit, PairP, Phrase, Prim, Proj, Var, free_vars, seq_all,
+                     subtree_iter, unapply)
 from . import index as IX
 from .ctypes_map import CudaError, TypeTable, split_array
 from .index import Ix, div, ix, mod, render
@@ -278,9 +279,10 @@ class BarrierPlanner:
     barrier inside the body (the reference's insert_barriers,
     SRC/opencl.py:209-244, handles only the straight-line RAW case)."""
 
-    def __init__(self, shared, skip=()):
+    def __init__(self, shared, skip=(), opaque=()):
         self.shared = shared
         self.skip = set(skip)
+        self.opaque = set(opaque)   # single-thread units: analysed as one leaf
         self.before: Set[int] = set()
 
     def run(self, c: Phrase, loop: bool = False, alias=None):
@@ -294,9 +296,15 @@ class BarrierPlanner:
         if u is None or id(c) in self.skip:
             return st
         name, targs, args = u
-        if name == ";":
+        if name == ";" and id(c) not in self.opaque:
             st = self.visit(args[0].fst, st, alias)
             return self.visit(args[0].snd, st, alias)
+        if id(c) in self.opaque:
+            R, W = rw_sets(c, alias)
+            R = {n for n in R if self.shared(n)}
+            W = {n for n in W if self.shared(n)}
+            st = self._hazard(c, st, R, W)
+            return (st[0] | R, st[1] | W)
         if _is_new(name):
             return self.visit(args[0].body, st, alias)
         if name == "barrier":
@@ -346,6 +354,7 @@ class KernelEmitter:
         self.launch = prog.launch
         self.sigma = prog.sigma
         self.slices: Dict[str, int] = {}
+        self.promote: Set[str] = set()
         self.reset()
 
     def reset(self):
@@ -365,6 +374,7 @@ class KernelEmitter:
         self.uses_gid = False
         self.uniform_decl: Dict[str, bool] = {}
         self.hoisted: Dict[int, Buffer] = {}
+        self.decl_depth: Dict[str, int] = {}
         self.hoisted_writes: Set[int] = set()
 
     # ---------------------------------------------------------- helpers
@@ -434,7 +444,8 @@ class KernelEmitter:
             raise CudaError(f"partial or malformed access to {buf.key}")
         idxs = [s for _, s in steps[:k]]
         if self.recording and buf.space == "private":
-            self.records.setdefault(buf.key, []).append((idxs, list(self.loops)))
+            self.records.setdefault(buf.key, []).append(
+                (idxs, list(self.loops), self.single_thread, self.decl_depth.get(buf.key, 0)))
         idxs, dims = idxs[buf.sliced:], dims[buf.sliced:]
         flat = None
         if dims:
@@ -717,7 +728,12 @@ class KernelEmitter:
             return
         space = NEW_SPACE[prim] or "private"
         cname = self.fresh(f.binder)
+        if space == "private" and f.binder in self.promote:
+            # written and read by different work-items: per-thread registers
+            # cannot hold it -- stage it in the work-group's shared memory
+            space = "local"
         if space == "private":
+            self.decl_depth[f.binder] = len(self.loops)
             sl = self.slices.get(f.binder, 0)
             buf = Buffer(f.binder, cname, "private", d, [], sl)
             dims, elem = split_array(d)
@@ -919,8 +935,8 @@ class KernelEmitter:
             if "workgroup" not in lv and not self.prog.in_tail:
                 raise CudaError(f"{prim}: work-item loop with no enclosing work-group loop")
 
-    def plan_uniform(self, c: Phrase, loop: bool = False, alias=None):
-        planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes)
+    def plan_uniform(self, c: Phrase, loop: bool = False, alias=None, opaque=()):
+        planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes, opaque)
         self.barriers |= planner.run(c, loop, alias)
 
     # ---------------------------------------------- loop-invariant staging
@@ -1164,7 +1180,9 @@ class ProgramEmitter:
             ke.recording = attempt == "record"
             self._kernel_body(ke, grid, tail, decls)
             if attempt == "record":
-                ke.slices = self._decide_slices(ke)
+                ke.slices, ke.promote = self._decide_slices(ke)
+                for key in ke.promote:
+                    self.spaces[key] = "local"
             body_lines = ke.lines
         args: List[Tuple[str, str]] = [("out", n) for n, _ in self.outputs]
         args += [("in", n) for n, _ in self.inputs]
@@ -1267,17 +1285,23 @@ class ProgramEmitter:
                 ke.line("__shared__ bool dpia_last;")
                 ke.open("if (dpia::grid_arrive(dpia_counter, dpia_tid, &dpia_last))")
             for space, binder, d in decls:
-                if space == "private":
+                if space == "private" and binder in ke.promote:
+                    ke.env[binder] = ke._declare_local(binder, d)
+                elif space == "private":
                     dims, elem = split_array(d)
                     n = ke._elements(d)
                     cname = ke.fresh(binder)
+                    ke.decl_depth[binder] = len(ke.loops)
                     ke.line(f"{self.types.c_elem(elem)} {cname}" + (f"[{n}];" if dims else ";"))
                     ke.env[binder] = Buffer(binder, cname, "private", d)
+            ke.plan_uniform(seq_all(list(tail)),
+                            opaque={id(it) for it in tail if not self.is_cooperative(it)})
             for it in tail:
                 if self.is_cooperative(it):
-                    ke.plan_uniform(it)
                     ke.comm(it)
                 else:
+                    if id(it) in ke.barriers:
+                        ke.line("__syncthreads();")
                     ke.open("if (dpia_tid == 0)")
                     ke.single_thread = True
                     ke.comm(it)
@@ -1291,14 +1315,19 @@ class ProgramEmitter:
     def _decide_slices(self, ke: KernelEmitter) -> Dict[str, int]:
         """Thread slicing of work-group-level private buffers (see module doc)."""
         L = self.launch
-        if L is None:
-            return {}
-        one_d = L[1][1] == 1
-        out = {}
+        one_d = L is not None and L[1][1] == 1
+        out, promote = {}, set()
         for key, recs in ke.records.items():
             best = None
             keys_at: List = []
-            for idxs, loops in recs:
+            distributed = any(st or any(lp.level in ("local", "lin", "fold", "global")
+                                        for lp in loops[depth:])
+                              for _, loops, st, depth in recs)
+            if L is None:
+                if distributed:
+                    promote.add(key)
+                continue
+            for idxs, loops, st, depth in recs:
                 m = 0
                 for j, e in enumerate(idxs):
                     v = e.var_name()
@@ -1321,7 +1350,9 @@ class ProgramEmitter:
                     break
             if best:
                 out[key] = best
-        return out
+            elif distributed:
+                promote.add(key)
+        return out, promote
 
 
 # ------------------------------------------------------------------ API

@@ -204,6 +204,11 @@ class Module:
 
 # --------------------------------------------------------------- memory
 
+def _sh(stream):
+    """Raw CUstream handle of a Stream (or None for the legacy stream)."""
+    return stream.handle if isinstance(stream, Stream) else stream
+
+
 class DeviceBuffer:
     def __init__(self, nbytes: int, device: int = 0):
         init(device)
@@ -228,16 +233,16 @@ class DeviceBuffer:
         a = np.ascontiguousarray(host_array)
         assert a.nbytes <= self.nbytes, (a.nbytes, self.nbytes)
         lib().dpia_memcpy_htod(self.device, self.ptr, a.ctypes.data_as(ctypes.c_void_p), a.nbytes,
-                               stream)
+                               _sh(stream))
 
     def download(self, out, stream=None):
         assert out.flags["C_CONTIGUOUS"] and out.nbytes <= self.nbytes
         lib().dpia_memcpy_dtoh(self.device, out.ctypes.data_as(ctypes.c_void_p), self.ptr, out.nbytes,
-                               stream)
+                               _sh(stream))
         return out
 
     def zero(self, stream=None):
-        lib().dpia_memset(self.device, self.ptr, 0, self.nbytes, stream)
+        lib().dpia_memset(self.device, self.ptr, 0, self.nbytes, _sh(stream))
 
 
 class PinnedBuffer:
