@@ -1,0 +1,389 @@
+"""Benchmark: DPIA-emitted CUDA kernels on B200 against the HBM / FP32 roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload asum|dot|gemv|scaleout] [--no-suite]
+
+Headline workload (BASELINE.json configs[1]): asum over N = 2^26 fp32 with
+the vectorised asVector(4) + mapWorkgroup/mapLocal + reduceLocal strategy.
+A "step" is one pass of the emitted program over the resident input (all of
+its kernels, the fused work-group/grid combine included); L2 is flushed
+between steps (2x-L2 memset, outside the timed events).  Multi-GPU (torchrun,
+one process per GPU): every rank runs the full per-GPU workload on its own
+shard (weak scaling) and the partial sums are combined with an NCCL
+all-reduce inside the step; the time is the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
+from paper_1710_08332_b200 import runtime as RT  # noqa: E402
+from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
+                                                  gemv_config)
+
+METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(workload):
+    """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.samples = []
+        if self.proc is None:
+            return
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate()
+        for ln in out.splitlines():
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) == 6:
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), parts[2:]))
+                except ValueError:
+                    pass
+
+    def summary(self):
+        if not getattr(self, "samples", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for _, _, flags in self.samples for n, fl in zip(names, flags)
+                          if fl.lower() == "active"})
+        loaded = [s for s, _, _ in self.samples if s > 500] or [s for s, _, _ in self.samples]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.samples[0][1],
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ workloads
+
+def make_workload(name, device, rank=0, world=1):
+    """(config, executable, host inputs, algorithmic bytes, flops)."""
+    if name == "asum":
+        cfg = asum_config()
+        inputs = {"xs": _seeded(1 << 26, 2 + 1000 * rank, -1.0, 1.0)}
+    elif name == "dot":
+        cfg = dot_config()
+        inputs = {"xs": _seeded(1 << 24, 0 + 1000 * rank, 0.0, 1.0),
+                  "ys": _seeded(1 << 24, 1 + 1000 * rank, 0.0, 1.0)}
+    elif name == "gemv":
+        cfg = gemv_config()
+        inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
+    else:
+        raise SystemExit(f"unknown workload {name}")
+    prog = compile_program(cfg.text, name=name)
+    exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device)
+    return cfg, exe, inputs
+
+
+def _seeded(shape, seed, lo, hi):
+    return np.random.default_rng(seed).uniform(lo, hi, size=shape).astype(np.float32)
+
+
+def time_steps(exe, stream, steps, warmup, flush=True, allreduce=None):
+    dev = exe.device
+    ev = [(RT.Event(dev), RT.Event(dev)) for _ in range(steps)]
+    for _ in range(warmup):
+        if flush:
+            RT.lib().dpia_l2_flush(dev, stream.handle)
+        exe.launch(stream)
+        if allreduce:
+            allreduce(stream)
+    stream.sync()
+    return ev
+
+
+def run_timed(exe, stream, steps, flush=True, allreduce=None):
+    dev = exe.device
+    ev = [(RT.Event(dev), RT.Event(dev)) for _ in range(steps)]
+    for e0, e1 in ev:
+        if flush:
+            RT.lib().dpia_l2_flush(dev, stream.handle)
+        e0.record(stream)
+        exe.launch(stream)
+        if allreduce:
+            allreduce(stream)
+        e1.record(stream)
+    stream.sync()
+    return [e0.elapsed_ms(e1) for e0, e1 in ev]
+
+
+def e2e_measure(exe, inputs, stream, steps):
+    """Public-API path with host buffers: H2D of the step's inputs from pinned
+    memory, the kernels, D2H of the result -- all inside the timed events."""
+    from paper_1710_08332_b200 import layout as LY
+    dev = exe.device
+    pinned, h2d = {}, 0
+    for n, d in exe.sig.inputs:
+        img = LY.to_bytes(inputs[n], d, exe.sigma, True)
+        pb = RT.PinnedBuffer(img.nbytes)
+        pb.array(np.uint8, img.nbytes)[:] = img
+        pinned[n] = (pb, img.nbytes)
+        h2d += img.nbytes
+    outn, outd = exe.sig.outputs[0]
+    d2h = LY.nbytes(outd, exe.sigma, True)
+    ob = RT.PinnedBuffer(d2h)
+    times = []
+    for _ in range(steps + 1):
+        e0, e1 = RT.Event(dev), RT.Event(dev)
+        e0.record(stream)
+        for n, (pb, nb) in pinned.items():
+            RT.lib().dpia_memcpy_htod(dev, exe.buffers[n].ptr, pb.ptr, nb, stream.handle)
+        exe.launch(stream)
+        RT.lib().dpia_memcpy_dtoh(dev, ob.ptr, exe.buffers[outn].ptr, d2h, stream.handle)
+        e1.record(stream)
+        stream.sync()
+        times.append(e0.elapsed_ms(e1))
+    for pb, _ in pinned.values():
+        pb.free()
+    ob.free()
+    return statistics.mean(times[1:]), h2d, d2h
+
+
+# ------------------------------------------------------------ CPU legs
+
+def ref_lib():
+    import ctypes
+    path = os.path.join(ROOT, "oracle", "_ref", "libref_cpu.so")
+    if not os.path.exists(path):
+        return None
+    lib = ctypes.CDLL(path)
+    return lib
+
+
+def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None):
+    """Time the reference's own CPU path (its c-openmp emission of the same
+    strategy, compiled by oracle/build_ref.py) on all host threads."""
+    import ctypes
+    lib = ref_lib()
+    if lib is None:
+        return None
+    vp, ci = ctypes.c_void_p, ctypes.c_int
+    out = np.zeros(8192, np.float32)
+    if workload == "asum":
+        n = (1 << 26) // 1024
+        xs = _seeded(1 << 26, 2, -1.0, 1.0)
+        fn = lib.asum_proxy
+        fn.argtypes = [vp, vp, ci]
+        call = lambda: fn(out.ctypes.data, xs.ctypes.data, n)  # noqa: E731
+        nbytes, sample = 4 << 26, "asum proxy (sum; the reference has no abs) over 2^26 fp32, full size"
+    elif workload == "dot":
+        n = (1 << 24) // 1024
+        xs, ys = _seeded(1 << 24, 0, 0.0, 1.0), _seeded(1 << 24, 1, 0.0, 1.0)
+        fn = lib.dot
+        fn.argtypes = [vp, vp, vp, ci]
+        call = lambda: fn(out.ctypes.data, xs.ctypes.data, ys.ctypes.data, n)  # noqa: E731
+        nbytes, sample = 8 << 24, "dot over 2^24 fp32 pairs, full size"
+    elif workload == "gemv":
+        A, x = _seeded((8192, 8192), 3, -1.0, 1.0), _seeded(8192, 4, -1.0, 1.0)
+        fn = lib.gemv
+        fn.argtypes = [vp, vp, vp]
+        call = lambda: fn(out.ctypes.data, A.ctypes.data, x.ctypes.data)  # noqa: E731
+        nbytes, sample = 4 * (8192 * 8192 + 2 * 8192), "gemv 8192x8192 fp32, full size"
+    else:
+        return None
+    call()
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        call()
+        times.append(time.perf_counter() - t0)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and (time.perf_counter() - t_start > min_seconds or len(times) >= max_reps):
+            break
+    best = min(times)
+    return {"value": round(nbytes / statistics.median(times) / 1e9, 3), "unit": "GB/s",
+            "cores": int(lib.ref_threads()), "kind": "reference",
+            "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
+                      f"median of {len(times)} calls, best {nbytes / best / 1e9:.1f} GB/s",
+            "ms_per_call": round(1e3 * statistics.median(times), 4)}
+
+
+# ------------------------------------------------------------ main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="asum")
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+        if args.impl == "ours":
+            import ctypes
+            uid = ctypes.create_string_buffer(128)
+            if rank == 0:
+                RT.lib().dpia_nccl_unique_id(uid)
+            obj = [bytes(uid.raw)]
+            dist.broadcast_object_list(obj, src=0)
+            RT.init(local)
+            RT.lib().dpia_nccl_init(local, world, rank, obj[0])
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(args.workload, steps=args.steps)
+        line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": {"workload": f"{args.workload} (reference c-openmp path on host cores)"}}
+        if r is None:
+            line.update({"unavailable": "oracle/_ref/libref_cpu.so not built (needs /root/reference at build)"})
+        else:
+            line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
+                         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                 "d2h_bytes_per_step": 0}})
+        print(json.dumps(line), flush=True)
+        return
+
+    device = local
+    RT.init(device)
+    stream = RT.Stream(device)
+    peak, peak_src = peaks()
+
+    def measure(workload, steps, warmup, with_e2e):
+        cfg, exe, inputs = make_workload(workload, device, rank, world)
+        for n, v in inputs.items():
+            exe.upload(n, v, stream)
+        stream.sync()
+        allreduce = None
+        if world > 1:
+            import torch
+            outbuf = exe.buffers["out"]
+
+            def allreduce(s):  # NCCL sum of the per-rank partial, on our stream
+                RT.lib().dpia_nccl_allreduce(outbuf.ptr, 1, 0, s.handle)
+        time_steps(exe, stream, steps, warmup, allreduce=allreduce)
+        if dist is not None:
+            dist.barrier()
+        RT.lib().dpia_device_sync(device)
+        with Clocks(device) as clk:
+            t0 = time.perf_counter()
+            ms = run_timed(exe, stream, steps, allreduce=allreduce)
+            wall = time.perf_counter() - t0
+        RT.lib().dpia_device_sync(device)
+        mean_ms = statistics.mean(ms)
+        if dist is not None:
+            import torch
+            t = torch.tensor([mean_ms], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            mean_ms = float(t.item())
+            dist.barrier()
+        kernel_ms = run_timed(exe, stream, min(steps, 10))  # dominant kernel alone, no collective
+        kmean = statistics.mean(kernel_ms)
+        achieved = cfg.bytes / (kmean * 1e-3) / 1e9
+        res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
+               "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
+               "value": world * cfg.bytes / (mean_ms * 1e-3) / 1e9,
+               "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                            "unit": "GB/s", "frac": round(achieved / peak, 4),
+                            "traffic": ncu_traffic(workload),
+                            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                            "algorithmic_bytes_per_launch": cfg.bytes,
+                            "kernel_ms": round(kmean, 5)}}
+        if with_e2e:
+            e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
+            res["e2e"] = {"value": round(cfg.bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                          "ms_per_step": round(e2e_ms, 4),
+                          "path": "run_kernel public API: pinned H2D + kernels + D2H"}
+        return res
+
+    head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
+    suite = {}
+    if not args.no_suite and world == 1:
+        for w in ("dot", "asum", "gemv"):
+            if w == args.workload:
+                continue
+            r = measure(w, min(args.steps, 20), 3, with_e2e=False)
+            suite[w] = {"value": round(r["value"], 1), "unit": "GB/s", "ms_per_step": round(r["mean_ms"], 5),
+                        "roofline": r["roofline"], "config": _cfg_desc(r["cfg"])}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_reference(args.workload)
+    if rank != 0:
+        return
+    cfg, exe = head["cfg"], head["exe"]
+    line = {"metric": METRIC, "value": round(head["value"], 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["mean_ms"], 5),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (numpy default_rng uniform, resident in HBM)",
+            "config": _cfg_desc(cfg),
+            "roofline": head["roofline"], "e2e": head["e2e"], "clocks": head["clocks"],
+            "gpu_launches": args.steps * len(exe.sig.kernels),
+            "kernels": exe.kernel_names(),
+            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                             if cpu else None),
+            "suite": suite}
+    print(json.dumps(line), flush=True)
+
+
+def _cfg_desc(cfg):
+    return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",
+                         "dot": "dot N=2^24 fp32, asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal",
+                         "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x"}[cfg.name],
+            "sigma": cfg.sigma, "launch": list(cfg.launch),
+            "l2": "flushed between steps (2x L2 memset, outside the timed events)"}
+
+
+if __name__ == "__main__":
+    main()

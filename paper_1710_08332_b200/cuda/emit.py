@@ -1129,6 +1129,7 @@ class ProgramEmitter:
             use[binder] = {ki for ki, (g, tail) in enumerate(kernels)
                            for it in ([g] if g is not None else []) + tail
                            if binder in exp_names(it)}
+        n_items = {binder: sum(1 for it in items if binder in exp_names(it)) for _, _, binder in top}
         top_global: List[Tuple[str, DataType]] = []
         kernel_top: Dict[int, List[Tuple[str, str, DataType]]] = {}
         for b_prim, d, binder in top:
@@ -1138,7 +1139,7 @@ class ProgramEmitter:
                     kernels[k][0] is not None and binder in exp_names(kernels[k][0]) for k in ks))):
                 top_global.append((binder, d))
                 self.spaces[binder] = "global"
-            elif space == "local" and len(ks) > 1:
+            elif space == "local" and (len(ks) > 1 or n_items[binder] > 1):
                 # outside any work-group, local memory has no per-group
                 # meaning; a buffer shared by several phases lives in HBM
                 top_global.append((binder, d))
