@@ -99,21 +99,21 @@ def gemv_program(M: int, N: int, L: int = 256) -> str:
 """
 
 
-def dot_config(N: int = 1 << 24, L: int = 256, K: int = 16, blocks=None) -> Config:
+def dot_config(N: int = 1 << 24, L: int = 512, K: int = 32, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
     n = N // per_wg
     return Config("dot", dot_program(L, K), {"n": n}, (blocks or n, L), bytes=8 * N, flops=2 * N)
 
 
-def asum_config(N: int = 1 << 26, L: int = 256, K: int = 32, blocks=None) -> Config:
+def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 32, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
     n = N // per_wg
     return Config("asum", asum_program(L, K), {"n": n}, (blocks or n, L), bytes=4 * N, flops=2 * N)
 
 
-def gemv_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int = 148 * 8) -> Config:
+def gemv_config(M: int = 8192, N: int = 8192, L: int = 512, blocks: int = 148 * 4) -> Config:
     return Config("gemv", gemv_program(M, N, L), {}, (min(blocks, M), L),
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
