@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
-                                                  gemv_config)
+                                                  gemv_config, mm_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
 
@@ -42,6 +42,18 @@ def peaks():
         return p["hbm_gbs"], "measured"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback"
+
+
+def fp32_peak(device):
+    """FP32 FFMA peak: SMs x 128 lanes x 2 flop x max SM clock (nominal).
+    Returns (TFLOP/s, description)."""
+    sms = RT.device_attribute(device, RT.ATTR_SM_COUNT)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+    except (OSError, KeyError, ValueError):
+        mhz = 1965.0
+    return sms * 128 * 2 * mhz * 1e6 / 1e12, f"computed: {sms} SMs x 128 FFMA x 2 x {mhz:.0f} MHz"
 
 
 def ncu_traffic(workload):
@@ -112,6 +124,9 @@ def make_workload(name, device, rank=0, world=1):
     elif name == "gemv":
         cfg = gemv_config()
         inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
+    elif name == "mm":
+        cfg = mm_config()
+        inputs = {"A": _seeded((4096, 4096), 5, -1.0, 1.0), "B": _seeded((4096, 4096), 6, -1.0, 1.0)}
     else:
         raise SystemExit(f"unknown workload {name}")
     prog = compile_program(cfg.text, name=name)
@@ -330,16 +345,25 @@ def main():
             dist.barrier()
         kernel_ms = run_timed(exe, stream, min(steps, 10))  # dominant kernel alone, no collective
         kmean = statistics.mean(kernel_ms)
-        achieved = cfg.bytes / (kmean * 1e-3) / 1e9
+        if workload == "mm":
+            fp32 = fp32_peak(device)
+            achieved = cfg.flops / (kmean * 1e-3) / 1e12
+            value = world * cfg.flops / (mean_ms * 1e-3) / 1e9
+            roof = {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(fp32[0], 2),
+                    "unit": "TFLOP/s", "frac": round(achieved / fp32[0], 4),
+                    "traffic": ncu_traffic(workload), "peak_source": fp32[1],
+                    "algorithmic_flops_per_launch": cfg.flops, "kernel_ms": round(kmean, 5)}
+        else:
+            achieved = cfg.bytes / (kmean * 1e-3) / 1e9
+            value = world * cfg.bytes / (mean_ms * 1e-3) / 1e9
+            roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4),
+                    "traffic": ncu_traffic(workload),
+                    "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
+                    "algorithmic_bytes_per_launch": cfg.bytes, "kernel_ms": round(kmean, 5)}
         res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
                "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
-               "value": world * cfg.bytes / (mean_ms * 1e-3) / 1e9,
-               "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                            "unit": "GB/s", "frac": round(achieved / peak, 4),
-                            "traffic": ncu_traffic(workload),
-                            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
-                            "algorithmic_bytes_per_launch": cfg.bytes,
-                            "kernel_ms": round(kmean, 5)}}
+               "value": value, "roofline": roof}
         if with_e2e:
             e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
             res["e2e"] = {"value": round(cfg.bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
@@ -351,12 +375,13 @@ def main():
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
     suite = {}
     if not args.no_suite and world == 1:
-        for w in ("dot", "asum", "gemv"):
+        for w in ("dot", "asum", "gemv", "mm"):
             if w == args.workload:
                 continue
             r = measure(w, min(args.steps, 20), 3, with_e2e=False)
-            suite[w] = {"value": round(r["value"], 1), "unit": "GB/s", "ms_per_step": round(r["mean_ms"], 5),
-                        "roofline": r["roofline"], "config": _cfg_desc(r["cfg"])}
+            suite[w] = {"value": round(r["value"], 1), "unit": "GFLOP/s" if w == "mm" else "GB/s",
+                        "ms_per_step": round(r["mean_ms"], 5), "roofline": r["roofline"],
+                        "clocks": r["clocks"], "config": _cfg_desc(r["cfg"])}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference(args.workload)
@@ -380,7 +405,9 @@ def main():
 def _cfg_desc(cfg):
     return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",
                          "dot": "dot N=2^24 fp32, asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal",
-                         "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x"}[cfg.name],
+                         "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x",
+                         "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
+                               "tiles, toLocal k-tiles of 8"}[cfg.name],
             "sigma": cfg.sigma, "launch": list(cfg.launch),
             "l2": "flushed between steps (2x L2 memset, outside the timed events)"}
 

@@ -4,7 +4,7 @@ CPU restatement of the reference's functional semantics `eval_phrase`
 (/root/reference/pkg/src/dpia/eval_fn.py:120-215) over this repo's phrase AST,
 plus the shim for primitives the reference lacks (SURVEY.md 8c "parity
 unpinned" list): transpose, abs, reduceSeq, reduceLocal, mapWorkgroup1,
-mapLocal1 and array-splat literals.
+mapLocal1, let, lane indexing of vectors and array-splat literals.
 
 Values follow the reference: numbers are Python int (exact "int mode") or
 float (float64 "float mode"); index values are ints; arrays are lists; pairs
@@ -151,6 +151,8 @@ def _prim(name, targs, args, env, sigma):
         return ev(args[0])[0]
     if name == "snd" and k == 1:
         return ev(args[0])[1]
+    if name == "let" and k == 2:  # shim: bind the value
+        return ev(args[1])(ev(args[0]))
     if name in ("toGlobal", "toLocal", "toPrivate") and k == 2:
         return ev(args[0])(ev(args[1]))
     if name == "idx" and k == 2:

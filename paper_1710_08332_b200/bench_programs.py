@@ -99,6 +99,81 @@ def gemv_program(M: int, N: int, L: int = 256) -> str:
 """
 
 
+def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) -> str:
+    """C = A B (row-major), SURVEY.md App. A.4 strategy:
+
+    * mapWorkgroup1 / mapWorkgroup over T x T output tiles (blockIdx.y/x);
+    * a sequential reduce over K/BK k-tiles whose accumulator is the T x T
+      tile viewed as [T/R][T/R][R][R] -- one R x R register tile per work-item
+      (mapLocal1 / mapLocal = threadIdx.y / x), initialised by an explicit
+      mapLocal nest over a zero splat so the backend can thread-slice it;
+    * per k-tile, A and B tiles staged by toLocal with one vec4 global load
+      per work-item (A stored transposed, k-major, for the outer products);
+      the B tile is bound with `let` so it is staged once per k-tile rather
+      than once per work-item row;
+    * per work-item an R x R outer-product reduceSeq over the BK k-steps.
+    """
+    P = T // R                       # work-items per dimension
+    V = T * BK // 4                  # vec4 per staged tile
+    rows = V // P
+    zero_t = f"(array {P} (array {P} (array {R} (array {R} num))))"
+    a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {P} (asVector4 (join t))))))))) (fst tiles))")
+    b_stage = (f"(toLocal (lam t (split {T} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {P} (asVector4 (join t)))))))) (snd tiles))")
+    micro = f"""
+          (reduceSeq
+           (lam (ab (exp (pair (array {R} num) (array {R} num))))
+            (lam (t (exp (array {R} (array {R} num))))
+             (mapSeq (lam (q (exp (pair num (array {R} num))))
+                      (mapSeq (lam (w (exp (pair num num))) (+ (snd w) (* (fst w) (fst q))))
+                              (zip (fst ab) (snd q))))
+                     (zip (snd ab) t))))
+           (snd pb)
+           (zip (transpose (fst pa)) (transpose (fst pb))))"""
+    del rows
+    return f"""
+(param A (exp (array {M} (array {K} num))))
+(param B (exp (array {K} (array {N} num))))
+(join
+ (mapWorkgroup1
+  (lam (aRows (exp (array {T} (array {K} num))))
+   (transpose
+    (mapWorkgroup
+     (lam (bCols (exp (array {T} (array {K} num))))
+      (join
+       (mapLocal1
+        (lam (accRow (exp (array {P} (array {R} (array {R} num)))))
+         (transpose (join (mapLocal (lam (blk (exp (array {R} (array {R} num))))
+                                     (mapSeq (mapSeq (lam (z (exp num)) z)) blk))
+                                    accRow))))
+        (reduceSeq
+         (lam (tiles (exp (pair (array {T} (array {BK} num)) (array {BK} (array {T} num)))))
+          (lam (acc (exp {zero_t}))
+           (let {b_stage}
+            (lam (bl (exp (array {BK} (array {T} num))))
+             (mapLocal1
+              (lam (pa (exp (pair (array {R} (array {BK} num)) (array {P} (array {R} (array {R} num))))))
+               (mapLocal
+                (lam (pb (exp (pair (array {R} (array {BK} num)) (array {R} (array {R} num)))))
+                 {micro})
+                (zip (split {R} (transpose bl)) (snd pa))))
+              (zip (split {R} (transpose {a_stage})) acc))))))
+         (mapLocal1 (lam r (mapLocal (lam b (mapSeq (mapSeq (lam z z)) b)) r)) (as {zero_t} 0))
+         (zip (transpose (split {K // BK} (split {BK} (join aRows))))
+              (split {BK} (transpose bCols)))))))
+     (split {T} (transpose B)))))
+  (split {T} A)))
+"""
+
+
+def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 8,
+              R: int = 8) -> Config:
+    P = T // R
+    return Config("mm", mm_program(M, N, K, T, BK, R), {}, ((N // T, M // T), (P, P)),
+                  bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
+
+
 def dot_config(N: int = 1 << 24, L: int = 512, K: int = 32, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -118,7 +193,7 @@ def gemv_config(M: int = 8192, N: int = 8192, L: int = 512, blocks: int = 148 * 
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
 
-CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config}
+CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config}
 
 
 def aot_sources():

@@ -304,6 +304,23 @@ def _r_proj(index: int):
     return rule
 
 
+def _r_let(el, sx) -> Typed:
+    _arity(sx, 3, "(let E F)")
+    e, et = el.infer(sx[1])
+    d1 = _data(sx, et)
+    f, ft = el.check_fn(sx[2], [ExpT(d1)])
+    d2 = _data(sx, ft)
+    return apply_prim("let", [d1, d2], [e, f]), ExpT(d2)
+
+
+def _r_as(el, sx) -> Typed:
+    """(as DTYPE E): E checked at (exp DTYPE); a literal becomes a splat of
+    that type (extension: e.g. the zero register tile of mm)."""
+    _arity(sx, 3, "(as DTYPE E)")
+    d = parse_data(sx[1])
+    return el.check(sx[2], ExpT(d)), ExpT(d)
+
+
 def _r_tuple(el, sx) -> Typed:
     _arity(sx, 3, "(tuple P1 P2)")
     (p1, t1), (p2, t2) = el.infer(sx[1]), el.infer(sx[2])
@@ -615,7 +632,7 @@ def _r_zip_acc(index: int):
 
 _RULES: Dict[str, Callable] = {
     "lam": _r_lam, "tlam": _r_tlam, "tapp": _r_tapp, "proj1": _r_proj(1), "proj2": _r_proj(2),
-    "tuple": _r_tuple, "reduceLocal": _r_reduce_local, "zip": _r_zip, "split": _r_split,
+    "tuple": _r_tuple, "as": _r_as, "let": _r_let, "reduceLocal": _r_reduce_local, "zip": _r_zip, "split": _r_split,
     "join": _r_join, "transpose": _r_transpose, "pair": _r_pair, "fst": _r_pair_elim,
     "snd": _r_pair_elim, "idx": _r_idx, "seq": _r_seq, ":=": _r_assign, "for": _r_for,
     "reduceI": _r_reducei, "reduceILocal": _r_reducei_local, "idxAcc": _r_idx_acc,

@@ -14,6 +14,10 @@ SURVEY.md section 0 finding 1):
   dimension (blockIdx.y / threadIdx.y)
 * ``reduceIInit``                      -- reduceI whose initial value is written
   by a command (acceptor translation of a non-trivial init expression)
+* ``let``                              -- (let E (lam x B)): E materialised once
+  and shared by every use of x in B (the reference has no sharing construct,
+  so a staged value used inside a nested map is re-staged per iteration,
+  SURVEY.md section 7 hard part 6)
 """
 from __future__ import annotations
 
@@ -100,6 +104,8 @@ PRIMITIVES: Dict[str, PhraseType] = {
     "negate": _UNOP_T, "abs": _UNOP_T,
     "+": _BINOP_T, "-": _BINOP_T, "*": _BINOP_T, "/": _BINOP_T,
     "reduce": _REDUCE_T, "reduceSeq": _REDUCE_T, "reduceLocal": _COMBINE_T,
+    # let: E is materialised once (by its continuation translation) and bound
+    "let": _forall("d1:data d2:data", _arrow(E(_d1), _arrow(E(_d1), E(_d2)), E(_d2))),
     "zip": _forall("n:nat d1:data d2:data", _arrow(EA(_n, _d1), EA(_n, _d2), EA(_n, Pair(_d1, _d2)))),
     "split": _forall("n:nat m:nat d:data", _arrow(EA(_n * _m, _d), EA(_m, Array(_n, _d)))),
     "join": _forall("n:nat m:nat d:data", _arrow(EA(_n, Array(_m, _d)), EA(_n * _m, _d))),

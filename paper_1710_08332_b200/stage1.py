@@ -14,7 +14,9 @@ Differences from the reference, all conservative extensions:
   layout-only combinators (split/join/transpose/asVector/asScalar/idx), so
   ``toLocal (lam t (transpose (mapLocal F t))) E`` stages in local memory;
 * a non-trivial reduce initial value is written straight into the
-  accumulator by A (``reduceIInit``) instead of through a temporary.
+  accumulator by A (``reduceIInit``) instead of through a temporary;
+* ``let``: A(let E f, a) = C(E, v. A(f v, a)) and C(let E f, c) =
+  C(E, v. C(f v, c)) -- E is materialised once, where the let stands.
 """
 from __future__ import annotations
 
@@ -29,7 +31,7 @@ from .terms import (App, Lam, PairP, Phrase, Prim, Proj, Var, apply_prim,
 Cont = Callable[[Phrase], Phrase]
 
 # heads that make an expression non-trivial (need a translation clause)
-_NONTRIVIAL = set(MAP_FAMILY) | set(REDUCE_FAMILY) | {"reduceLocal"} | set(TO_SPACE)
+_NONTRIVIAL = set(MAP_FAMILY) | set(REDUCE_FAMILY) | {"reduceLocal", "let"} | set(TO_SPACE)
 _LAYOUT = ("split", "join", "transpose")
 
 
@@ -149,6 +151,10 @@ class Translator:
             return self.acceptor(src, Array(m, Vector(w)), apply_prim(f"asScalarAcc{w}", [m], [a]))
         if name in TO_SPACE and len(args) == 2:
             return self.acceptor(beta_normalize(App(args[0], args[1])), d, a)
+        if name == "let" and len(args) == 2:
+            d1, _d2 = targs
+            return self.continuation(args[0], d1, lambda v: self.acceptor(
+                beta_normalize(App(args[1], v)), d, a))
         if name == "idx" and len(args) == 2 and not is_trivial(e):
             n, dd = targs
             return self.continuation(args[0], Array(n, dd), lambda x: self.gen_assign(
@@ -199,8 +205,20 @@ class Translator:
             return self.continuation(src, src_t, lambda x: c(apply_prim(name, [m], [x])),
                                      space=space)
         if name in TO_SPACE and len(args) == 2:
-            return self.continuation(beta_normalize(App(args[0], args[1])), d, c,
-                                     space=TO_SPACE[name])
+            body = beta_normalize(App(args[0], args[1]))
+            bu = unapply(body)
+            if bu is not None and (bu[0] in _LAYOUT or (vector_prim(bu[0]) or ("",))[0] in
+                                   ("asVector", "asScalar")) and not is_trivial(body):
+                # a layout view of a computed value: store the value itself in
+                # space X, written through the acceptor duals of the view
+                tmp = self.fresh("tmp")
+                stage = seq(self.acceptor(body, d, Proj(Var(tmp), 1)), c(Proj(Var(tmp), 2)))
+                return apply_prim(SPACE_NEW[TO_SPACE[name]], [d], [Lam(tmp, stage)])
+            return self.continuation(body, d, c, space=TO_SPACE[name])
+        if name == "let" and len(args) == 2:
+            d1, _d2 = targs
+            return self.continuation(args[0], d1, lambda v: self.continuation(
+                beta_normalize(App(args[1], v)), d, c))
         if name == "idx" and len(args) == 2 and not is_trivial(e):
             n, dd = targs
             return self.continuation(args[0], Array(n, dd),

@@ -113,3 +113,34 @@ def test_sizes_polynomials():
     from paper_1710_08332_b200.sizes import nat_divide
     assert nat_divide(n * 1024, 1024) == n
     assert nat_divide(n * 1024 + 3, 1024) is None
+
+
+def test_mm_strategy_matches_numpy_oracle_small():
+    """The mm strategy program (transpose, let, 2-D maps, splat init) under
+    the oracle interpreter equals the NumPy restatement used at full size."""
+    import numpy as np
+    from oracle import blas_np
+    from paper_1710_08332_b200.bench_programs import mm_program
+    sp = parse(mm_program(32, 16, 24, T=16, BK=8, R=4))
+    A = np.random.default_rng(1).integers(-9, 10, (32, 24))
+    B = np.random.default_rng(2).integers(-9, 10, (24, 16))
+    got = eval_phrase(sp.body, {"A": A.tolist(), "B": B.tolist()})
+    flat = [x for row in got for blk in row for x in blk]
+    assert np.array_equal(np.array(flat).reshape(32, 16), A @ B)
+    want, _ = blas_np.mm(A, B)
+    assert np.array_equal(want, A @ B)
+    s2 = stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private")
+    out = run_program(s2, [("out", sp.body_type.data, "out"), ("A", sp.params[0][1].data, "in"),
+                           ("B", sp.params[1][1].data, "in")], {"A": A.tolist(), "B": B.tolist()}, {})
+    assert [x for row in out["out"] for blk in row for x in blk] == flat
+
+
+def test_let_shares_and_matches_reference_semantics():
+    src = ("(param xs (exp (array 8 num)))\n"
+           "(let (toLocal (mapLocal (lam (x (exp num)) (* x x))) xs)"
+           " (lam (s (exp (array 8 num))) (zip s (mapSeq (lam (y (exp num)) (+ y 1)) s))))")
+    sp = parse(src)
+    xs = list(range(8))
+    assert eval_phrase(sp.body, {"xs": xs}) == [(x * x, x * x + 1) for x in xs]
+    s1 = translate_program(sp.body, sp.body_type.data, "out", "global")
+    assert _count(s1, {"mapILocal"}) == 1  # the staged value is computed once

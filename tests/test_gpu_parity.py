@@ -17,7 +17,8 @@ from oracle import blas_np
 from oracle.dpia_eval import eval_phrase, flatten_value, from_json
 from paper_1710_08332_b200 import CudaError, compile_program, run_program_cuda
 from paper_1710_08332_b200.bench_programs import (asum_config, asum_program, dot_config,
-                                                  dot_program, gemv_config, gemv_program)
+                                                  dot_program, gemv_config, gemv_program, mm_config,
+                                                  mm_program)
 
 pytestmark = pytest.mark.gpu
 
@@ -120,3 +121,26 @@ def test_gemv_full_size_fp32():
     got = run_program_cuda(compile_program(cfg.text), {"A": A, "x": x}, launch=cfg.launch, flat=True)
     want, absterms = blas_np.gemv(A, x)
     assert blas_np.within(got, want, absterms)
+
+
+@pytest.mark.parametrize("M,N,K,T,BK,R", [(32, 32, 32, 16, 8, 4), (64, 96, 128, 32, 8, 4),
+                                          (256, 128, 384, 128, 8, 8), (128, 256, 64, 64, 16, 4)])
+def test_mm_strategy_int_exact(M, N, K, T, BK, R):
+    prog = compile_program(mm_program(M, N, K, T, BK, R))
+    A = np.random.default_rng(6).integers(-9, 10, (M, K))
+    B = np.random.default_rng(7).integers(-9, 10, (K, N))
+    P = T // R
+    got = run_program_cuda(prog, {"A": A, "B": B}, launch=((N // T, M // T), (P, P)),
+                           float_mode=False, flat=True)
+    assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
+
+
+def test_mm_full_size_fp32():
+    cfg = mm_config()
+    A = blas_np.seeded((4096, 4096), 5, -1.0, 1.0)
+    B = blas_np.seeded((4096, 4096), 6, -1.0, 1.0)
+    got = np.asarray(run_program_cuda(compile_program(cfg.text), {"A": A, "B": B}, launch=cfg.launch,
+                                      flat=True)).reshape(4096, 4096)
+    rows = np.random.default_rng(0).choice(4096, 64, replace=False)
+    want, absterms = blas_np.mm(A, B, rows)
+    assert blas_np.within(got[rows], want, absterms)

@@ -14,7 +14,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
-from paper_1710_08332_b200.bench_programs import asum_config, dot_config, gemv_config  # noqa: E402
+from paper_1710_08332_b200.bench_programs import asum_config, dot_config, gemv_config, mm_config  # noqa: E402
 
 
 def time_cfg(cfg, inputs, reps=20):
@@ -46,6 +46,22 @@ def main(which):
                   "ys": rng.uniform(0, 1, 1 << 24).astype(np.float32)}
         grid = [(L, K, b) for L in (512, 1024) for K in (8, 16, 32, 64) for b in (None, 592, 1184)]
         mk = lambda L, K, b: dot_config(L=L, K=K, blocks=b)  # noqa: E731
+    elif which == "mm":
+        inputs = {"A": rng.uniform(-1, 1, (4096, 4096)).astype(np.float32),
+                  "B": rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)}
+        grid = [(T, BK, R) for T, BK, R in ((128, 8, 8), (128, 16, 8), (64, 8, 4), (64, 16, 4),
+                                            (128, 32, 8), (64, 32, 4))]
+        mk = lambda T, BK, R: mm_config(T=T, BK=BK, R=R)  # noqa: E731
+        for T, BK, R in grid:
+            cfg = mk(T, BK, R)
+            try:
+                med, best = time_cfg(cfg, inputs, reps=10)
+            except Exception as e:  # noqa: BLE001
+                print(f"mm T={T} BK={BK} R={R}: {type(e).__name__} {str(e)[:200]}", flush=True)
+                continue
+            print(f"mm T={T:4d} BK={BK:3d} R={R}  median {med:8.3f} ms  {cfg.flops / med / 1e9:8.1f} TFLOP/s"
+                  f"  best {cfg.flops / best / 1e9:8.1f}", flush=True)
+        return
     else:
         inputs = {"A": rng.uniform(-1, 1, (8192, 8192)).astype(np.float32),
                   "x": rng.uniform(-1, 1, 8192).astype(np.float32)}
