@@ -104,18 +104,20 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
 
     * mapWorkgroup1 / mapWorkgroup over T x T output tiles (blockIdx.y/x);
     * a sequential reduce over K/BK k-tiles whose accumulator is the T x T
-      tile viewed as [T/R][T/R][R][R] -- one R x R register tile per work-item
-      (mapLocal1 / mapLocal = threadIdx.y / x), initialised by an explicit
-      mapLocal nest over a zero splat so the backend can thread-slice it;
-    * per k-tile, A and B tiles staged by toLocal with one vec4 global load
-      per work-item (A stored transposed, k-major, for the outer products);
-      the B tile is bound with `let` so it is staged once per k-tile rather
-      than once per work-item row;
+      tile viewed as [P][P][R][R] (P = T/R) -- one R x R register tile per
+      work-item (mapLocal1 / mapLocal = threadIdx.y / x), initialised by an
+      explicit mapLocal nest over a zero splat so the backend thread-slices it;
+    * per k-tile the A and B tiles are staged by toLocal with one vec4 global
+      load per work-item; A is stored k-major (transposed) for the outer
+      products; the B tile is bound with `let` so it is staged once per k-tile;
+    * work-item (ty, tx) owns rows ty*R + ii and the *interleaved* columns
+      h*T/2 + tx*R/2 + q (jj = h*R/2 + q), so each k-step reads its B values
+      with two conflict-free 16-byte shared loads;
     * per work-item an R x R outer-product reduceSeq over the BK k-steps.
     """
     P = T // R                       # work-items per dimension
-    V = T * BK // 4                  # vec4 per staged tile
-    rows = V // P
+    Q = 4 if R % 4 == 0 else R       # contiguous columns per shared load
+    H = R // Q                       # interleaved column groups
     zero_t = f"(array {P} (array {P} (array {R} (array {R} num))))"
     a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
                f" (split {P} (asVector4 (join t))))))))) (fst tiles))")
@@ -130,8 +132,7 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
                               (zip (fst ab) (snd q))))
                      (zip (snd ab) t))))
            (snd pb)
-           (zip (transpose (fst pa)) (transpose (fst pb))))"""
-    del rows
+           (zip (transpose (fst pa)) (transpose (join (fst pb)))))"""
     return f"""
 (param A (exp (array {M} (array {K} num))))
 (param B (exp (array {K} (array {N} num))))
@@ -144,9 +145,10 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
       (join
        (mapLocal1
         (lam (accRow (exp (array {P} (array {R} (array {R} num)))))
-         (transpose (join (mapLocal (lam (blk (exp (array {R} (array {R} num))))
-                                     (mapSeq (mapSeq (lam (z (exp num)) z)) blk))
-                                    accRow))))
+         (transpose (join (join (transpose
+          (mapLocal (lam (blk (exp (array {R} (array {R} num))))
+                     (split {Q} (mapSeq (mapSeq (lam (z (exp num)) z)) blk)))
+                    accRow))))))
         (reduceSeq
          (lam (tiles (exp (pair (array {T} (array {BK} num)) (array {BK} (array {T} num)))))
           (lam (acc (exp {zero_t}))
@@ -155,9 +157,9 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
              (mapLocal1
               (lam (pa (exp (pair (array {R} (array {BK} num)) (array {P} (array {R} (array {R} num))))))
                (mapLocal
-                (lam (pb (exp (pair (array {R} (array {BK} num)) (array {R} (array {R} num)))))
+                (lam (pb (exp (pair (array {H} (array {Q} (array {BK} num))) (array {R} (array {R} num)))))
                  {micro})
-                (zip (split {R} (transpose bl)) (snd pa))))
+                (zip (transpose (split {P} (split {Q} (transpose bl)))) (snd pa))))
               (zip (split {R} (transpose {a_stage})) acc))))))
          (mapLocal1 (lam r (mapLocal (lam b (mapSeq (mapSeq (lam z z)) b)) r)) (as {zero_t} 0))
          (zip (transpose (split {K // BK} (split {BK} (join aRows))))

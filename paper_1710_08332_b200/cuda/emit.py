@@ -375,6 +375,10 @@ class KernelEmitter:
         self.uniform_decl: Dict[str, bool] = {}
         self.hoisted: Dict[int, Buffer] = {}
         self.decl_depth: Dict[str, int] = {}
+        self.pf = None
+        self.pf_i = 0
+        self._pf_tag = 0
+        self.pipelined: Dict[int, tuple] = {}
         self.hoisted_writes: Set[int] = set()
 
     # ---------------------------------------------------------- helpers
@@ -655,6 +659,20 @@ class KernelEmitter:
         else:
             target = self.acc(a, steps)
             rhs = self.exp(e, steps)
+        if self.pf is not None:
+            mode, regs = self.pf
+            T = self.types.c_elem(d)
+            if mode == "declare":           # prologue: new register
+                name = f"pf{self._pf_tag}_{len(regs)}"
+                regs.append((name, T))
+                self.line(f"{name} = {rhs};")
+                return
+            name = regs[self.pf_i][0]
+            self.pf_i += 1
+            if mode == "refill":            # next iteration's global loads
+                self.line(f"{name} = {rhs};")
+                return
+            rhs = name                       # commit: registers -> shared memory
         buf = target.ref.buf if isinstance(target, VStore) else target.buf
         if isinstance(target, VStore):
             stmt = (f"dpia::vstore<{self.scalar}, {target.width}>({buf.cname}, "
@@ -667,7 +685,8 @@ class KernelEmitter:
 
     # --------------------------------------------------------- commands
     def comm(self, p: Phrase):
-        if id(p) in self.barriers and not self.per_thread:
+        if id(p) in self.barriers and not self.per_thread and \
+                (self.pf is None or self.pf[0] == "commit"):
             self.line("__syncthreads();")
         u = unapply(p)
         if u is None:
@@ -691,6 +710,12 @@ class KernelEmitter:
             return
         if name == "for":
             f = args[0]
+            trip = self.nat_int(targs[0])
+            cands = []
+            if not self.per_thread and self.launch and trip is not None and trip > 1:
+                cands = self.pipeline_candidates(f.body, f.binder)
+            if cands:
+                self.pipeline_prologue(cands, f.binder, targs[0], trip)
             self.loop("seq", 0, targs[0], f.binder, lambda: self.comm(f.body))
             return
         if name in PARFOR_FAMILY:
@@ -717,6 +742,27 @@ class KernelEmitter:
         return buf
 
     def new(self, prim: str, d: DataType, f: Lam, node: Phrase = None):
+        if node is not None and id(node) in self.pipelined:
+            buf, regs, c1, c2, binder, trip = self.pipelined[id(node)]
+            old = self.env.get(f.binder)
+            self.env[f.binder] = buf
+            # commit this iteration's prefetched tile, then prefetch the next
+            self.pf, self.pf_i = ("commit", regs), 0
+            self.comm(c1)
+            cur = self.env[binder]
+            self.open(f"if ({self.r(cur.ixv)} + 1 < {trip})")
+            self.env[binder] = Val(cur.dtype, ixv=cur.ixv + 1)
+            self.pf, self.pf_i = ("refill", regs), 0
+            self.comm(c1)
+            self.pf = None
+            self.env[binder] = cur
+            self.close()
+            self.comm(c2)
+            if old is None:
+                del self.env[f.binder]
+            else:
+                self.env[f.binder] = old
+            return
         if node is not None and id(node) in self.hoisted:
             old = self.env.get(f.binder)
             self.env[f.binder] = self.hoisted[id(node)]
@@ -938,6 +984,78 @@ class KernelEmitter:
     def plan_uniform(self, c: Phrase, loop: bool = False, alias=None, opaque=()):
         planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes, opaque)
         self.barriers |= planner.run(c, loop, alias)
+
+    # -------------------------------------- software-pipelined staging
+    def pipeline_candidates(self, body: Phrase, binder: str):
+        """newLocal stagings at the top level of a work-group-uniform
+        sequential loop body whose initialising command only copies from
+        read-only inputs through single-iteration work-item loops.  Their
+        global loads for iteration k+1 can be issued into registers before
+        iteration k's compute (the shared-memory writes stay in place)."""
+        inputs = {n for n, sp in self.prog.spaces.items() if sp == "in"}
+        L = self.launch
+        found = []
+
+        def simple(c) -> bool:
+            for q in subtree_iter(c):
+                if isinstance(q, Prim) and q.name in PARFOR_FAMILY:
+                    lvl, dim = LOOP_LEVEL[q.name]
+                    if lvl != "local":
+                        return False
+                if isinstance(q, Prim) and q.name in ("for", "reduceILocal", "new", "newLocal",
+                                                       "newPrivate", "newGlobal", "barrier"):
+                    return False
+            for q in subtree_iter(c):
+                u = unapply(q)
+                if u is not None and u[0] in PARFOR_FAMILY and len(u[1]) == 2:
+                    lvl, dim = LOOP_LEVEL[u[0]]
+                    t = self.nat_int(u[1][0])
+                    if t is None or t > L[1][dim]:
+                        return False
+            return True
+
+        def walk(q):
+            u = unapply(q)
+            if u is None:
+                return
+            name, targs, args = u
+            if name == ";":
+                walk(args[0].fst)
+                walk(args[0].snd)
+            elif _is_new(name) and isinstance(args[0], Lam):
+                fl = args[0]
+                inner = unapply(fl.body)
+                if name == "newLocal" and inner is not None and inner[0] == ";":
+                    c1, c2 = inner[2][0].fst, inner[2][0].snd
+                    R1, W1 = rw_sets(c1)
+                    free = free_vars(c1) - {fl.binder}
+                    outer_ix = {nm for nm, b in self.env.items() if isinstance(b, Val) and b.ixv is not None}
+                    if W1 == {fl.binder} and free <= inputs | {binder} | outer_ix and simple(c1):
+                        found.append((q, targs[0], fl, c1, c2))
+                walk(fl.body)
+
+        walk(body)
+        return found
+
+    def pipeline_prologue(self, cands, binder: str, n: Nat, trip: int):
+        for node, d0, fl, c1, c2 in cands:
+            buf = self._declare_local(fl.binder, d0)
+            self.env[fl.binder] = buf
+            old = self.env.get(binder)
+            self.env[binder] = Val(Idx(n), ixv=ix(0))
+            regs: List = []
+            self._pf_tag += 1
+            mark = len(self.lines)
+            self.pf = ("declare", regs)
+            self.comm(c1)
+            self.pf = None
+            self.lines[mark:mark] = ["  " * self.ind + f"{T} {nm};" for nm, T in regs]
+            if old is None:
+                del self.env[binder]
+            else:
+                self.env[binder] = old
+            del self.env[fl.binder]
+            self.pipelined[id(node)] = (buf, regs, c1, c2, binder, trip)
 
     # ---------------------------------------------- loop-invariant staging
     def invariant_stagings(self, body: Phrase, inner_binders: Set[str]):
