@@ -1,0 +1,188 @@
+"""`dpia`-compatible command line for the CUDA backend.
+
+    python -m paper_1710_08332_b200.cli compile P.dpia --target cuda [-o P.cu]
+                                        [--launch G,L] [--int|--float] [--dump-stages]
+    python -m paper_1710_08332_b200.cli run P.dpia --inputs P.inputs --device cuda
+                                        [--launch G,L] [--int|--float]
+
+Flags, input files (`key=value` lines, arrays in brackets) and exit codes (2
+parse error, 3 type error, 70 internal error) follow the reference CLI
+(SRC/cli.py:26-28, 140-189, 230-288).  `--launch` for compile specialises the
+emitted source to that geometry; without it sizes stay runtime parameters.
+"""
+from __future__ import annotations
+
+import argparse
+import ast
+import sys
+from pathlib import Path
+from typing import Dict, List, Optional, Tuple
+
+from .api import compile_program
+from .cuda.ctypes_map import CudaError
+from .cuda.emit import emit_cuda
+from .dtypes import ExpT
+from .reader import ElabError, ParseError
+
+EXIT_PARSE, EXIT_TYPE, EXIT_INTERNAL = 2, 3, 70
+
+
+class CliError(Exception):
+    def __init__(self, message: str, code: int):
+        super().__init__(message)
+        self.code = code
+
+
+def _load(path: str):
+    try:
+        text = Path(path).read_text()
+    except OSError as e:
+        raise CliError(f"cannot read {path}: {e}", EXIT_PARSE)
+    try:
+        prog = compile_program(text, name=Path(path).stem.replace("-", "_"))
+    except ElabError as e:
+        raise CliError(f"{path}: type error: {e}", EXIT_TYPE)
+    except ParseError as e:
+        raise CliError(f"{path}: parse error: {e}", EXIT_PARSE)
+    if not isinstance(prog.source.body_type, ExpT):
+        raise CliError(f"{path}: type error: program body must be an expression", EXIT_TYPE)
+    return prog
+
+
+def _launch_pair(text: str):
+    try:
+        parts = [int(x) for x in text.replace("x", ",").split(",")]
+        if len(parts) == 2:
+            g, l = parts
+            if g < 1 or l < 1:
+                raise ValueError
+            return g, l
+        if len(parts) == 4 and min(parts) >= 1:
+            return (parts[0], parts[1]), (parts[2], parts[3])
+        raise ValueError
+    except ValueError:
+        raise argparse.ArgumentTypeError("launch must be G,L or GX,GY,LX,LY with positive integers")
+
+
+def _parse_inputs(path: str) -> Dict[str, object]:
+    out: Dict[str, object] = {}
+    for ln, line in enumerate(Path(path).read_text().splitlines(), 1):
+        line = line.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if "=" not in line:
+            raise CliError(f"{path}:{ln}: expected key=value", EXIT_PARSE)
+        key, _, value = line.partition("=")
+        try:
+            out[key.strip()] = ast.literal_eval(value.strip())
+        except (ValueError, SyntaxError) as e:
+            raise CliError(f"{path}:{ln}: bad value: {e}", EXIT_PARSE)
+    return out
+
+
+def _compile(args) -> int:
+    prog = _load(args.file)
+    base = Path(args.file).with_suffix("")
+    if args.dump_stages:
+        Path(f"{base}.stage1.txt").write_text(repr(prog.stage1) + "\n")
+        Path(f"{base}.stage2.txt").write_text(repr(prog.imperative) + "\n")
+        print(f"wrote {base}.stage1.txt, {base}.stage2.txt")
+    sigma = _parse_inputs(args.sizes) if args.sizes else None
+    if sigma is not None:
+        sigma = {n: int(sigma[n]) for n in prog.source.nat_params}
+    src, _sig = emit_cuda(prog.imperative, [("out", prog.out_type)],
+                          [(n, t.data) for n, t in prog.source.params],
+                          float_mode=not args.int_mode, name=prog.name, sigma=sigma,
+                          launch=args.launch)
+    out = args.output or f"{base}.cu"
+    Path(out).write_text(src)
+    print(f"wrote {out}")
+    return 0
+
+
+def _run(args) -> int:
+    from .launcher import run_kernel
+    prog = _load(args.file)
+    data = _parse_inputs(args.inputs) if args.inputs else {}
+    sigma = {}
+    for n in prog.source.nat_params:
+        if n not in data:
+            raise CliError(f"missing size parameter {n}=...", EXIT_PARSE)
+        sigma[n] = int(data[n])
+    inputs = {}
+    for n, _t in prog.source.params:
+        if n not in data:
+            raise CliError(f"missing input {n}=...", EXIT_PARSE)
+        inputs[n] = data[n]
+    outs = run_kernel(prog.imperative, prog.params, inputs, args.launch or (148, 256), sigma,
+                      float_mode=not args.int_mode, device=args.gpu, name=prog.name)
+    for k in sorted(outs):
+        print(f"{k} = {_show(outs[k])}")
+    return 0
+
+
+def _show(v):
+    if hasattr(v, "items") and not isinstance(v, (list, tuple, dict)):
+        return "<" + ", ".join(_show(x) for x in v.items) + ">"
+    if isinstance(v, list):
+        return "[" + ", ".join(_show(x) for x in v) + "]"
+    if isinstance(v, tuple):
+        return "(" + ", ".join(_show(x) for x in v) + ")"
+    if isinstance(v, float) and v.is_integer():
+        return repr(v)
+    return repr(v)
+
+
+def build_parser() -> argparse.ArgumentParser:
+    ap = argparse.ArgumentParser(prog="dpia-cuda")
+    sub = ap.add_subparsers(dest="command", required=True)
+    c = sub.add_parser("compile", help="emit CUDA C for sm_100a")
+    c.add_argument("file")
+    c.add_argument("--target", choices=["cuda"], default="cuda")
+    c.add_argument("-o", "--output")
+    c.add_argument("--dump-stages", action="store_true")
+    c.add_argument("--launch", type=_launch_pair, help="specialise to G,L (or GX,GY,LX,LY)")
+    c.add_argument("--sizes", help="key=value file with the nat parameters to specialise")
+    _mode_flags(c)
+    c.set_defaults(fn=_compile)
+    r = sub.add_parser("run", help="execute on the GPU")
+    r.add_argument("file")
+    r.add_argument("--inputs")
+    r.add_argument("--device", choices=["cuda"], default="cuda")
+    r.add_argument("--gpu", type=int, default=0)
+    r.add_argument("--launch", type=_launch_pair)
+    _mode_flags(r)
+    r.set_defaults(fn=_run)
+    return ap
+
+
+def _mode_flags(p):
+    g = p.add_mutually_exclusive_group()
+    g.add_argument("--float", dest="int_mode", action="store_false")
+    g.add_argument("--int", dest="int_mode", action="store_true")
+    p.set_defaults(int_mode=False)
+
+
+def main(argv: Optional[List[str]] = None) -> int:
+    args = build_parser().parse_args(argv)
+    try:
+        return args.fn(args)
+    except CliError as e:
+        print(str(e), file=sys.stderr)
+        return e.code
+    except ElabError as e:
+        print(str(e), file=sys.stderr)
+        return EXIT_TYPE
+    except ParseError as e:
+        print(str(e), file=sys.stderr)
+        return EXIT_PARSE
+    except CudaError as e:
+        print(f"cuda backend: {e}", file=sys.stderr)
+        return EXIT_INTERNAL
+    except Exception as e:  # noqa: BLE001
+        print(f"internal error: {type(e).__name__}: {e}", file=sys.stderr)
+        return EXIT_INTERNAL
+
+
+if __name__ == "__main__":
+    sys.exit(main())

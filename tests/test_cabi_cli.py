@@ -1,0 +1,90 @@
+"""CPU-side checks of the native boundary and the CLI:
+* libdpia_rt.so loads without a GPU driver and exports every entry point
+  declared in include/dpia_rt.h;
+* NVRTC (in-process, no GPU needed) compiles emitted kernels for sm_100a;
+* the CLI follows the reference's exit codes (TST/test_cli.py:95-117)."""
+import os
+import re
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+from paper_1710_08332_b200 import runtime as RT
+from paper_1710_08332_b200.cli import main
+
+HEADER = os.path.join(ROOT, "include", "dpia_rt.h")
+
+
+def declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(dpia_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert declared() == sorted(RT.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = RT.lib()
+    for name in declared():
+        assert hasattr(lib.so, name), name
+    out = subprocess.run(["nm", "-D", RT.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (dpia_\w+)", out))
+    assert set(declared()) <= exported
+
+
+def test_no_driver_needed_to_load_and_errors_are_reported():
+    lib = RT.lib()
+    assert lib.so.dpia_last_error() is not None
+    if not os.path.exists("/dev/nvidia0"):
+        n = RT.C.c_int()
+        rc = lib.so.dpia_device_count(RT.C.byref(n))
+        assert rc != 0 and b"driver" in lib.so.dpia_last_error().lower() or rc == 0
+
+
+def test_nvrtc_compiles_emitted_benchmarks():
+    from paper_1710_08332_b200.bench_programs import aot_sources
+    for tag, src in aot_sources():
+        img = RT.nvrtc_compile(src)
+        assert img[:4] == b"\x7fELF", tag   # an sm_100a cubin
+
+
+def test_nvrtc_reports_compile_errors():
+    with pytest.raises(RT.DpiaRuntimeError) as ei:
+        RT.nvrtc_compile('extern "C" __global__ void k() { this is not cuda; }')
+    assert "error" in str(ei.value).lower()
+
+
+def _prog(tmp_path, text, name="p.dpia"):
+    p = tmp_path / name
+    p.write_text(text)
+    return str(p)
+
+
+def test_cli_compile_cuda(tmp_path):
+    src = open(os.path.join(ROOT, "tests", "golden", "dotvec.dpia")).read() \
+        if os.path.exists(os.path.join(ROOT, "tests", "golden", "dotvec.dpia")) else None
+    if src is None:
+        from conftest import load_golden
+        src = [c for c in load_golden("programs.json") if c["name"] == "dotvec.dpia"][0]["text"]
+    f = _prog(tmp_path, src, "dotvec.dpia")
+    assert main(["compile", f, "--target", "cuda", "--launch", "2,4"]) == 0
+    text = open(str(tmp_path / "dotvec.cu")).read()
+    for needle in ("__global__", "blockIdx.x", "threadIdx.x", "dpia::vload<float, 4>",
+                   "dpia::vec<float, 4>"):
+        assert needle in text, needle
+
+
+def test_cli_exit_codes(tmp_path):
+    assert main(["compile", _prog(tmp_path, "(param xs (exp (array 4 num))) (map")]) == 2
+    assert main(["compile", _prog(tmp_path, "(param xs (exp (array 4 num)))\n(zip xs (split 2 xs))",
+                                  "t.dpia")]) == 3
+    assert main(["compile", str(tmp_path / "missing.dpia")]) == 2
+
+
+def test_cli_module_entry_point():
+    r = subprocess.run([sys.executable, "-m", "paper_1710_08332_b200.cli", "--help"],
+                       capture_output=True, text=True, cwd=ROOT)
+    assert r.returncode == 0 and "compile" in r.stdout

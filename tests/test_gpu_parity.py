@@ -144,3 +144,15 @@ def test_mm_full_size_fp32():
     rows = np.random.default_rng(0).choice(4096, 64, replace=False)
     want, absterms = blas_np.mm(A, B, rows)
     assert blas_np.within(got[rows], want, absterms)
+
+
+def test_cli_run_device_cuda(tmp_path, capsys):
+    """`run --device cuda` on the reference's dot.dpia / dot.inputs prints
+    out = 120 (TST/test_cli.py:69-73)."""
+    from paper_1710_08332_b200.cli import main
+    case = [c for c in GOLDEN if c["name"] == "dot.dpia"][0]
+    (tmp_path / "dot.dpia").write_text(case["text"])
+    (tmp_path / "dot.inputs").write_text("xs = [1, 2, 3, 4, 5, 6, 7, 8]\nys = [8, 7, 6, 5, 4, 3, 2, 1]\n")
+    assert main(["run", str(tmp_path / "dot.dpia"), "--inputs", str(tmp_path / "dot.inputs"),
+                 "--device", "cuda", "--launch", "2,4", "--int"]) == 0
+    assert "out = 120" in capsys.readouterr().out
