@@ -1,0 +1,96 @@
+"""Sharded reductions (config 5).
+
+CPU (gloo, world size 2): the shard plan covers the outer chunk range exactly
+once, and per-rank partials of the oracle combined with an all-reduce equal
+the unsharded oracle -- the host-side logic of the multi-GPU driver.
+GPU: one rank runs the emitted kernel on device-generated hashed inputs and
+matches the host restatement of the same hash (bit-exact inputs), both at
+full N = 2^31 for asum and on a smaller dot.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import blas_np
+from paper_1710_08332_b200.scaleout import SEEDS, shard_plan
+
+
+def test_shard_plan_partitions_the_range():
+    for world in (1, 2, 4, 8):
+        shards = [shard_plan(1 << 31, 1 << 17, world, r) for r in range(world)]
+        covered = sorted((s.elem_offset, s.elem_offset + s.elems) for s in shards)
+        assert covered[0][0] == 0 and covered[-1][1] == 1 << 31
+        assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
+    with pytest.raises(ValueError):
+        shard_plan(1000, 64, 2, 0)
+
+
+def test_hash_is_a_pure_function_of_the_global_index():
+    full = blas_np.hash_f32(4096, 0, 7, -1.0, 1.0)
+    assert np.array_equal(full[1000:3000], blas_np.hash_f32(2000, 1000, 7, -1.0, 1.0))
+    assert full.min() >= -1.0 and full.max() < 1.0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, total, chunk, kind, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+    sh = shard_plan(total, chunk, world, rank)
+    x = blas_np.hash_f32(sh.elems, sh.elem_offset, SEEDS["x"], -1.0, 1.0).astype(np.float64)
+    if kind == "asum":
+        part = float(np.abs(x).sum())
+    else:
+        y = blas_np.hash_f32(sh.elems, sh.elem_offset, SEEDS["y"], -1.0, 1.0).astype(np.float64)
+        part = float(np.dot(x, y))
+    t = torch.tensor([part], dtype=torch.float64)
+    dist.all_reduce(t)
+    if rank == 0:
+        q.put(float(t.item()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["asum", "dot"])
+def test_gloo_world2_partials_combine_to_the_unsharded_result(kind):
+    total, chunk, world = 1 << 20, 1 << 14, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, total, chunk, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
+            else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
+    assert abs(got - want[0]) <= 1e-12 * want[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,total", [("asum", 1 << 31), ("dot", 1 << 26)])
+def test_sharded_kernel_matches_hash_oracle(kind, total):
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    run = ShardedReduction(kind, total)
+    st = RT.Stream(0)
+    run.fill_inputs(st)
+    run.launch(st, allreduce=False)
+    st.sync()
+    got = run.result()
+    want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
+            else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
+    assert blas_np.within(got, want[0], want[1]), (got, want)
