@@ -176,7 +176,7 @@ def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int
                   bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
 
 
-def dot_config(N: int = 1 << 24, L: int = 512, K: int = 32, blocks=None) -> Config:
+def dot_config(N: int = 1 << 24, L: int = 1024, K: int = 16, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
     n = N // per_wg

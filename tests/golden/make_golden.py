@@ -12,6 +12,9 @@ Outputs (committed; the GPU box never reads /root/reference):
   fuzz.json      -- the reference fuzzer's programs (`harness.generate_program`,
                     seeds 0..FUZZ_SEEDS-1) pretty-printed by the reference,
                     with `random_inputs` and the `eval_phrase` result.
+  Kernel-legal entries also carry "hoisted": the reference's hoisted kernel
+  form (`hoist_allocations`, the input of `emit_kernel`) pretty-printed, with
+  the typing environment needed to re-parse it.
   index.json     -- index-simplifier known answers (`codegen_c.simplify_index`).
 """
 from __future__ import annotations
@@ -55,6 +58,9 @@ def from_json(j):
     return j
 
 
+HOISTED = {}
+
+
 def kernel_result(sp, inputs, sigma, float_mode):
     s1 = translate_program(sp.body, sp.body_type.data, out="out", default_space="global")
     s2 = stage2(s1, accum_space="private")
@@ -63,6 +69,10 @@ def kernel_result(sp, inputs, sigma, float_mode):
     hoisted, _ = hoist_allocations(s2)
     params = [("out", sp.body_type.data, "out")] + [(n, t.data, "in") for n, t in sp.params]
     out = simulate_kernel(hoisted, params, inputs, (2, 2), sigma, float_mode)
+    # the reference's hoisted kernel form (the input of emit_kernel), printed
+    HOISTED["last"] = {"text": pretty_print(hoisted),
+                       "env": {"out": f"(acc {sp.body_type.data})",
+                               **{n: str(t) for n, t in sp.params}}}
     return True, to_json(out["out"])
 
 
@@ -71,10 +81,12 @@ def case(name, text, inputs, sigma=None, float_mode=False, note=""):
     sigma = sigma or {}
     inputs = {k: from_json(v) for k, v in inputs.items()}
     want = eval_phrase(sp.body, dict(inputs), sigma)
+    HOISTED.pop("last", None)
     legal, sim = kernel_result(sp, inputs, sigma, float_mode)
     return {"name": name, "text": text, "inputs": {k: to_json(v) for k, v in inputs.items()},
             "sigma": sigma, "float": float_mode, "expected": to_json(want),
-            "opencl_legal": legal, "simulated_2x2": sim, "note": note}
+            "opencl_legal": legal, "simulated_2x2": sim, "note": note,
+            "hoisted": HOISTED.pop("last", None)}
 
 
 def ints(n, a, b):
@@ -139,7 +151,9 @@ def main():
         sp = generate_program(seed, depth=4, sizes=64)
         inputs = random_inputs(sp, seed)
         text = "".join(f"(param {n} {t})\n" for n, t in sp.params) + pretty_print(sp.body)
+        HOISTED.pop("last", None)
         legal, sim = kernel_result(sp, inputs, {}, False)
+        hoisted = HOISTED.pop("last", None)
         try:  # the reference's printer is not a perfect inverse for vector literals
             parse(text)
             reparses = True
@@ -148,7 +162,7 @@ def main():
         fuzz.append({"seed": seed, "text": text, "type": str(sp.body_type), "reparses": reparses,
                      "inputs": {k: to_json(v) for k, v in inputs.items()},
                      "expected": to_json(eval_phrase(sp.body, dict(inputs), {})),
-                     "opencl_legal": legal, "simulated_2x2": sim})
+                     "opencl_legal": legal, "simulated_2x2": sim, "hoisted": hoisted})
 
     from dpia.c_ast import CBin, CInt, CVar, expr_str
     from dpia.codegen_c import simplify_index

@@ -88,3 +88,19 @@ def test_cli_module_entry_point():
     r = subprocess.run([sys.executable, "-m", "paper_1710_08332_b200.cli", "--help"],
                        capture_output=True, text=True, cwd=ROOT)
     assert r.returncode == 0 and "compile" in r.stdout
+
+
+def test_criterion3_analogue_cuda_kernel_text():
+    """The vectorised dot kernel (TST/test_acceptance.py:119-153) rendered for
+    CUDA carries the strategy: work-group and work-item ids, float4 loads and
+    stores, a private float4 accumulator."""
+    from conftest import load_golden
+    from paper_1710_08332_b200 import compile_program, emit_cuda
+    case = [c for c in load_golden("programs.json") if c["name"] == "dotvec.dpia"][0]
+    prog = compile_program(case["text"], name="dotvec")
+    src, sig = emit_cuda(prog.imperative, [("out", prog.out_type)],
+                         [(n, t.data) for n, t in prog.source.params], float_mode=True, name="dotvec")
+    for needle in ("blockIdx.x", "gridDim.x", "threadIdx.x", "blockDim.x",
+                   "dpia::vload<float, 4>", "dpia::vstore<float, 4>", "dpia::vec<float, 4> acc"):
+        assert needle in src, needle
+    assert [k.name for k in sig.kernels] == ["dotvec_k0"]

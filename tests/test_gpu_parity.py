@@ -156,3 +156,29 @@ def test_cli_run_device_cuda(tmp_path, capsys):
     assert main(["run", str(tmp_path / "dot.dpia"), "--inputs", str(tmp_path / "dot.inputs"),
                  "--device", "cuda", "--launch", "2,4", "--int"]) == 0
     assert "out = 120" in capsys.readouterr().out
+
+
+HOISTED = [c for c in GOLDEN + FUZZ if c.get("hoisted")]
+
+
+@pytest.mark.parametrize("case", HOISTED, ids=lambda c: c.get("name") or f"seed{c['seed']}")
+def test_reference_hoisted_kernel_form(case):
+    """run_kernel accepts the reference's *hoisted* kernel form -- the exact
+    input of emit_kernel / simulate_kernel (SRC/opencl.py:124-134, 397) --
+    printed by the reference, and reproduces its simulate_kernel result."""
+    from paper_1710_08332_b200 import run_kernel
+    from paper_1710_08332_b200.reader import ParseError, parse_phrase, parse_phrase_type, read_all
+    env = {k: parse_phrase_type(read_all(v)[0]) for k, v in case["hoisted"]["env"].items()}
+    try:
+        p, _ = parse_phrase(case["hoisted"]["text"], env)
+    except ParseError:
+        pytest.skip("the reference's printer does not round-trip this vector literal")
+    params = [("out", env["out"].data, "out")] + [(k, t.data, "in") for k, t in env.items() if k != "out"]
+    inputs = {k: from_json(v) for k, v in case["inputs"].items()}
+    fm = case.get("float", False)
+    got = run_kernel(p, params, inputs, (2, 2), case.get("sigma", {}), fm, flat=True)["out"]
+    want = flatten_value(from_json(case["simulated_2x2"]))
+    if fm:
+        assert np.allclose(got, want, rtol=1e-5, atol=1e-5)
+    else:
+        assert [int(v) for v in got] == want
