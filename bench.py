@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
-                                                  gemv_config, mm_config)
+                                                  gemv_config, mm_config, scal_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
 
@@ -132,6 +132,9 @@ def make_workload(name, device, rank=0, world=1):
     elif name == "gemv":
         cfg = gemv_config()
         inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
+    elif name == "scal":
+        cfg = scal_config()
+        inputs = {"alpha": np.full(4, 1.5, np.float32), "xs": _seeded(1 << 26, 7, -1.0, 1.0)}
     elif name == "mm":
         cfg = mm_config()
         inputs = {"A": _seeded((4096, 4096), 5, -1.0, 1.0), "B": _seeded((4096, 4096), 6, -1.0, 1.0)}
@@ -394,7 +397,7 @@ def main():
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
     suite = {}
     if not args.no_suite and world == 1:
-        for w in ("dot", "asum", "gemv", "mm"):
+        for w in ("dot", "asum", "gemv", "mm", "scal"):
             if w == args.workload:
                 continue
             r = measure(w, min(args.steps, 20), 3, with_e2e=False)
@@ -434,6 +437,7 @@ def _cfg_desc(cfg, world=1):
     return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",
                          "dot": "dot N=2^24 fp32, asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal",
                          "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x",
+                         "scal": "scal N=2^26 fp32 (read + write), grid-stride mapGlobal over vec4",
                          "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
                                "tiles, toLocal k-tiles of 8"}[cfg.name],
             "sigma": cfg.sigma, "launch": list(cfg.launch),

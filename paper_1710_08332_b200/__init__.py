@@ -13,8 +13,10 @@ from .stage2 import stage2  # noqa: F401
 from .cuda.ctypes_map import CudaError  # noqa: F401
 from .cuda.emit import CudaSignature, emit_cuda  # noqa: F401
 from .launcher import Executable, run_kernel  # noqa: F401
+from .cuda.hierarchy import HoistedBuffer, cuda_legal, hoist_allocations, lint_hierarchy  # noqa: F401
 from .api import Program, compile_program, executable, run_program_cuda  # noqa: F401
 
 __all__ = ["parse", "parse_phrase", "translate_program", "stage2", "emit_cuda", "run_kernel",
            "compile_program", "run_program_cuda", "executable", "CudaError", "ParseError",
-           "ElabError", "SourceProgram", "Program", "Executable", "CudaSignature"]
+           "ElabError", "SourceProgram", "Program", "Executable", "CudaSignature",
+           "hoist_allocations", "lint_hierarchy", "cuda_legal", "HoistedBuffer"]

@@ -176,6 +176,22 @@ def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int
                   bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
 
 
+def scal_program() -> str:
+    """y = alpha * x (the paper's fourth BLAS kernel): one
+    grid-stride mapGlobal over float4 vectors; alpha arrives as a (vec 4)
+    splat because DPIA arithmetic is typed at one data type."""
+    return """
+(nat n)
+(param alpha (exp (vec 4)))
+(param xs (exp (array (* n 4) num)))
+(asScalar4 (mapGlobal (lam (v (exp (vec 4))) (* v alpha)) (asVector4 xs)))
+"""
+
+
+def scal_config(N: int = 1 << 26, L: int = 256, blocks: int = 148 * 8) -> Config:
+    return Config("scal", scal_program(), {"n": N // 4}, (blocks, L), bytes=8 * N, flops=N)
+
+
 def dot_config(N: int = 1 << 24, L: int = 1024, K: int = 16, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -195,7 +211,8 @@ def gemv_config(M: int = 8192, N: int = 8192, L: int = 512, blocks: int = 148 * 
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
 
-CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config}
+CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
+           "scal": scal_config}
 
 
 def aot_sources():

@@ -144,3 +144,99 @@ def test_let_shares_and_matches_reference_semantics():
     assert eval_phrase(sp.body, {"xs": xs}) == [(x * x, x * x + 1) for x in xs]
     s1 = translate_program(sp.body, sp.body_type.data, "out", "global")
     assert _count(s1, {"mapILocal"}) == 1  # the staged value is computed once
+
+
+# ---------------------------------------------------------------- index algebra
+def _ix_from_sexp(sx, R):
+    from paper_1710_08332_b200.cuda import index as IX
+    from paper_1710_08332_b200.reader import Token, read_all
+    if isinstance(sx, Token):
+        return IX.ix(int(sx.text)) if sx.text.isdigit() else IX.ix(sx.text)
+    op, a, b = sx[0].text, _ix_from_sexp(sx[1], R), sx[2]
+    if op in "/%":
+        n = int(b.text)
+        return IX.div(a, n, R) if op == "/" else IX.mod(a, n, R)
+    bb = _ix_from_sexp(b, R)
+    return a + bb if op == "+" else (a + bb * (-1) if op == "-" else a * bb)
+
+
+def _eval_sexp(sx, env):
+    from paper_1710_08332_b200.reader import Token
+    if isinstance(sx, Token):
+        return int(sx.text) if sx.text.isdigit() else env[sx.text]
+    a, b = _eval_sexp(sx[1], env), _eval_sexp(sx[2], env)
+    op = sx[0].text
+    if op in "/%":
+        return a // b if op == "/" else a % b
+    return a + b if op == "+" else (a - b if op == "-" else a * b)
+
+
+@pytest.mark.parametrize("case", load_golden("index.json"), ids=lambda c: c["expr"])
+def test_index_simplifier_matches_reference_known_answers(case):
+    """Same cases as the reference's simplify_index tests
+    (TST/test_codegen_c.py:61-96, TST/test_acceptance.py:287-324): the CUDA
+    index algebra is exhaustively sound and removes every / and % that the
+    reference removes."""
+    import itertools
+    from paper_1710_08332_b200.cuda import index as IX
+    from paper_1710_08332_b200.reader import read_all
+    sx = read_all(case["expr"])[0]
+    R = dict(case["ranges"])
+    e = _ix_from_sexp(sx, R)
+    ev_ranges = {**{n: 20 for n in IX.free_names(e)}, **R}   # unknown-range names: sample
+    names = sorted(ev_ranges)
+    for vals in itertools.product(*(range(ev_ranges[n]) for n in names)):
+        env = dict(zip(names, vals))
+        assert IX.evaluate(e, env) == _eval_sexp(sx, env)
+    ours = IX.render(e)
+    ref = case["reference_simplified"]
+    if "/" not in ref and "%" not in ref:
+        assert "/" not in ours and "%" not in ours, (ours, ref)
+
+
+# ------------------------------------------------- reference-compatible hierarchy API
+HOIST_SRC = ("(nat n)\n(param xss (exp (array n (array 1024 num))))\n"
+             "(mapGlobal (lam (row (exp (array 1024 num)))"
+             " (reduce (+) 0 (toGlobal (mapSeq (lam x (* x x))) row))) xss)")
+
+
+def test_hoist_allocations_criterion9_analogue():
+    """TST/test_acceptance.py:250-284: one n x 1024 global buffer, indexed by
+    the loop variable, semantics unchanged."""
+    from paper_1710_08332_b200.cuda.hierarchy import hoist_allocations
+    from paper_1710_08332_b200.sizes import nat
+    sp = parse(HOIST_SRC)
+    s2 = stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private")
+    hoisted, bufs = hoist_allocations(s2)
+    assert len(bufs) == 1 and bufs[0].space == "global"
+    assert bufs[0].dtype.size == nat("n") and bufs[0].dtype.elem.size == nat(1024)
+    assert sum(1 for s in subtree_iter(hoisted) if isinstance(s, Prim) and s.name == "newGlobal") == 1
+    small = parse(HOIST_SRC.replace("1024", "8"))
+    s2s = stage2(translate_program(small.body, small.body_type.data, "out", "global"), "private")
+    hs, _ = hoist_allocations(s2s)
+    xss = [[(i * 8 + j) % 9 for j in range(8)] for i in range(4)]
+    params = [("out", array(nat("n"), Num()), "out"), ("xss", array(nat("n"), array(8, Num())), "in")]
+    want = eval_phrase(small.body, {"xss": xss}, {"n": 4})
+    for phrase in (s2s, hs):
+        assert run_program(phrase, params, {"xss": xss}, {"n": 4})["out"] == want
+
+
+def test_lint_hierarchy_messages():
+    from paper_1710_08332_b200.cuda.hierarchy import cuda_legal, lint_hierarchy
+
+    def lint(src):
+        sp = parse(src)
+        return lint_hierarchy(stage2(translate_program(sp.body, sp.body_type.data, "out", "global"),
+                                     "private"))
+    ok = ("(param xs (exp (array 8 num)))\n(mapWorkgroup (lam (c (exp (array 4 num)))"
+          " (mapLocal (lam x (+ x 1)) c)) (split 4 xs))")
+    assert lint(ok) == []
+    nested = ("(param xss (exp (array 4 (array 4 num))))\n(mapGlobal (lam (r (exp (array 4 num)))"
+              " (mapGlobal (lam x (+ x 1)) r)) xss)")
+    assert any("nested" in w for w in lint(nested))
+    assert any("work-group" in w for w in lint("(param xs (exp (array 8 num)))\n(mapLocal (lam x (+ x 1)) xs)"))
+    two_d = ("(param m (exp (array 4 (array 8 num))))\n(mapWorkgroup1 (lam (r (exp (array 8 num)))"
+             " (mapWorkgroup (lam (c (exp (array 4 num))) (mapLocal (lam x x) c)) (split 4 r))) m)")
+    assert lint(two_d) == []
+    sp = parse(two_d)
+    assert cuda_legal(stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private"))

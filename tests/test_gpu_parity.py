@@ -18,7 +18,7 @@ from oracle.dpia_eval import eval_phrase, flatten_value, from_json
 from paper_1710_08332_b200 import CudaError, compile_program, run_program_cuda
 from paper_1710_08332_b200.bench_programs import (asum_config, asum_program, dot_config,
                                                   dot_program, gemv_config, gemv_program, mm_config,
-                                                  mm_program)
+                                                  mm_program, scal_config, scal_program)
 
 pytestmark = pytest.mark.gpu
 
@@ -188,3 +188,16 @@ def test_reference_hoisted_kernel_form(case):
         assert [int(v) for v in got] == want
     if case["simulated_2x2"] != case["expected"]:
         assert case["name"] == "bench.gemv_rowwg"
+
+
+def test_scal_exact_and_full_size():
+    prog = compile_program(scal_program())
+    xs = _ints(4096, 9)
+    got = run_program_cuda(prog, {"alpha": [3, 3, 3, 3], "xs": xs}, sigma={"n": 1024}, launch=(7, 64),
+                           float_mode=False, flat=True)
+    assert [int(v) for v in got] == [3 * x for x in xs]
+    cfg = scal_config()
+    x = blas_np.seeded(1 << 26, 7, -1.0, 1.0)
+    got = run_program_cuda(compile_program(cfg.text), {"alpha": np.full(4, 1.5, np.float32), "xs": x},
+                           sigma=cfg.sigma, launch=cfg.launch, flat=True)
+    assert np.array_equal(np.asarray(got, np.float32), np.float32(1.5) * x)
