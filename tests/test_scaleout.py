@@ -94,3 +94,24 @@ def test_sharded_kernel_matches_hash_oracle(kind, total):
     want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
             else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
     assert blas_np.within(got, want[0], want[1]), (got, want)
+
+
+@pytest.mark.gpu
+def test_nccl_single_rank_allreduce_through_the_c_abi():
+    """dpia_nccl_* (NCCL from the torch wheel, dlopen'ed) on one rank: the
+    sum all-reduce of a partial leaves it unchanged."""
+    import ctypes
+    from paper_1710_08332_b200 import runtime as RT
+    RT.init(0)
+    uid = ctypes.create_string_buffer(128)
+    RT.lib().dpia_nccl_unique_id(uid)
+    RT.lib().dpia_nccl_init(0, 1, 0, uid.raw)
+    buf = RT.DeviceBuffer(16)
+    buf.upload(np.array([2.5, 0, 0, 0], np.float32))
+    st = RT.Stream(0)
+    RT.lib().dpia_nccl_allreduce(buf.ptr, 1, 0, st.handle)
+    st.sync()
+    out = np.zeros(4, np.float32)
+    buf.download(out)
+    assert out[0] == 2.5
+    RT.lib().dpia_nccl_destroy()
