@@ -56,6 +56,38 @@ def fp32_peak(device):
     return sms * 128 * 2 * mhz * 1e6 / 1e12, f"computed: {sms} SMs x 128 FFMA x 2 x {mhz:.0f} MHz"
 
 
+_SOL_CACHE = {}
+
+
+def read_sol(device, nbytes, stream):
+    """Size-matched speed of light: a hand-written minimal CUDA streaming-read
+    kernel (tools/readsol.py; measurement infrastructure, not product) timed
+    exactly like the benchmark steps on `nbytes` of HBM."""
+    if nbytes in _SOL_CACHE:
+        return _SOL_CACHE[nbytes]
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from readsol import SRC
+    mod = RT.Module(RT.get_cubin(SRC), device)
+    fn = mod.function("readsum")
+    buf, out = RT.DeviceBuffer(nbytes, device), RT.DeviceBuffer(16, device)
+    buf.zero(stream)
+    args = [RT.C.c_uint64(buf.ptr), RT.C.c_longlong(nbytes // 16), RT.C.c_uint64(out.ptr)]
+    ts = []
+    for it in range(13):
+        RT.lib().dpia_l2_flush(device, stream.handle)
+        e0, e1 = RT.Event(device), RT.Event(device)
+        e0.record(stream)
+        RT.launch(fn, device, (296, 1), (1024, 1), 0, args, stream)
+        e1.record(stream)
+        stream.sync()
+        if it >= 3:
+            ts.append(e0.elapsed_ms(e1))
+    buf.free()
+    out.free()
+    _SOL_CACHE[nbytes] = round(nbytes / statistics.median(ts) / 1e6, 1)
+    return _SOL_CACHE[nbytes]
+
+
 def ncu_traffic(workload):
     """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
     try:
@@ -383,6 +415,10 @@ def main():
                     "traffic": ncu_traffic(workload),
                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                     "algorithmic_bytes_per_launch": cfg.bytes, "kernel_ms": round(kmean, 5)}
+            if workload in ("asum", "dot", "gemv"):
+                sol = read_sol(device, cfg.bytes, stream)
+                roof["size_matched_read_sol_gbs"] = sol
+                roof["frac_of_size_matched_sol"] = round(achieved / sol, 4)
         res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
                "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
                "value": value, "roofline": roof}

@@ -151,6 +151,9 @@ def _prim(name, targs, args, env, sigma):
         return ev(args[0])[0]
     if name == "snd" and k == 1:
         return ev(args[0])[1]
+    if name.startswith("idxVec") and k == 2:  # shim: lane of a vector
+        v, i = ev(args[0]), ev(args[1])
+        return v.items[i]
     if name == "let" and k == 2:  # shim: bind the value
         return ev(args[1])(ev(args[0]))
     if name in ("toGlobal", "toLocal", "toPrivate") and k == 2:

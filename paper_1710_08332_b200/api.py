@@ -35,8 +35,13 @@ class Program:
         return [("out", self.out_type, "out")] + [(n, t.data, "in") for n, t in self.source.params]
 
 
-def compile_program(text: str, name: str = "KERNEL") -> Program:
+def compile_program(text: str, name: str = "KERNEL", check: bool = True) -> Program:
+    """parse -> SCIR type check (rejects racy parfor bodies, as the reference
+    CLI does, SRC/cli.py:48-53) -> Stage I -> Stage II."""
     sp = parse(text)
+    if check:
+        from .checker import type_check
+        type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
     s1 = translate_program(sp.body, sp.body_type.data, out="out", default_space="global")
     return Program(sp, s1, stage2(s1, accum_space="private"), name)
 

@@ -19,6 +19,7 @@ from pathlib import Path
 from typing import Dict, List, Optional, Tuple
 
 from .api import compile_program
+from .checker import DpiaTypeError
 from .cuda.ctypes_map import CudaError
 from .cuda.emit import emit_cuda
 from .dtypes import ExpT
@@ -40,7 +41,7 @@ def _load(path: str):
         raise CliError(f"cannot read {path}: {e}", EXIT_PARSE)
     try:
         prog = compile_program(text, name=Path(path).stem.replace("-", "_"))
-    except ElabError as e:
+    except (ElabError, DpiaTypeError) as e:
         raise CliError(f"{path}: type error: {e}", EXIT_TYPE)
     except ParseError as e:
         raise CliError(f"{path}: parse error: {e}", EXIT_PARSE)

@@ -555,7 +555,7 @@ class KernelEmitter:
             return self.resolve(args[k - 1], rest)
         if name in ("fst", "snd"):
             return self.resolve(args[0], [("f", 1 if name == "fst" else 2)] + steps)
-        if name == "idx":
+        if name == "idx" or name.startswith("idxVec"):
             return self.resolve(args[0], [("i", self.index(args[1]))] + steps)
         if name.startswith("asVector") and "Acc" not in name:
             w = int(name[len("asVector"):])

@@ -443,8 +443,8 @@ def _r_idx(el, sx) -> Typed:
     e, et = el.infer(sx[1])
     if isinstance(et, ExpT) and isinstance(et.data, Vector):
         # lane of a vector (extension: vectors read as arrays of lanes)
-        w = nat(et.data.width)
-        return apply_prim("idx", [w, NUM], [e, el.check(sx[2], ExpT(Idx(w)))]), ExpT(NUM)
+        w = et.data.width
+        return apply_prim(f"idxVec{w}", [], [e, el.check(sx[2], ExpT(Idx(nat(w))))]), ExpT(NUM)
     n, d = _arr_exp(sx, et)
     return apply_prim("idx", [n, d], [e, el.check(sx[2], ExpT(Idx(n)))]), ExpT(d)
 

@@ -14,6 +14,7 @@ SURVEY.md section 0 finding 1):
   dimension (blockIdx.y / threadIdx.y)
 * ``reduceIInit``                      -- reduceI whose initial value is written
   by a command (acceptor translation of a non-trivial init expression)
+* ``idxVec{w}``                         -- lane of a vector, written (idx v k)
 * ``let``                              -- (let E (lam x B)): E materialised once
   and shared by every use of x in B (the reference has no sharing construct,
   so a staged value used inside a nested map is re-staged per iteration,
@@ -152,6 +153,8 @@ for _w in VECTOR_WIDTHS:
     PRIMITIVES[f"asScalar{_w}"] = _forall("m:nat", _arrow(EA(_m, _v), EA(_m * _w, NUM)))
     PRIMITIVES[f"asVectorAcc{_w}"] = _forall("m:nat", _arrow(AA(_m, _v), AA(_m * _w, NUM)))
     PRIMITIVES[f"asScalarAcc{_w}"] = _forall("m:nat", _arrow(AA(_m * _w, NUM), AA(_m, _v)))
+    # lane of a vector: surface syntax (idx v k) at vector type
+    PRIMITIVES[f"idxVec{_w}"] = _arrow(E(_v), E(Idx(nat(_w))), E(NUM))
 
 
 def primitive_type(name: str) -> PhraseType:
@@ -175,7 +178,7 @@ IMPERATIVE_PRIMS = (
      "transpose", "zip", "pair", "fst", "snd", "splitAcc", "joinAcc", "transposeAcc", "pairAcc1",
      "pairAcc2", "zipAcc1", "zipAcc2", "reduceILocal"}
     | set(PARFOR_FAMILY) | set(NEW_SPACE) | set(ARITH_OPS)
-    | {f"{p}{w}" for p in ("asVector", "asScalar", "asVectorAcc", "asScalarAcc")
+    | {f"{p}{w}" for p in ("asVector", "asScalar", "asVectorAcc", "asScalarAcc", "idxVec")
        for w in VECTOR_WIDTHS}
 )
 INTERMEDIATE_PRIMS = set(MAPI_FAMILY) | {"reduceI", "reduceIInit"}

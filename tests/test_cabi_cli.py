@@ -82,6 +82,9 @@ def test_cli_exit_codes(tmp_path):
     assert main(["compile", _prog(tmp_path, "(param xs (exp (array 4 num)))\n(zip xs (split 2 xs))",
                                   "t.dpia")]) == 3
     assert main(["compile", str(tmp_path / "missing.dpia")]) == 2
+    racy = ("(param b (acc num))\n(param out2 (acc (array 4 num)))\n"
+            "(parfor out2 (lam (i (exp (idx 4))) (lam (o (acc num)) (:= b 1))))")
+    assert main(["compile", _prog(tmp_path, racy, "racy.dpia")]) == 3   # SCIR interference
 
 
 def test_cli_module_entry_point():

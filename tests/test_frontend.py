@@ -240,3 +240,54 @@ def test_lint_hierarchy_messages():
     assert lint(two_d) == []
     sp = parse(two_d)
     assert cuda_legal(stage2(translate_program(sp.body, sp.body_type.data, "out", "global"), "private"))
+
+
+# ------------------------------------------------------------------ SCIR checker
+def test_checker_interference_rejection_criterion8():
+    """TST/test_acceptance.py:236-247."""
+    from paper_1710_08332_b200.checker import DpiaTypeError, type_check
+    src = ("(param out (acc (array 4 num)))\n(param b (acc num))\n"
+           "(parfor out (lam (i (exp (idx 4))) (lam (o (acc num)) (:= b 1))))")
+    sp = parse(src)
+    with pytest.raises(DpiaTypeError) as ei:
+        type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
+    assert "passive" in str(ei.value) and "'b'" in str(ei.value)
+    ok = ("(param out (acc (array 4 num)))\n"
+          "(parfor out (lam (i (exp (idx 4))) (lam (o (acc num)) (:= o 1))))")
+    sp = parse(ok)
+    t, uses = type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
+    assert isinstance(t, type(COMM_T)) and uses.mode("out") == "active"
+
+
+from paper_1710_08332_b200.dtypes import COMM as COMM_T  # noqa: E402
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c.get("reparses", True)][::2], ids=_id)
+def test_stage1_type_preservation_criterion4(case):
+    """Every source type-checks and Stage I output re-checks at comm
+    (Theorem 4.1; TST/test_acceptance.py:164-178), for the reference's
+    programs and its fuzz corpus, in both translation modes."""
+    from paper_1710_08332_b200.checker import type_check
+    sp = parse(case["text"])
+    type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
+    for space in (None, "global"):
+        s1 = translate_program(sp.body, sp.body_type.data, "out", space)
+        t, _ = type_check(s1, delta=sp.delta, pi=sp.pi,
+                          gamma={**sp.gamma, "out": AccT(sp.body_type.data)})
+        assert t == COMM_T
+
+
+def test_benchmark_strategies_type_check():
+    """The B200 strategies (with transpose, reduceLocal, let, 2-D maps)
+    are well-typed SCIR, and so is their Stage I output."""
+    from paper_1710_08332_b200.bench_programs import (asum_program, dot_program, gemv_program,
+                                                      mm_program, scal_program)
+    from paper_1710_08332_b200.checker import type_check
+    for text in (dot_program(64, 4), asum_program(64, 4), gemv_program(8, 512, 64),
+                 mm_program(64, 64, 64, 32, 8, 4), scal_program()):
+        sp = parse(text)
+        type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
+        s1 = translate_program(sp.body, sp.body_type.data, "out", "global")
+        t, _ = type_check(s1, delta=sp.delta, pi=sp.pi,
+                          gamma={**sp.gamma, "out": AccT(sp.body_type.data)})
+        assert t == COMM_T
