@@ -34,7 +34,7 @@ from dpia.parser import parse  # noqa: E402
 from dpia.pretty import pretty_print  # noqa: E402
 from dpia.translate import translate_program  # noqa: E402
 
-FUZZ_SEEDS = 400
+FUZZ_SEEDS = 1000
 PROGS = "/root/reference/pkg/programs"
 
 
