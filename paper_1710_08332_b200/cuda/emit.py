@@ -711,6 +711,11 @@ class KernelEmitter:
         if name == "for":
             f = args[0]
             trip = self.nat_int(targs[0])
+            if not self.per_thread and not self.in_workgroup and not self.prog.in_tail and \
+                    contains_prim(f.body, {"parforGlobal", "parforWorkgroup", "parforWorkgroup1"}):
+                raise CudaError("a sequential loop around a grid-level parallel loop needs a "
+                                "grid-wide barrier per iteration (one kernel per iteration); "
+                                "not supported")
             cands = []
             if not self.per_thread and self.launch and trip is not None and trip > 1:
                 cands = self.pipeline_candidates(f.body, f.binder)
