@@ -128,6 +128,12 @@ class KernelInfo:
     args: List[Tuple[str, str]]   # (kind, name): kind in out/in/scratch/size/counter
     smem: int
     fused_tail: bool
+    # execution plan, for the phase-synchronous simulator (oracle/phase_sim.py)
+    grid_item: Optional[Phrase] = field(default=None, repr=False)
+    tail_items: List[Phrase] = field(default_factory=list, repr=False)
+    barriers: frozenset = field(default=frozenset(), repr=False)     # ids: barrier before node
+    hoisted: frozenset = field(default=frozenset(), repr=False)      # ids: LICM-staged newLocal
+    decls: List = field(default_factory=list, repr=False)            # kernel-level buffers
 
 
 @dataclass
@@ -140,6 +146,7 @@ class CudaSignature:
     scalar: str
     launch: Optional[Tuple[Tuple[int, int], Tuple[int, int]]]
     sigma: Optional[Dict[str, int]]
+    spaces: Dict[str, str] = field(default_factory=dict, repr=False)   # buffer binder -> space
 
     def params(self) -> List[str]:
         out = [f"{self.scalar} *{n}" for n, _ in self.outputs]
@@ -1290,7 +1297,7 @@ class ProgramEmitter:
         size_names = sorted(self.size_names) if self.sigma is None else []
         sig = CudaSignature(self.outputs, self.inputs,
                             [(b.cname, b.dtype) for b in self.scratch], size_names, infos,
-                            self.scalar, self.launch, self.sigma)
+                            self.scalar, self.launch, self.sigma, dict(self.spaces))
         src = ["// generated by the DPIA CUDA backend (paper_1710_08332_b200) for sm_100a",
                header, self.types.struct_text()] + bodies
         return "\n".join(s for s in src if s) + "\n", sig
@@ -1353,7 +1360,8 @@ class ProgramEmitter:
             head.append(f"  const {it} dpia_gsize = ({it})gridDim.x * gridDim.y * dpia_nthreads;")
         text = "\n".join(head + body_lines + ["}"])
         info = KernelInfo(kname, "launch" if grid is not None else "single", args, ke.smem,
-                          grid is not None and bool(tail))
+                          grid is not None and bool(tail), grid, list(tail),
+                          frozenset(ke.barriers), frozenset(ke.hoisted), list(decls))
         return text, info
 
     def _kernel_names(self, grid, tail):
