@@ -31,6 +31,7 @@ class Executable:
     device: int
     float_mode: bool
     sigma: Dict[str, int]
+    geometry: tuple = None          # ((gx, gy), (lx, ly)) used at launch
     module: RT.Module = None
     buffers: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
     counters: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
@@ -95,7 +96,7 @@ class Executable:
 
     # ------------------------------------------------------------ launch
     def launch(self, stream: Optional[RT.Stream] = None):
-        (g, l) = self.sig.launch
+        (g, l) = self.sig.launch or self.geometry
         for k, vals in zip(self.sig.kernels, self._args):
             grid = g if k.grid == "launch" else (1, 1)
             fn = self.module.function(k.name)
@@ -112,24 +113,29 @@ def _split_params(params):
 
 
 def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None,
-          float_mode: bool = False, device: int = 0, name: str = "KERNEL") -> Executable:
-    """Emit + compile + allocate (no data movement)."""
+          float_mode: bool = False, device: int = 0, name: str = "KERNEL",
+          specialize: bool = True) -> Executable:
+    """Emit + compile + allocate (no data movement).  specialize=False keeps
+    sizes as kernel arguments and the geometry runtime-only (the source the
+    CLI's `compile` writes without --launch)."""
     sigma = dict(sigma or {})
     outs, ins = _split_params(params)
-    src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name, sigma=sigma,
-                         launch=normalize_launch(launch))
-    exe = Executable(src, sig, device, float_mode, sigma)
+    geom = normalize_launch(launch)
+    src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name,
+                         sigma=sigma if specialize else None, launch=geom if specialize else None)
+    exe = Executable(src, sig, device, float_mode, sigma, geometry=geom)
     return exe.compile().allocate()
 
 
 def run_kernel(p: Phrase, params: List[Tuple[str, DataType, str]], inputs: Dict[str, object],
                launch, sigma: Optional[Dict[str, int]] = None, float_mode: bool = False,
-               device: int = 0, name: str = "KERNEL", flat: bool = False) -> Dict[str, object]:
+               device: int = 0, name: str = "KERNEL", flat: bool = False,
+               specialize: bool = True) -> Dict[str, object]:
     """Drop-in for `simulate_kernel(p, params, inputs, launch, sigma,
     float_mode)` (SRC/opencl.py:397): same arguments, same result mapping,
     executed on the GPU.  flat=True returns numpy arrays of scalar leaves."""
     normalize_launch(launch)  # ValueError for non-positive launches, like the reference
-    exe = build(p, params, launch, sigma, float_mode, device, name)
+    exe = build(p, params, launch, sigma, float_mode, device, name, specialize)
     stream = RT.Stream(device)
     for n, d, mode in params:
         if mode == "in":

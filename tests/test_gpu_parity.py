@@ -201,3 +201,23 @@ def test_scal_exact_and_full_size():
     got = run_program_cuda(compile_program(cfg.text), {"alpha": np.full(4, 1.5, np.float32), "xs": x},
                            sigma=cfg.sigma, launch=cfg.launch, flat=True)
     assert np.array_equal(np.asarray(got, np.float32), np.float32(1.5) * x)
+
+
+@pytest.mark.parametrize("launch", [(2, 4), (3, 32)])
+@pytest.mark.parametrize("case", [c for c in GOLDEN + FUZZ[:150] if c.get("opencl_legal")],
+                         ids=lambda c: c.get("name") or f"seed{c['seed']}")
+def test_unspecialised_kernels(case, launch):
+    """The generic source (sizes as kernel arguments, geometry only at launch
+    -- what `compile --target cuda` writes without --launch) computes the same
+    result."""
+    from paper_1710_08332_b200 import run_kernel
+    prog = compile_program(case["text"])
+    inputs = {k: from_json(v) for k, v in case["inputs"].items()}
+    fm = case.get("float", False)
+    got = run_kernel(prog.imperative, prog.params, inputs, launch, case.get("sigma", {}), fm,
+                     flat=True, specialize=False)["out"]
+    want = flatten_value(from_json(case["expected"]))
+    if fm:
+        assert np.allclose(got, want, rtol=1e-5, atol=1e-5)
+    else:
+        assert [int(v) for v in got] == want
