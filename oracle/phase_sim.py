@@ -12,8 +12,9 @@ have placed is missing.  Work-groups of a kernel run one after another and
 cross-work-group conflicts on global memory are reported too.
 
 It executes the emitter's *plan* (kernels, fused tails, planned barrier
-positions, hoisted stagings, single-thread uniform writes, the cooperative
-combine), so it checks the backend's decisions on the CPU at desk scale.
+positions, hoisted stagings, stagings rotated between two slices,
+single-thread uniform writes, the cooperative combine), so it checks the
+backend's decisions on the CPU at desk scale.
 """
 from __future__ import annotations
 
@@ -283,6 +284,12 @@ class Sim:
         elif space == "local":
             if ctx.per_thread:
                 cell = Cell(f.binder, d, False)
+            elif f.binder in info.rotated:
+                # the emitter alternates this staging between two slices
+                k = ("rot", f.binder, env[info.rotated[f.binder]] % 2)
+                if k not in ctx.block:
+                    ctx.block[k] = Cell(f.binder, d, True)
+                cell = ctx.block[k]
             else:
                 k = ("local", f.binder)
                 if k not in ctx.block:
@@ -474,6 +481,7 @@ class Sim:
 class _NoPlan:
     barriers = frozenset()
     hoisted = frozenset()
+    rotated: dict = {}
 
 
 _NOPLAN = _NoPlan()

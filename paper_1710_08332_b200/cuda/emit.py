@@ -133,6 +133,7 @@ class KernelInfo:
     tail_items: List[Phrase] = field(default_factory=list, repr=False)
     barriers: frozenset = field(default=frozenset(), repr=False)     # ids: barrier before node
     hoisted: frozenset = field(default=frozenset(), repr=False)      # ids: LICM-staged newLocal
+    rotated: Dict[str, str] = field(default_factory=dict, repr=False)  # buffer -> its loop binder
     decls: List = field(default_factory=list, repr=False)            # kernel-level buffers
 
 
@@ -286,10 +287,13 @@ class BarrierPlanner:
     barrier inside the body (the reference's insert_barriers,
     SRC/opencl.py:209-244, handles only the straight-line RAW case)."""
 
-    def __init__(self, shared, skip=(), opaque=()):
+    def __init__(self, shared, skip=(), opaque=(), rotated=()):
         self.shared = shared
         self.skip = set(skip)
         self.opaque = set(opaque)   # single-thread units: analysed as one leaf
+        # shared buffers that alternate between two slices across iterations
+        # of their sequential loop: no loop-carried hazard
+        self.rotated = frozenset(rotated)
         self.before: Set[int] = set()
 
     def run(self, c: Phrase, loop: bool = False, alias=None):
@@ -326,6 +330,8 @@ class BarrierPlanner:
                 body = args[1].body.body
                 alias = {**alias, args[1].body.binder: acc_roots(args[0], alias)}
             s1 = self.visit(body, st, alias)
+            if name == "for":
+                s1 = (s1[0] - self.rotated, s1[1] - self.rotated)
             s2 = self.visit(body, s1, alias)
             return s2
         if name == "reduceILocal":
@@ -386,6 +392,8 @@ class KernelEmitter:
         self.pf_i = 0
         self._pf_tag = 0
         self.pipelined: Dict[int, tuple] = {}
+        self.for_plans: Dict[int, list] = {}
+        self.rotated: Dict[str, str] = {}
         self.hoisted_writes: Set[int] = set()
 
     # ---------------------------------------------------------- helpers
@@ -449,7 +457,7 @@ class KernelEmitter:
     # ---------------------------------------------------- access paths
     def fold(self, buf: Buffer, steps: List[Step]) -> Ref:
         dims, elem = split_array(buf.dtype)
-        steps = [("i", p) for p in buf.prefix] + list(steps)
+        steps = [("i", p() if callable(p) else p) for p in buf.prefix] + list(steps)
         k = len(dims)
         if len(steps) < k or any(t != "i" for t, _ in steps[:k]):
             raise CudaError(f"partial or malformed access to {buf.key}")
@@ -723,11 +731,13 @@ class KernelEmitter:
                 raise CudaError("a sequential loop around a grid-level parallel loop needs a "
                                 "grid-wide barrier per iteration (one kernel per iteration); "
                                 "not supported")
-            cands = []
-            if not self.per_thread and self.launch and trip is not None and trip > 1:
+            cands, rotate = [], False
+            if id(p) in self.for_plans:
+                cands, rotate = self.for_plans[id(p)], True
+            elif not self.per_thread and self.launch and trip is not None and trip > 1:
                 cands = self.pipeline_candidates(f.body, f.binder)
             if cands:
-                self.pipeline_prologue(cands, f.binder, targs[0], trip)
+                self.pipeline_prologue(cands, f.binder, targs[0], trip, rotate)
             self.loop("seq", 0, targs[0], f.binder, lambda: self.comm(f.body))
             return
         if name in PARFOR_FAMILY:
@@ -970,6 +980,7 @@ class KernelEmitter:
 
         def emit_body():
             if entering_wg:
+                self.plan_pipelines(body)
                 self.plan_uniform(body, loop=True, alias={ovar: acc_roots(a, {})})
             self.comm(body)
 
@@ -994,7 +1005,8 @@ class KernelEmitter:
                 raise CudaError(f"{prim}: work-item loop with no enclosing work-group loop")
 
     def plan_uniform(self, c: Phrase, loop: bool = False, alias=None, opaque=()):
-        planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes, opaque)
+        rotated = {fl.binder for cands in self.for_plans.values() for _n, _d, fl, _c1, _c2 in cands}
+        planner = BarrierPlanner(self.prog.is_shared, self.hoisted_writes, opaque, rotated)
         self.barriers |= planner.run(c, loop, alias)
 
     # -------------------------------------- software-pipelined staging
@@ -1049,9 +1061,41 @@ class KernelEmitter:
         walk(body)
         return found
 
-    def pipeline_prologue(self, cands, binder: str, n: Nat, trip: int):
+    def plan_pipelines(self, body: Phrase):
+        """Pipelining decisions for the uniform sequential loops of a
+        work-group loop body, made before barrier planning so the planner
+        knows which staged buffers rotate between two slices."""
+        if not self.launch:
+            return
+
+        def walk(q):
+            u = unapply(q)
+            if u is None:
+                return
+            name, targs, args = u
+            if name == ";":
+                walk(args[0].fst)
+                walk(args[0].snd)
+            elif _is_new(name) and isinstance(args[0], Lam):
+                walk(args[0].body)
+            elif name == "for" and isinstance(args[0], Lam):
+                trip = self.nat_int(targs[0])
+                if trip is not None and trip > 1:
+                    cands = self.pipeline_candidates(args[0].body, args[0].binder)
+                    if cands:
+                        self.for_plans[id(q)] = cands
+        walk(body)
+
+    def pipeline_prologue(self, cands, binder: str, n: Nat, trip: int, rotate: bool = False):
         for node, d0, fl, c1, c2 in cands:
-            buf = self._declare_local(fl.binder, d0)
+            if rotate:
+                # two slices, iteration k writes and reads slice k % 2
+                buf = self._declare_local(fl.binder, Array(nat(2), d0))
+                R = self.R
+                buf.prefix = [lambda b=binder: mod(self.env[b].ixv, 2, R)] + buf.prefix
+                self.rotated[fl.binder] = binder
+            else:
+                buf = self._declare_local(fl.binder, d0)
             self.env[fl.binder] = buf
             old = self.env.get(binder)
             self.env[binder] = Val(Idx(n), ixv=ix(0))
@@ -1360,8 +1404,9 @@ class ProgramEmitter:
             head.append(f"  const {it} dpia_gsize = ({it})gridDim.x * gridDim.y * dpia_nthreads;")
         text = "\n".join(head + body_lines + ["}"])
         info = KernelInfo(kname, "launch" if grid is not None else "single", args, ke.smem,
-                          grid is not None and bool(tail), grid, list(tail),
-                          frozenset(ke.barriers), frozenset(ke.hoisted), list(decls))
+                          grid is not None and bool(tail), grid_item=grid, tail_items=list(tail),
+                          barriers=frozenset(ke.barriers), hoisted=frozenset(ke.hoisted),
+                          rotated=dict(ke.rotated), decls=list(decls))
         return text, info
 
     def _kernel_names(self, grid, tail):

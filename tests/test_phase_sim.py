@@ -44,6 +44,10 @@ STRATS = [
      lambda: {"A": [_ints(256, 3 + r) for r in range(3)], "x": _ints(256, 11)}),
     ("mm", mm_program(16, 16, 16, 8, 4, 4), {}, ((2, 2), (2, 2)),
      lambda: {"A": [_ints(16, 3 + r) for r in range(16)], "B": [_ints(16, 5 + r) for r in range(16)]}),
+    # one vec4 staging load per work-item: the k-loop is software-pipelined
+    # and its shared tiles rotate between two slices (one barrier per k-step)
+    ("mm_pipelined", mm_program(16, 16, 16, 8, 2, 4), {}, ((2, 2), (2, 2)),
+     lambda: {"A": [_ints(16, 3 + r) for r in range(16)], "B": [_ints(16, 5 + r) for r in range(16)]}),
 ]
 
 
@@ -57,7 +61,8 @@ def test_benchmark_strategies_phase_exact(name, text, sigma, launch, mk):
 
 
 @pytest.mark.parametrize("name,text,sigma,launch,mk",
-                         [s for s in STRATS if s[0] in ("gemv", "mm")], ids=["gemv", "mm"])
+                         [s for s in STRATS if s[0] in ("gemv", "mm", "mm_pipelined")],
+                         ids=["gemv", "mm", "mm_pipelined"])
 def test_missing_barriers_are_detected(name, text, sigma, launch, mk):
     prog = compile_program(text)
     sim = Sim(prog.imperative, prog.params, mk(), launch, sigma)
@@ -65,5 +70,17 @@ def test_missing_barriers_are_detected(name, text, sigma, launch, mk):
     for k in sim.sig.kernels:
         k.barriers = frozenset()
         k.hoisted = frozenset()
+        k.rotated = {}
+    with pytest.raises(PhaseRace):
+        sim.run()
+
+
+def test_pipelined_mm_rotates_and_needs_one_barrier_per_k_step():
+    prog = compile_program(mm_program(16, 16, 16, 8, 2, 4))
+    sim = Sim(prog.imperative, prog.params, STRATS[-1][4](), ((2, 2), (2, 2)))
+    (k,) = sim.sig.kernels
+    assert len(k.rotated) == 2
+    # rotation without the planned barrier before the compute is a race
+    sim.sig.kernels[0].barriers = frozenset()
     with pytest.raises(PhaseRace):
         sim.run()
