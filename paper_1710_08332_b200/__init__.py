@@ -16,9 +16,10 @@ from .launcher import Executable, run_kernel  # noqa: F401
 from .cuda.hierarchy import HoistedBuffer, cuda_legal, hoist_allocations, lint_hierarchy  # noqa: F401
 from .api import Program, compile_program, executable, run_program_cuda  # noqa: F401
 from .checker import DpiaTypeError, type_check  # noqa: F401
+from .pretty import pretty_print  # noqa: F401
 
 __all__ = ["parse", "parse_phrase", "translate_program", "stage2", "emit_cuda", "run_kernel",
            "compile_program", "run_program_cuda", "executable", "CudaError", "ParseError",
            "ElabError", "SourceProgram", "Program", "Executable", "CudaSignature",
            "hoist_allocations", "lint_hierarchy", "cuda_legal", "HoistedBuffer",
-           "type_check", "DpiaTypeError"]
+           "type_check", "DpiaTypeError", "pretty_print"]

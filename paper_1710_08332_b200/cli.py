@@ -85,9 +85,10 @@ def _compile(args) -> int:
     prog = _load(args.file)
     base = Path(args.file).with_suffix("")
     if args.dump_stages:
-        Path(f"{base}.stage1.txt").write_text(repr(prog.stage1) + "\n")
-        Path(f"{base}.stage2.txt").write_text(repr(prog.imperative) + "\n")
-        print(f"wrote {base}.stage1.txt, {base}.stage2.txt")
+        from .pretty import show
+        Path(f"{base}.stage1.dpia").write_text(show(prog.stage1) + "\n")
+        Path(f"{base}.stage2.dpia").write_text(show(prog.imperative) + "\n")
+        print(f"wrote {base}.stage1.dpia, {base}.stage2.dpia")
     sigma = _parse_inputs(args.sizes) if args.sizes else None
     if sigma is not None:
         sigma = {n: int(sigma[n]) for n in prog.source.nat_params}

@@ -560,6 +560,19 @@ def _r_reducei(el, sx) -> Typed:
     return apply_prim("reduceI", [n, d1, d2], [f, init, e, c]), COMM
 
 
+def _r_reducei_init(el, sx) -> Typed:
+    _arity(sx, 5, "(reduceIInit F W E C)")
+    e, et = el.infer(sx[3])
+    n, d1 = _arr_exp(sx, et)
+    w, wt = el.infer(sx[2])
+    if not (isinstance(wt, FnT) and isinstance(wt.arg, AccT) and isinstance(wt.ret, CommT)):
+        raise error_at(sx, "reduceIInit initialiser must be (lam (o (acc T)) COMMAND)")
+    d2 = wt.arg.data
+    f = el._reduce_fn(sx[1], d1, d2, imperative=True)
+    c = el._command_fn(sx, sx[4], [ExpT(d2)], "reduceIInit consumer")
+    return apply_prim("reduceIInit", [n, d1, d2], [f, w, e, c]), COMM
+
+
 def _r_reducei_local(el, sx) -> Typed:
     _arity(sx, 5, "(reduceILocal F I E C)")
     e, et = el.infer(sx[3])
@@ -635,7 +648,7 @@ _RULES: Dict[str, Callable] = {
     "tuple": _r_tuple, "as": _r_as, "let": _r_let, "reduceLocal": _r_reduce_local, "zip": _r_zip, "split": _r_split,
     "join": _r_join, "transpose": _r_transpose, "pair": _r_pair, "fst": _r_pair_elim,
     "snd": _r_pair_elim, "idx": _r_idx, "seq": _r_seq, ":=": _r_assign, "for": _r_for,
-    "reduceI": _r_reducei, "reduceILocal": _r_reducei_local, "idxAcc": _r_idx_acc,
+    "reduceI": _r_reducei, "reduceIInit": _r_reducei_init, "reduceILocal": _r_reducei_local, "idxAcc": _r_idx_acc,
     "splitAcc": _r_split_acc, "joinAcc": _r_join_acc, "transposeAcc": _r_transpose_acc,
     "pairAcc1": _r_pair_acc(1), "pairAcc2": _r_pair_acc(2), "zipAcc1": _r_zip_acc(1),
     "zipAcc2": _r_zip_acc(2),

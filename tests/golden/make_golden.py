@@ -16,6 +16,8 @@ Outputs (committed; the GPU box never reads /root/reference):
   form (`hoist_allocations`, the input of `emit_kernel`) pretty-printed, with
   the typing environment needed to re-parse it.
   index.json     -- index-simplifier known answers (`codegen_c.simplify_index`).
+  fuzz_float.json -- the kernel-legal fuzz programs again on float inputs,
+                    with the reference's float64 `eval_phrase` result.
 """
 from __future__ import annotations
 
@@ -164,6 +166,37 @@ def main():
                      "expected": to_json(eval_phrase(sp.body, dict(inputs), {})),
                      "opencl_legal": legal, "simulated_2x2": sim, "hoisted": hoisted})
 
+    # float mode: the same kernel-legal fuzz programs on float inputs, with
+    # the reference's float64 eval_phrase result
+    import random as _random
+    fuzz_float = []
+    for c in fuzz:
+        if not (c["opencl_legal"] and c["reparses"]):
+            continue
+        sp = parse(c["text"])
+        rng = _random.Random(c["seed"] ^ 0xF10A7)
+
+        def rand_f(d):
+            from dpia.types import Array as RArr, Num as RNum, Pair as RPair, Vector as RVec
+            if isinstance(d, RNum):
+                return round(rng.uniform(-2, 2), 3)
+            if isinstance(d, RVec):
+                return VectorVal(tuple(round(rng.uniform(-2, 2), 3) for _ in range(d.width)))
+            if isinstance(d, RArr):
+                from dpia.nat import nat_const_value
+                return [rand_f(d.elem) for _ in range(nat_const_value(d.size))]
+            if isinstance(d, RPair):
+                return (rand_f(d.fst), rand_f(d.snd))
+            raise ValueError(d)
+        finputs = {n: rand_f(t.data) for n, t in sp.params}
+        try:
+            want = eval_phrase(sp.body, dict(finputs), {})
+        except ZeroDivisionError:
+            continue
+        fuzz_float.append({"seed": c["seed"], "text": c["text"], "float": True,
+                           "inputs": {k: to_json(v) for k, v in finputs.items()},
+                           "expected": to_json(want)})
+
     from dpia.c_ast import CBin, CInt, CVar, expr_str
     from dpia.codegen_c import simplify_index
     i, j, k = CVar("i"), CVar("j"), CVar("k")
@@ -190,7 +223,8 @@ def main():
     index = [{"expr": sexp(e), "ranges": r, "reference_simplified": expr_str(simplify_index(e, r))}
              for e, r in idx_cases]
 
-    for fname, obj in (("programs.json", cases), ("fuzz.json", fuzz), ("index.json", index)):
+    for fname, obj in (("programs.json", cases), ("fuzz.json", fuzz), ("index.json", index),
+                       ("fuzz_float.json", fuzz_float)):
         with open(os.path.join(HERE, fname), "w") as f:
             json.dump(obj, f, indent=None, separators=(",", ":"))
             f.write("\n")

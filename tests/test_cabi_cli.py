@@ -107,3 +107,16 @@ def test_criterion3_analogue_cuda_kernel_text():
                    "dpia::vload<float, 4>", "dpia::vstore<float, 4>", "dpia::vec<float, 4> acc"):
         assert needle in src, needle
     assert [k.name for k in sig.kernels] == ["dotvec_k0"]
+
+
+def test_cli_dump_stages_reparse(tmp_path):
+    from conftest import load_golden
+    from paper_1710_08332_b200.dtypes import AccT
+    from paper_1710_08332_b200.reader import parse, parse_phrase
+    case = [c for c in load_golden("programs.json") if c["name"] == "dottiled.dpia"][0]
+    f = _prog(tmp_path, case["text"], "dottiled.dpia")
+    assert main(["compile", f, "--dump-stages"]) == 0
+    sp = parse(case["text"])
+    env = {**dict(sp.params), "out": AccT(sp.body_type.data)}
+    for stage in ("stage1", "stage2"):
+        parse_phrase(open(str(tmp_path / f"dottiled.{stage}.dpia")).read(), env)

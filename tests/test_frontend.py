@@ -291,3 +291,52 @@ def test_benchmark_strategies_type_check():
         t, _ = type_check(s1, delta=sp.delta, pi=sp.pi,
                           gamma={**sp.gamma, "out": AccT(sp.body_type.data)})
         assert t == COMM_T
+
+
+@pytest.mark.parametrize("case", load_golden("fuzz_float.json"), ids=lambda c: f"fseed{c['seed']}")
+def test_float_mode_oracle_matches_reference(case):
+    """float64 oracle == the reference's float64 eval_phrase on the fuzz corpus."""
+    import math
+    sp = parse(case["text"])
+    got = eval_phrase(sp.body, {k: from_json(v) for k, v in case["inputs"].items()})
+    g = to_json(got)
+
+    def close(a, b):
+        if isinstance(a, list):
+            return len(a) == len(b) and all(close(x, y) for x, y in zip(a, b))
+        if isinstance(a, dict):
+            return all(close(a[k], b[k]) for k in a)
+        return math.isclose(a, b, rel_tol=1e-12, abs_tol=1e-12)
+    assert close(g, case["expected"])
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c.get("reparses", True)][::4], ids=_id)
+def test_pretty_print_round_trips_every_stage(case):
+    """show(p) re-parses to an alpha-equivalent phrase for the source, the
+    Stage I and the Stage II forms (the reference's printer round-trip,
+    TST/test_parser.py:173-187)."""
+    from paper_1710_08332_b200.pretty import show
+    from paper_1710_08332_b200.terms import alpha_equal
+    sp = parse(case["text"])
+    env = dict(sp.params)
+    p1, _ = parse_phrase(show(sp.body), env)
+    assert alpha_equal(p1, sp.body)
+    env_out = {**env, "out": AccT(sp.body_type.data)}
+    s1 = translate_program(sp.body, sp.body_type.data, "out", "global")
+    q1, _ = parse_phrase(show(s1), env_out)
+    assert alpha_equal(q1, s1)
+    s2 = stage2(s1, "private")
+    q2, _ = parse_phrase(show(s2), env_out)
+    assert alpha_equal(q2, s2)
+
+
+def test_pretty_print_benchmark_strategies():
+    from paper_1710_08332_b200.bench_programs import dot_program, gemv_program, mm_program
+    from paper_1710_08332_b200.pretty import show
+    from paper_1710_08332_b200.terms import alpha_equal
+    for text in (dot_program(64, 4), gemv_program(8, 512, 64), mm_program(64, 64, 64, 32, 8, 4)):
+        sp = parse(text)
+        env = dict(sp.params)
+        for ph in (sp.body, translate_program(sp.body, sp.body_type.data, "out", "global")):
+            q, _ = parse_phrase(show(ph), {**env, "out": AccT(sp.body_type.data)})
+            assert alpha_equal(q, ph)

@@ -221,3 +221,18 @@ def test_unspecialised_kernels(case, launch):
         assert np.allclose(got, want, rtol=1e-5, atol=1e-5)
     else:
         assert [int(v) for v in got] == want
+
+
+FUZZ_FLOAT = load_golden("fuzz_float.json")
+
+
+@pytest.mark.parametrize("case", FUZZ_FLOAT, ids=lambda c: f"fseed{c['seed']}")
+def test_reference_fuzz_programs_fp32(case):
+    """Kernel-legal reference fuzz programs in float mode: the fp32 kernel
+    against the reference's float64 result (short expressions of values in
+    [-2, 2]: |got - want| <= 1e-3 + 1e-4 |want|)."""
+    prog = compile_program(case["text"])
+    inputs = {k: from_json(v) for k, v in case["inputs"].items()}
+    got = run_program_cuda(prog, inputs, launch=(2, 4), float_mode=True, flat=True)
+    want = flatten_value(from_json(case["expected"]))
+    assert np.allclose(np.asarray(got, np.float64), np.asarray(want, np.float64), rtol=1e-4, atol=1e-3)
