@@ -455,7 +455,9 @@ def main():
                      else "synthetic (numpy default_rng uniform, resident in HBM)"),
             "config": _cfg_desc(cfg, world),
             "roofline": head["roofline"], "e2e": head.get("e2e"), "clocks": head["clocks"],
-            "gpu_launches": args.steps * len(exe.sig.kernels),
+            "gpu_launches": args.steps * (len(exe.sig.kernels) + 1),
+            "gpu_launches_breakdown": {"emitted program kernels": args.steps * len(exe.sig.kernels),
+                                       "dpia_l2_scrub (libdpia_rt, between steps)": args.steps},
             "kernels": exe.kernel_names(),
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
                              if cpu else None),

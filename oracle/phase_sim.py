@@ -24,7 +24,7 @@ from typing import Dict, List, Optional, Tuple
 from paper_1710_08332_b200.cuda.emit import emit_cuda, normalize_launch
 from paper_1710_08332_b200.dtypes import Array, Idx, Num, Pair, Vector
 from paper_1710_08332_b200.signatures import LOOP_LEVEL, NEW_SPACE, PARFOR_FAMILY
-from paper_1710_08332_b200.terms import Lam, Lit, PairP, Proj, Var, unapply
+from paper_1710_08332_b200.terms import Lam, Lit, Proj, Var, unapply
 
 from .dpia_eval import Vec, binop, c_divide, unop
 from .imp_eval import leaves

@@ -20,7 +20,7 @@ the multi-GPU driver may split the outer parallel loop across devices.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 from typing import Dict, FrozenSet, Optional, Tuple
 
 from .dtypes import (AccT, Array, CommT, DataType, DataVar, DepFnT, ExpT, FnT, Idx, Num,

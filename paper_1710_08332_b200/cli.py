@@ -16,7 +16,7 @@ import argparse
 import ast
 import sys
 from pathlib import Path
-from typing import Dict, List, Optional, Tuple
+from typing import Dict, List, Optional
 
 from .api import compile_program
 from .checker import DpiaTypeError

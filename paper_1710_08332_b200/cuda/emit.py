@@ -36,7 +36,6 @@ Additions over the reference backend (SURVEY.md sections 0 and 7):
 """
 from __future__ import annotations
 
-import hashlib
 import os
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Set, Tuple, Union
@@ -383,9 +382,7 @@ class KernelEmitter:
         self.single_thread = False
         self.used_scratch: Set[str] = set()
         self._k = 0
-        self.counter = False
         self.uses_gid = False
-        self.uniform_decl: Dict[str, bool] = {}
         self.hoisted: Dict[int, Buffer] = {}
         self.decl_depth: Dict[str, int] = {}
         self.pf = None
@@ -932,7 +929,7 @@ class KernelEmitter:
             self.open("")
             self.line(f"const int {v} = 0;")
         else:
-            if level == "seq" and trip is not None and trip <= UNROLL_LIMIT and self._small_body(body):
+            if level == "seq" and trip is not None and trip <= UNROLL_LIMIT:
                 self.line("#pragma unroll")
             self.open(f"for ({ctype} {v} = {start}; {v} < {bound}; {v} += {stride})")
         self.loops.append(lp)
@@ -951,9 +948,6 @@ class KernelEmitter:
                 self.env[nm] = ov
         self.loops.pop()
         self.close()
-
-    def _small_body(self, body) -> bool:
-        return True
 
     def parfor(self, prim: str, targs, args):
         n, d = targs
@@ -1437,7 +1431,6 @@ class ProgramEmitter:
     def _kernel_body(self, ke: KernelEmitter, grid, tail, decls):
         saved_env = {}
         for space, binder, d in decls:
-            lam = Lam(binder, Prim("skip"))
             # declare kernel-level buffers (top-level local / private)
             if space == "local":
                 n = ke._elements(d)
@@ -1448,7 +1441,6 @@ class ProgramEmitter:
                 cname = ke.fresh(binder)
                 ke.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
                 saved_env[binder] = Buffer(binder, cname, "local", d)
-            del lam
         ke.env.update(saved_env)
         if grid is not None:
             self.in_tail = False
@@ -1458,7 +1450,6 @@ class ProgramEmitter:
         if tail:
             self.in_tail = True
             if grid is not None:
-                ke.counter = True
                 ke.line("__shared__ bool dpia_last;")
                 ke.open("if (dpia::grid_arrive(dpia_counter, dpia_tid, &dpia_last))")
             for space, binder, d in decls:
@@ -1548,7 +1539,3 @@ def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple
     thread slicing and compile-time index arithmetic."""
     del simplify  # subscripts are always range-simplified
     return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new).emit(p)
-
-
-def source_hash(src: str, opts: str = "") -> str:
-    return hashlib.sha256((src + "\0" + opts).encode()).hexdigest()[:24]

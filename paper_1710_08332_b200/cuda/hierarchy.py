@@ -22,7 +22,7 @@ from typing import List, Tuple
 
 from ..dtypes import Array, DataType
 from ..signatures import LOOP_LEVEL, NEW_SPACE, PARFOR_FAMILY
-from ..terms import (App, Lam, PairP, Phrase, Proj, Var, apply_prim, beta_normalize,
+from ..terms import (Lam, PairP, Phrase, Proj, Var, apply_prim, beta_normalize,
                      children, rebuild, substitute, unapply)
 
 

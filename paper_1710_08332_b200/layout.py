@@ -11,7 +11,7 @@ contiguous scalar arrays and marshal without any scatter.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Optional, Tuple
+from typing import List, Tuple
 
 import numpy as np
 

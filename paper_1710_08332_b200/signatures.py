@@ -22,7 +22,7 @@ SURVEY.md section 0 finding 1):
 """
 from __future__ import annotations
 
-from typing import Dict, List, Optional, Tuple
+from typing import Dict, Optional, Tuple
 
 from .dtypes import (NUM, AccT, Array, CommT, DataVar, DepFnT, ExpT, FnT, Idx,
                      Pair, PhraseType, ProdT, VECTOR_WIDTHS, Vector, var_t)
