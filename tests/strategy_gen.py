@@ -1,0 +1,103 @@
+"""Random hierarchical DPIA strategy programs (test infrastructure).
+
+The reference fuzzer (SRC/harness.py:37-247) never emits work-group/work-item
+nests with local staging, so it cannot exercise most of the CUDA backend.
+This generator builds seeded, well-typed programs in the shape of the
+benchmark strategies -- mapWorkgroup over chunks, mapLocal over columns,
+toLocal / toPrivate staging, let, transpose, reduceSeq / reduceLocal,
+vec4 views, 2-D work-groups -- with small random element expressions, plus
+inputs and a launch geometry.  Values are small integers so int-mode results
+are exact.
+"""
+from __future__ import annotations
+
+import random
+
+
+def _expr(rng: random.Random, x: str, depth: int = 2) -> str:
+    """Random integer-preserving expression that mentions the variable x
+    (so its type is x's type: literals only ever appear as bare operands,
+    which adopt the other operand's type)."""
+    if depth == 0 or rng.random() < 0.3:
+        return x
+    op = rng.choice(["+", "-", "*", "abs", "negate"])
+    if op in ("abs", "negate"):
+        return f"({op} {_expr(rng, x, depth - 1)})"
+    a = _expr(rng, x, depth - 1)
+    b = str(rng.randint(-3, 3)) if rng.random() < 0.5 else _expr(rng, x, depth - 1)
+    return f"({op} {a} {b})" if rng.random() < 0.5 else f"({op} {b} {a})"
+
+
+def generate(seed: int):
+    """(text, inputs, sigma, launch, description)."""
+    rng = random.Random(seed)
+    L = rng.choice([32, 64])
+    K = rng.choice([1, 2, 3])
+    chunks = rng.choice([1, 2, 3, 5])
+    vec = rng.random() < 0.35
+    two = rng.random() < 0.4            # zip of two inputs
+    w = 4 if vec else 1
+    C = L * K                            # elements (or vec4s) per chunk
+    N = chunks * C * w
+    elem_t = "(vec 4)" if vec else "num"
+    src = "(asVector4 xs)" if vec else "xs"
+    if two:
+        src = f"(zip {src} {'(asVector4 ys)' if vec else 'ys'})"
+        elem_t = f"(pair {elem_t} {elem_t})"
+        x_expr = lambda v: f"(* (fst {v}) (snd {v}))"  # noqa: E731
+    else:
+        x_expr = lambda v: v  # noqa: E731
+    params = f"(param xs (exp (array {N} num)))\n" + (f"(param ys (exp (array {N} num)))\n" if two else "")
+    acc_t = "(vec 4)" if vec else "num"
+    shape = rng.choice(["reduce", "reduce", "map", "stage", "let", "rows"])
+    top_combine = shape == "reduce" and rng.random() < 0.6
+    e = _expr(rng, "v")
+    if shape == "reduce":
+        body = (f"(reduceLocal (+) 0 (toPrivate (mapLocal (lam (col (exp (array {K} {elem_t})))"
+                f" (reduceSeq (lam (p (exp {elem_t})) (lam (a (exp {acc_t}))"
+                f" (+ a (let {x_expr('p')} (lam (v (exp {acc_t})) {e})))))"
+                f" 0 col))) (transpose (split {L} chunk))))")
+        out_t = acc_t
+    elif shape == "map":
+        body = f"(mapLocal (lam (q (exp {elem_t})) (let {x_expr('q')} (lam (v (exp {acc_t})) {e}))) chunk)"
+        out_t = f"(array {C} {acc_t})"
+    elif shape == "stage":
+        e2 = _expr(rng, "u")
+        body = (f"(mapLocal (lam (u (exp {acc_t})) {e2})"
+                f" (toLocal (mapLocal (lam (q (exp {elem_t})) (let {x_expr('q')} (lam (v (exp {acc_t})) {e}))))"
+                f" chunk))")
+        out_t = f"(array {C} {acc_t})"
+    elif shape == "let":
+        e2 = _expr(rng, "u")
+        body = (f"(let (toLocal (mapLocal (lam (q (exp {elem_t})) (let {x_expr('q')}"
+                f" (lam (v (exp {acc_t})) {e})))) chunk)"
+                f" (lam (s (exp (array {C} {acc_t})))"
+                f" (join (mapLocal (lam (r (exp (array {K} {acc_t})))"
+                f" (mapSeq (lam (u (exp {acc_t})) {e2}) r)) (transpose (split {L} s))))))")
+        out_t = f"(array {C} {acc_t})"
+    else:  # rows: per work-item sequential reduce over a contiguous row, staged partials
+        body = (f"(reduceLocal (+) 0 (toPrivate (mapLocal (lam (row (exp (array {K} {elem_t})))"
+                f" (reduceSeq (lam (p (exp {elem_t})) (lam (a (exp {acc_t})) (+ a {x_expr('p')}))) 0 row)))"
+                f" (split {K} chunk)))")
+        out_t = acc_t
+    prog = (f"(mapWorkgroup (lam (chunk (exp (array {C} {elem_t}))) {body})"
+            f" (split {C} {src}))")
+    if shape in ("map", "stage", "let"):
+        prog = f"(join {prog})"
+        if vec:
+            prog = f"(asScalar4 {prog})"
+    elif vec:
+        prog = f"(asScalar4 {prog})"
+    if top_combine:
+        prog = f"(reduceLocal (+) 0 {prog})"
+    text = params + prog
+    r2 = random.Random(seed ^ 0xBEEF)
+    inputs = {"xs": [r2.randint(-5, 5) for _ in range(N)]}
+    if two:
+        inputs["ys"] = [r2.randint(-5, 5) for _ in range(N)]
+    combine = "reduceLocal" in text
+    Ls = [L] if combine else [L, max(1, L // 2), L * 2]
+    launch = (rng.choice([1, 2, 3, chunks]), rng.choice(Ls))
+    desc = f"{shape}{'+vec4' if vec else ''}{'+zip' if two else ''}{'+top' if top_combine else ''} L={L} K={K}"
+    del out_t
+    return text, inputs, {}, launch, desc

@@ -1,0 +1,33 @@
+"""Differential fuzzing of the CUDA backend on random hierarchical strategy
+programs (tests/strategy_gen.py) -- SURVEY.md 8f row f2 extended to the
+primitives the reference's fuzzer never generates.  Oracle: the eval_phrase
+restatement (pinned to the reference's golden vectors); int mode, exact."""
+import pytest
+
+from oracle.dpia_eval import eval_phrase, flatten_value
+from oracle.phase_sim import simulate
+from paper_1710_08332_b200 import compile_program
+from strategy_gen import generate
+
+
+def _case(seed):
+    text, inputs, sigma, launch, desc = generate(seed)
+    prog = compile_program(text)
+    want = flatten_value(eval_phrase(prog.source.body, inputs, sigma))
+    return prog, inputs, sigma, launch, want
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_strategy_fuzz_phase_simulator(seed):
+    prog, inputs, sigma, launch, want = _case(seed)
+    got = simulate(prog.imperative, prog.params, inputs, launch, sigma)["out"]
+    assert flatten_value(got) == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(400))
+def test_strategy_fuzz_gpu(seed):
+    from paper_1710_08332_b200 import run_program_cuda
+    prog, inputs, sigma, launch, want = _case(seed)
+    got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=False, flat=True)
+    assert [int(v) for v in got] == want
