@@ -214,34 +214,36 @@ def run_timed(exe, stream, steps, flush=True, allreduce=None):
 
 
 def e2e_measure(exe, inputs, stream, steps):
-    """Public-API path with host buffers: H2D of the step's inputs from pinned
-    memory, the kernels, D2H of the result -- all inside the timed events."""
+    """The public API end to end with host buffers: `Executable.run` copies
+    the step's inputs from page-locked host memory, launches the program and
+    copies the result back to page-locked host memory, synchronising before
+    it returns -- all inside the timed events."""
     from paper_1710_08332_b200 import layout as LY
     dev = exe.device
-    pinned, h2d = {}, 0
+    pinned, host, h2d = [], {}, 0
     for n, d in exe.sig.inputs:
         img = LY.to_bytes(inputs[n], d, exe.sigma, True)
         pb = RT.PinnedBuffer(img.nbytes)
-        pb.array(np.uint8, img.nbytes)[:] = img
-        pinned[n] = (pb, img.nbytes)
+        arr = pb.array(np.float32, img.nbytes // 4)
+        arr[:] = img.view(np.float32)
+        pinned.append(pb)
+        host[n] = arr
         h2d += img.nbytes
     outn, outd = exe.sig.outputs[0]
     d2h = LY.nbytes(outd, exe.sigma, True)
     ob = RT.PinnedBuffer(d2h)
+    pinned.append(ob)
+    res = {outn: ob.array(np.float32, d2h // 4)}
     times = []
     for _ in range(steps + 1):
         e0, e1 = RT.Event(dev), RT.Event(dev)
         e0.record(stream)
-        for n, (pb, nb) in pinned.items():
-            RT.lib().dpia_memcpy_htod(dev, exe.buffers[n].ptr, pb.ptr, nb, stream.handle)
-        exe.launch(stream)
-        RT.lib().dpia_memcpy_dtoh(dev, ob.ptr, exe.buffers[outn].ptr, d2h, stream.handle)
+        exe.run(host, stream, out=res)
         e1.record(stream)
         stream.sync()
         times.append(e0.elapsed_ms(e1))
-    for pb, _ in pinned.values():
+    for pb in pinned:
         pb.free()
-    ob.free()
     return statistics.mean(times[1:]), h2d, d2h
 
 
@@ -285,6 +287,19 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None):
         fn.argtypes = [vp, vp, vp]
         call = lambda: fn(out.ctypes.data, A.ctypes.data, x.ctypes.data)  # noqa: E731
         nbytes, sample = 4 * (8192 * 8192 + 2 * 8192), "gemv 8192x8192 fp32, full size"
+    elif workload == "mm":
+        A, B = _seeded((4096, 4096), 5, -1.0, 1.0), _seeded((4096, 4096), 6, -1.0, 1.0)
+        Bt = np.ascontiguousarray(B.T)
+        big = np.zeros(4096 * 4096, np.float32)
+        fn = lib.mm_bt
+        fn.argtypes = [vp, vp, vp]
+        call = lambda: fn(big.ctypes.data, A.ctypes.data, Bt.ctypes.data)  # noqa: E731
+        flops = 2 * 4096 ** 3
+        sample = ("mm 4096^3 fp32, full size, B passed pre-transposed (the reference language has "
+                  "no transpose)")
+        min_seconds, max_reps = 0.0, 2
+        steps = None if steps is None else min(steps, 2)  # ~5 s per call on 16 threads
+        nbytes = None
     else:
         return None
     call()
@@ -299,6 +314,12 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None):
         if steps is None and (time.perf_counter() - t_start > min_seconds or len(times) >= max_reps):
             break
     best = min(times)
+    if nbytes is None:  # mm: flop rate
+        return {"value": round(flops / statistics.median(times) / 1e9, 3), "unit": "GFLOP/s",
+                "cores": int(lib.ref_threads()), "kind": "reference",
+                "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
+                          f"median of {len(times)} calls",
+                "ms_per_call": round(1e3 * statistics.median(times), 4)}
     return {"value": round(nbytes / statistics.median(times) / 1e9, 3), "unit": "GB/s",
             "cores": int(lib.ref_threads()), "kind": "reference",
             "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
@@ -424,10 +445,11 @@ def main():
                "value": value, "roofline": roof}
         if with_e2e and inputs is not None:
             e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
-            res["e2e"] = {"value": round(cfg.bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            work, unit = (cfg.flops, "GFLOP/s") if workload == "mm" else (cfg.bytes, "GB/s")
+            res["e2e"] = {"value": round(work / (e2e_ms * 1e-3) / 1e9, 3), "unit": unit,
                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                           "ms_per_step": round(e2e_ms, 4),
-                          "path": "run_kernel public API: pinned H2D + kernels + D2H"}
+                          "path": "Executable.run (public API): pinned H2D + kernels + D2H + stream sync"}
         return res
 
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
@@ -436,10 +458,14 @@ def main():
         for w in ("dot", "asum", "gemv", "mm", "scal"):
             if w == args.workload:
                 continue
-            r = measure(w, min(args.steps, 20), 3, with_e2e=False)
+            r = measure(w, min(args.steps, 20), 3, with_e2e=True)
             suite[w] = {"value": round(r["value"], 1), "unit": "GFLOP/s" if w == "mm" else "GB/s",
                         "ms_per_step": round(r["mean_ms"], 5), "roofline": r["roofline"],
-                        "clocks": r["clocks"], "config": _cfg_desc(r["cfg"])}
+                        "e2e": r.get("e2e"), "clocks": r["clocks"], "config": _cfg_desc(r["cfg"])}
+            if not args.no_cpu:
+                c = cpu_reference(w)
+                suite[w]["cpu_baseline"] = ({k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                                            if c else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference(args.workload)
@@ -479,7 +505,7 @@ def _cfg_desc(cfg, world=1):
                          "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
                                "tiles, toLocal k-tiles of 8"}[cfg.name],
             "sigma": cfg.sigma, "launch": list(cfg.launch),
-            "l2": "flushed between steps (2x L2 memset, outside the timed events)"}
+            "l2": "scrubbed between steps (a read of 2x L2 by dpia_l2_scrub, outside the timed events)"}
 
 
 if __name__ == "__main__":

@@ -325,6 +325,13 @@ class BarrierPlanner:
         if uniform_loop:
             if name == "for":
                 body = args[0].body
+                # a hazard between the code before a sequential loop and its
+                # body is fenced once, before the loop, not on every
+                # iteration (loop-carried hazards are found by the second pass)
+                R, W = rw_sets(body, alias)
+                R = {n for n in R if self.shared(n)}
+                W = {n for n in W if self.shared(n)}
+                st = self._hazard(c, st, R, W)
             else:
                 body = args[1].body.body
                 alias = {**alias, args[1].body.binder: acc_roots(args[0], alias)}
@@ -1004,7 +1011,7 @@ class KernelEmitter:
         self.barriers |= planner.run(c, loop, alias)
 
     # -------------------------------------- software-pipelined staging
-    def pipeline_candidates(self, body: Phrase, binder: str):
+    def pipeline_candidates(self, body: Phrase, binder: str, extra_ix: Set[str] = frozenset()):
         """newLocal stagings at the top level of a work-group-uniform
         sequential loop body whose initialising command only copies from
         read-only inputs through single-iteration work-item loops.  Their
@@ -1048,6 +1055,7 @@ class KernelEmitter:
                     R1, W1 = rw_sets(c1)
                     free = free_vars(c1) - {fl.binder}
                     outer_ix = {nm for nm, b in self.env.items() if isinstance(b, Val) and b.ixv is not None}
+                    outer_ix |= extra_ix
                     if W1 == {fl.binder} and free <= inputs | {binder} | outer_ix and simple(c1):
                         found.append((q, targs[0], fl, c1, c2))
                 walk(fl.body)
@@ -1062,23 +1070,29 @@ class KernelEmitter:
         if not self.launch:
             return
 
-        def walk(q):
+        def walk(q, extra):
             u = unapply(q)
             if u is None:
                 return
             name, targs, args = u
             if name == ";":
-                walk(args[0].fst)
-                walk(args[0].snd)
+                walk(args[0].fst, extra)
+                walk(args[0].snd, extra)
             elif _is_new(name) and isinstance(args[0], Lam):
-                walk(args[0].body)
+                walk(args[0].body, extra)
+            elif name in PARFOR_FAMILY and LOOP_LEVEL[name][0] == "workgroup" and \
+                    len(args) == 2 and isinstance(args[1], Lam) and isinstance(args[1].body, Lam):
+                # a nested work-group loop (2-D hierarchy): its index is a
+                # work-group-uniform value inside, so plan its loops now,
+                # so this level's barrier plan already sees the rotation
+                walk(args[1].body.body, extra | {args[1].binder})
             elif name == "for" and isinstance(args[0], Lam):
                 trip = self.nat_int(targs[0])
                 if trip is not None and trip > 1:
-                    cands = self.pipeline_candidates(args[0].body, args[0].binder)
+                    cands = self.pipeline_candidates(args[0].body, args[0].binder, extra)
                     if cands:
                         self.for_plans[id(q)] = cands
-        walk(body)
+        walk(body, frozenset())
 
     def pipeline_prologue(self, cands, binder: str, n: Nat, trip: int, rotate: bool = False):
         for node, d0, fl, c1, c2 in cands:

@@ -102,6 +102,31 @@ class Executable:
             fn = self.module.function(k.name)
             RT.launch(fn, self.device, grid, l, k.smem, vals, stream)
 
+    def run(self, inputs: Dict[str, object], stream: Optional[RT.Stream] = None,
+            out: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:
+        """One end-to-end execution from host buffers: copy every input to
+        the device, launch the program, copy every out/var parameter back,
+        synchronise.  Results are flat scalar leaves (numpy).  Host arrays in
+        page-locked memory (`runtime.PinnedBuffer.array`) make both copies
+        direct DMA; `out` may supply such arrays for the results."""
+        for n, _d in self.sig.inputs:
+            self.upload(n, inputs[n], stream)
+        self.launch(stream)
+        res = {}
+        for n, d in self.sig.outputs:
+            size, _, dense = LY.shape_of(d, self.sigma, 4 if self.float_mode else 8)
+            dst = (out or {}).get(n)
+            if dense and dst is not None:
+                self.buffers[n].download(dst.reshape(-1).view(np.uint8)[:size], stream)
+                res[n] = dst
+            else:
+                res[n] = self.download(n, stream)
+        if stream is not None:
+            stream.sync()
+        else:
+            RT.lib().dpia_device_sync(self.device)
+        return res
+
     def kernel_names(self) -> List[str]:
         return [k.name for k in self.sig.kernels]
 

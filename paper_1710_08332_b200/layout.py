@@ -64,6 +64,34 @@ def layout(d: DataType, sigma=None, scalar_bytes: int = 4) -> Layout:
     raise TypeError(f"no layout for {d}")
 
 
+def shape_of(d: DataType, sigma=None, scalar_bytes: int = 4) -> Tuple[int, int, bool]:
+    """(size, align, dense) of type d without materialising per-leaf offsets:
+    dense means the leaves are consecutive scalars of one kind (num), so the
+    device image of a value is its flat scalar array (no scatter)."""
+    sigma = sigma or {}
+    s = scalar_bytes
+    if isinstance(d, Num):
+        return s, s, True
+    if isinstance(d, Idx):
+        return 8, 8, False
+    if isinstance(d, Vector):
+        a = _vec_align(d.width, s)
+        size = -(-s * d.width // a) * a
+        return size, a, size == s * d.width
+    if isinstance(d, Array):
+        n = d.size.evaluate(sigma)
+        size, a, dense = shape_of(d.elem, sigma, s)
+        return n * size, a, dense
+    if isinstance(d, Pair):
+        sa, aa, da = shape_of(d.fst, sigma, s)
+        sb, ab, db = shape_of(d.snd, sigma, s)
+        ob = -(-sa // ab) * ab
+        al = max(aa, ab)
+        size = -(-(ob + sb) // al) * al
+        return size, al, da and db and ob == sa and size == sa + sb
+    raise TypeError(f"no layout for {d}")
+
+
 def flatten(v) -> List:
     """Scalar leaves of a value in layout order."""
     if hasattr(v, "items") and not isinstance(v, (list, tuple, dict)):
@@ -101,12 +129,18 @@ def _py(x):
 def to_bytes(v, d: DataType, sigma, float_mode: bool) -> np.ndarray:
     """Device image (uint8) of value v (nested value or numpy array of leaves)."""
     s = 4 if float_mode else 8
+    sdt = np.float32 if float_mode else np.int64
+    size, _, dense = shape_of(d, sigma, s)
+    if dense and isinstance(v, np.ndarray):
+        # fast path (no per-leaf offsets): a flat scalar array is the image
+        if v.size * s != size:
+            raise ValueError(f"value has {v.size} scalars, type {d} needs {size // s}")
+        return np.ascontiguousarray(v.reshape(-1), dtype=sdt).view(np.uint8)
     lay = layout(d, sigma, s)
     leaves = np.asarray(v).ravel() if isinstance(v, np.ndarray) else np.asarray(flatten(v))
     n = lay.offsets.size
     if leaves.size != n:
         raise ValueError(f"value has {leaves.size} scalars, type {d} needs {n}")
-    sdt = np.float32 if float_mode else np.int64
     if not lay.kinds.any() and (n == 0 or (lay.offsets[-1] == (n - 1) * s and lay.size == n * s)):
         return np.ascontiguousarray(leaves, dtype=sdt).view(np.uint8)
     buf = np.zeros(lay.size, np.uint8)
@@ -123,9 +157,12 @@ def to_bytes(v, d: DataType, sigma, float_mode: bool) -> np.ndarray:
 def from_bytes(raw: np.ndarray, d: DataType, sigma, float_mode: bool) -> np.ndarray:
     """Leaves (float64 / int64 numpy array) of a device image."""
     s = 4 if float_mode else 8
+    sdt = np.float32 if float_mode else np.int64
+    size, _, dense = shape_of(d, sigma, s)
+    if dense:
+        return raw[:size].view(sdt).copy()
     lay = layout(d, sigma, s)
     n = lay.offsets.size
-    sdt = np.float32 if float_mode else np.int64
     if not lay.kinds.any() and (n == 0 or (lay.offsets[-1] == (n - 1) * s and lay.size == n * s)):
         return raw[:n * s].view(sdt).copy()
     out = np.zeros(n, np.float64 if float_mode else np.int64)
@@ -139,4 +176,4 @@ def from_bytes(raw: np.ndarray, d: DataType, sigma, float_mode: bool) -> np.ndar
 
 
 def nbytes(d: DataType, sigma, float_mode: bool) -> int:
-    return layout(d, sigma, 4 if float_mode else 8).size
+    return shape_of(d, sigma, 4 if float_mode else 8)[0]

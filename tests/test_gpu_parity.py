@@ -236,3 +236,34 @@ def test_reference_fuzz_programs_fp32(case):
     got = run_program_cuda(prog, inputs, launch=(2, 4), float_mode=True, flat=True)
     want = flatten_value(from_json(case["expected"]))
     assert np.allclose(np.asarray(got, np.float64), np.asarray(want, np.float64), rtol=1e-4, atol=1e-3)
+
+
+def test_executable_run_pinned_repeated():
+    """Executable.run (the end-to-end call bench.py's e2e leg times): inputs
+    from page-locked host memory, result into page-locked host memory, same
+    answers on every repetition (the fused grid combine resets its counter)."""
+    from paper_1710_08332_b200 import executable
+    from paper_1710_08332_b200 import runtime as RT
+    cfg = dot_config(N=1 << 20, L=256, K=16)
+    exe = executable(compile_program(cfg.text), cfg.launch, cfg.sigma, float_mode=True)
+    st = RT.Stream(0)
+    bufs = [RT.PinnedBuffer(4 << 20) for _ in range(2)] + [RT.PinnedBuffer(16)]
+    xs, ys = bufs[0].array(np.float32, 1 << 20), bufs[1].array(np.float32, 1 << 20)
+    out = {"out": bufs[2].array(np.float32, 1)}
+    try:
+        for seed in range(3):
+            xs[:] = blas_np.seeded(1 << 20, 10 + seed, 0.0, 1.0)
+            ys[:] = blas_np.seeded(1 << 20, 20 + seed, 0.0, 1.0)
+            res = exe.run({"xs": xs, "ys": ys}, st, out=out)
+            want, absterms = blas_np.dot(np.array(xs), np.array(ys))
+            assert res["out"] is out["out"]
+            assert blas_np.within(float(res["out"][0]), want, absterms)
+        # int mode, pageable numpy inputs, result allocated by run()
+        ie = executable(compile_program(cfg.text), cfg.launch, cfg.sigma, float_mode=False)
+        a, b = _ints(1 << 20, 3), _ints(1 << 20, 4)
+        for _ in range(2):
+            got = ie.run({"xs": np.asarray(a), "ys": np.asarray(b)}, st)
+            assert int(got["out"][0]) == int(np.dot(np.asarray(a, np.int64), np.asarray(b, np.int64)))
+    finally:
+        for b_ in bufs:
+            b_.free()

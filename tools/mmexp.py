@@ -1,0 +1,69 @@
+"""mm strategy/occupancy sweep (GPU box).
+
+    python tools/mmexp.py
+
+For each (T, BK, R) strategy parameterisation of bench_programs.mm_program,
+times the emitted kernel like bench.py (L2 scrubbed, events, mean of 10) at
+its natural occupancy and with the dynamic shared-memory request padded so
+that only one CTA fits per SM (which changes 1024 tiles from 3.46 waves over
+296 resident CTAs to 6.92 waves over 148).  Measurement infrastructure only.
+"""
+import os
+import statistics
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
+from paper_1710_08332_b200 import runtime as RT  # noqa: E402
+from paper_1710_08332_b200.bench_programs import mm_config  # noqa: E402
+
+
+def run(cfg, inputs, st, pad_smem=None, reps=10):
+    exe = executable(compile_program(cfg.text, name=cfg.name), cfg.launch, cfg.sigma, float_mode=True)
+    if pad_smem:
+        for k in exe.sig.kernels:
+            k.smem = max(k.smem, pad_smem)
+            RT.lib().dpia_kernel_set_smem(exe.module.function(k.name), k.smem)
+    for n, v in inputs.items():
+        exe.upload(n, v, st)
+    ts = []
+    for i in range(reps + 3):
+        RT.lib().dpia_l2_flush(0, st.handle)
+        e0, e1 = RT.Event(0), RT.Event(0)
+        e0.record(st)
+        exe.launch(st)
+        e1.record(st)
+        st.sync()
+        if i >= 3:
+            ts.append(e0.elapsed_ms(e1))
+    out = np.zeros((4096, 4096), np.float32)
+    exe.buffers["out"].download(out)
+    return statistics.mean(ts), out
+
+
+def main():
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    ref = (A[:64].astype(np.float64) @ B.astype(np.float64))
+    inputs = {"A": A, "B": B}
+    grid = [(128, 8, 8), (128, 16, 8), (128, 32, 8)]
+    for T, BK, R in grid:
+        cfg = mm_config(T=T, BK=BK, R=R)
+        for pad in (None, 120 * 1024):
+            try:
+                ms, out = run(cfg, inputs, st, pad)
+            except Exception as e:  # noqa: BLE001
+                print(f"T={T} BK={BK} R={R} pad={pad}: {type(e).__name__} {str(e)[:300]}", flush=True)
+                continue
+            err = float(np.max(np.abs(out[:64] - ref)))
+            print(f"T={T} BK={BK} R={R} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
+                  f"max|err| rows 0-63 = {err:.2e}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
