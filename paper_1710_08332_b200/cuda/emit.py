@@ -51,6 +51,9 @@ from .index import Ix, div, ix, mod, render
 
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "dpia_device.cuh")
 UNROLL_LIMIT = 64
+# work-item loops of a pipelined staging may take up to this many iterations
+# per thread (unrolled into guarded copies, one prefetch register set each)
+PF_MAX_COPIES = 4
 
 
 class NeedLanes(Exception):
@@ -924,8 +927,37 @@ class KernelEmitter:
         single = trip is not None and S is not None and trip <= S
         if level == "local" and self.launch and trip is not None and S is not None:
             single = trip <= S
-        lp = Loop(level, dim, v, trip, n, single)
         bound = str(trip) if trip is not None else f"({self.r(self.nat_ix(n))})"
+
+        def enter(is_single):
+            lp = Loop(level, dim, v, trip, n, is_single)
+            self.loops.append(lp)
+            old = {}
+            names = [binder] + ([bind[0]] if bind else [])
+            for nm in names:
+                old[nm] = self.env.get(nm)
+            self.env[binder] = Val(Idx(n), ixv=ix(v))
+            if bind:
+                self.env[bind[0]] = bind[1](ix(v))
+            body()
+            for nm, ov in old.items():
+                if ov is None:
+                    self.env.pop(nm, None)
+                else:
+                    self.env[nm] = ov
+            self.loops.pop()
+            self.close()
+
+        if self.pf is not None and level in ("local", "lin") and not single and trip is not None \
+                and S is not None and trip <= PF_MAX_COPIES * S:
+            # a work-item loop of a software-pipelined staging that takes a
+            # few iterations per thread: unrolled into guarded copies so each
+            # copy's loads get their own prefetch registers
+            for k in range(-(-trip // S)):
+                self.open("" if (k + 1) * S <= trip else f"if ({start} + {k * S} < {trip})")
+                self.line(f"const {ctype} {v} = {start} + {k * S};")
+                enter(True)
+            return
         if single and level != "seq":
             if trip == S:
                 self.open("")
@@ -939,22 +971,7 @@ class KernelEmitter:
             if level == "seq" and trip is not None and trip <= UNROLL_LIMIT:
                 self.line("#pragma unroll")
             self.open(f"for ({ctype} {v} = {start}; {v} < {bound}; {v} += {stride})")
-        self.loops.append(lp)
-        old = {}
-        names = [binder] + ([bind[0]] if bind else [])
-        for nm in names:
-            old[nm] = self.env.get(nm)
-        self.env[binder] = Val(Idx(n), ixv=ix(v))
-        if bind:
-            self.env[bind[0]] = bind[1](ix(v))
-        body()
-        for nm, ov in old.items():
-            if ov is None:
-                self.env.pop(nm, None)
-            else:
-                self.env[nm] = ov
-        self.loops.pop()
-        self.close()
+        enter(single)
 
     def parfor(self, prim: str, targs, args):
         n, d = targs
@@ -1035,7 +1052,7 @@ class KernelEmitter:
                 if u is not None and u[0] in PARFOR_FAMILY and len(u[1]) == 2:
                     lvl, dim = LOOP_LEVEL[u[0]]
                     t = self.nat_int(u[1][0])
-                    if t is None or t > L[1][dim]:
+                    if t is None or t > PF_MAX_COPIES * L[1][dim]:
                         return False
             return True
 

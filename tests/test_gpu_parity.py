@@ -124,7 +124,9 @@ def test_gemv_full_size_fp32():
 
 
 @pytest.mark.parametrize("M,N,K,T,BK,R", [(32, 32, 32, 16, 8, 4), (64, 96, 128, 32, 8, 4),
-                                          (256, 128, 384, 128, 8, 8), (128, 256, 64, 64, 16, 4)])
+                                          (256, 128, 384, 128, 8, 8), (128, 256, 64, 64, 16, 4),
+                                          # pipelined stagings with 2 and 4 loads per work-item
+                                          (256, 256, 128, 128, 16, 8), (128, 128, 128, 128, 32, 8)])
 def test_mm_strategy_int_exact(M, N, K, T, BK, R):
     prog = compile_program(mm_program(M, N, K, T, BK, R))
     A = np.random.default_rng(6).integers(-9, 10, (M, K))

@@ -48,7 +48,31 @@ def summarise(path):
     return res
 
 
+def launch_summary(path):
+    """Mean gpu__time_duration per kernel name from an `ncu --metrics
+    gpu__time_duration.sum --csv` launch list."""
+    import statistics
+    with open(path) as f:
+        lines = f.read().splitlines()
+    start = next(i for i, ln in enumerate(lines) if ln.startswith('"ID"'))
+    rows = list(csv.DictReader(lines[start:]))
+    per = {}
+    for r in rows:
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "")
+        us = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
+        per.setdefault(r["Kernel Name"], []).append(us)
+    return {k: (len(v), statistics.mean(v)) for k, v in per.items()}
+
+
 if __name__ == "__main__":
+    if sys.argv[1] == "--launches":
+        print("ncu --metrics gpu__time_duration.sum --clock-control none (cold cache, serialised)")
+        for k, (n, m) in launch_summary(sys.argv[2]).items():
+            print(f"{k:24s} launches={n:3d} mean={m:10.2f} us")
+        sys.exit(0)
     allres = {p: summarise(p) for p in sys.argv[1:]}
     json.dump(allres, sys.stdout, indent=1)
     print()
