@@ -503,7 +503,7 @@ def _cfg_desc(cfg, world=1):
                          "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x",
                          "scal": "scal N=2^26 fp32 (read + write), grid-stride mapGlobal over vec4",
                          "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
-                               "tiles, toLocal k-tiles of 8"}[cfg.name],
+                               "tiles, toLocal k-tiles of 16, FFMA2"}[cfg.name],
             "sigma": cfg.sigma, "launch": list(cfg.launch),
             "l2": "scrubbed between steps (a read of 2x L2 by dpia_l2_scrub, outside the timed events)"}
 

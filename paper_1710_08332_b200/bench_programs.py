@@ -99,7 +99,8 @@ def gemv_program(M: int, N: int, L: int = 256) -> str:
 """
 
 
-def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) -> str:
+def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
+               a_by_rows: bool = False) -> str:
     """C = A B (row-major), SURVEY.md App. A.4 strategy:
 
     * mapWorkgroup1 / mapWorkgroup over T x T output tiles (blockIdx.y/x);
@@ -113,7 +114,11 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
     * work-item (ty, tx) owns rows ty*R + ii and the *interleaved* columns
       h*T/2 + tx*R/2 + q (jj = h*R/2 + q), so each k-step reads its B values
       with two conflict-free 16-byte shared loads;
-    * per work-item an R x R outer-product reduceSeq over the BK k-steps.
+    * per work-item an R x R outer-product reduceSeq over the BK k-steps;
+    * a_by_rows: the A tile's vec4 loads are distributed over work-items
+      k-quad-major (transpose before split P), so a warp covers 32 distinct
+      rows at one k-quad and its transposed (k-major) shared stores hit 32
+      distinct banks, instead of 4 k-quads of 8 rows (4-way conflicts).
     """
     P = T // R                       # work-items per dimension
     Q = 4 if R % 4 == 0 else R       # contiguous columns per shared load
@@ -121,6 +126,11 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
     zero_t = f"(array {P} (array {P} (array {R} (array {R} num))))"
     a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
                f" (split {P} (asVector4 (join t))))))))) (fst tiles))")
+    if a_by_rows:
+        a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (transpose (split {T} (join"
+                   f" (mapLocal1 (lam r (mapLocal (lam v v) r))"
+                   f" (split {P} (join (transpose (split {BK // 4} (asVector4 (join t)))))))))))))))"
+                   f" (fst tiles))")
     b_stage = (f"(toLocal (lam t (split {T} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
                f" (split {P} (asVector4 (join t)))))))) (snd tiles))")
     micro = f"""
@@ -169,10 +179,10 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8) ->
 """
 
 
-def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 8,
-              R: int = 8) -> Config:
+def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 16,
+              R: int = 8, a_by_rows: bool = False) -> Config:
     P = T // R
-    return Config("mm", mm_program(M, N, K, T, BK, R), {}, ((N // T, M // T), (P, P)),
+    return Config("mm", mm_program(M, N, K, T, BK, R, a_by_rows), {}, ((N // T, M // T), (P, P)),
                   bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
 
 

@@ -8,6 +8,9 @@
 //                          warp-shuffle tree (__shfl_down_sync) + one shared-memory
 //                          hop per warp; absent from the reference, whose single
 //                          kernels stop at partial sums (programs/dotvec.dpia:4-5)
+// * dpia::fma2          -- two independent scalar FMAs issued as one packed
+//                          Blackwell fma.rn.f32x2 (FFMA2); per lane identical
+//                          to the contracted scalar c + a*b
 // * dpia::grid_arrive   -- last-block-done detection used to fuse a single
 //                          work-group tail phase into the preceding grid phase
 //
@@ -147,6 +150,17 @@ __device__ __forceinline__ T block_combine(T v, bool has, Op op, T* scratch, boo
   __syncthreads();
   has_out = scratch_has[32];
   return scratch[32];
+}
+
+// c0 += a0*b0 and c1 += a1*b1 as one FFMA2 (sm_100a).  When b0 and b1 are
+// the same register ptxas uses the broadcast-operand form.
+__device__ __forceinline__ void fma2(float& c0, float& c1, float a0, float b0, float a1, float b1) {
+  unsigned long long c, a, b;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(c) : "f"(c0), "f"(c1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(a) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(b) : "f"(b0), "f"(b1));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(a), "l"(b));
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(c0), "=f"(c1) : "l"(c));
 }
 
 // Last-block-done detection for a fused single-work-group tail phase.

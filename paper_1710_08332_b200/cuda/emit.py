@@ -279,6 +279,44 @@ def contains_prim(p: Phrase, names) -> bool:
 
 # ---------------------------------------------------------------- planner
 
+def _top_split(e: str, op: str):
+    """Split C text `(L op R)` at its top-level operator, else None."""
+    e = e.strip()
+    if not (e.startswith("(") and e.endswith(")")):
+        return None
+    inner, depth = e[1:-1], 0
+    for i, ch in enumerate(inner):
+        if ch in "([{":
+            depth += 1
+        elif ch in ")]}":
+            depth -= 1
+            if depth < 0:
+                return None
+        elif depth == 0 and inner.startswith(f" {op} ", i):
+            return inner[:i], inner[i + len(op) + 2:]
+    return None
+
+
+def _fma_stmt(lines):
+    """(T, X, Y) of one emitted statement `T = (T + (X * Y));` (either
+    operand order of the +), else None."""
+    if len(lines) != 1:
+        return None
+    st = lines[0].strip()
+    if not st.endswith(";") or " = " not in st:
+        return None
+    t, e = st[:-1].split(" = ", 1)
+    add = _top_split(e, "+")
+    if add is None:
+        return None
+    for acc, prod in (add, add[::-1]):
+        if acc.strip() == t:
+            mul = _top_split(prod, "*")
+            if mul is not None:
+                return t, mul[0], mul[1]
+    return None
+
+
 class BarrierPlanner:
     """Work-group barrier placement at uniform program points.
 
@@ -738,6 +776,8 @@ class KernelEmitter:
                 raise CudaError("a sequential loop around a grid-level parallel loop needs a "
                                 "grid-wide barrier per iteration (one kernel per iteration); "
                                 "not supported")
+            if self._fma2_loop(p, targs[0], f):
+                return
             cands, rotate = [], False
             if id(p) in self.for_plans:
                 cands, rotate = self.for_plans[id(p)], True
@@ -754,6 +794,55 @@ class KernelEmitter:
             self.combine(targs, args)
             return
         raise CudaError(f"no command clause for {name!r}")
+
+    # ------------------------------------------------- packed FP32 FMA
+    def _fma2_loop(self, p: Phrase, n: Nat, f: Lam) -> bool:
+        """Instruction selection for a sequential loop whose body is one
+        scalar update T[i] := T[i] + X[i] * Y[i] (the register-tile update of
+        a reduceSeq/mapSeq nest): iterations 2t and 2t+1 are issued as one
+        packed Blackwell fma.rn.f32x2 (FFMA2).  Each lane is the same single-
+        rounding FMA the scalar code contracts to (--fmad=true), so results
+        are bit-identical; the strategy (loop order, storage) is unchanged.
+        Returns False, emitting nothing, when the loop does not qualify."""
+        trip = self.nat_int(n)
+        body = unapply(f.body)
+        if self.scalar != "float" or self.pf is not None or trip is None or trip < 2 \
+                or trip % 2 or trip > UNROLL_LIMIT or body is None or body[0] != ":=" \
+                or not isinstance(body[1][0], Num):
+            return False
+        mark, nlines = len(self.lines), None
+        v = self.fresh(f.binder)
+        self.R[v] = trip
+        self.line("#pragma unroll")
+        self.open(f"for (int {v} = 0; {v} < {trip}; {v} += 2)")
+        self.loops.append(Loop("seq", 0, v, trip, n, False))
+        old = self.env.get(f.binder)
+        stmts = []
+        try:
+            for k in (0, 1):
+                self.env[f.binder] = Val(Idx(n), ixv=ix(v) + k)
+                at = len(self.lines)
+                self.comm(f.body)
+                stmts.append(self.lines[at:])
+                del self.lines[at:]
+        finally:
+            if old is None:
+                self.env.pop(f.binder, None)
+            else:
+                self.env[f.binder] = old
+            self.loops.pop()
+        parsed = [_fma_stmt(b) for b in stmts]
+        ok = all(x is not None for x in parsed)
+        if ok:
+            (t0, a0, b0), (t1, a1, b1) = parsed
+            ok = t0 != t1 and t1 not in a0 + b0 and t0 not in a1 + b1
+        if not ok:
+            del self.lines[mark:]
+            self.ind -= 1
+            return False
+        self.line(f"dpia::fma2({t0}, {t1}, {a0}, {b0}, {a1}, {b1});")
+        self.close()
+        return True
 
     def _declare_local(self, binder: str, d: DataType) -> Buffer:
         lp = [lp for lp in self.loops if lp.level in ("local", "lin")]

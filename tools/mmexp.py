@@ -51,19 +51,52 @@ def main():
     B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
     ref = (A[:64].astype(np.float64) @ B.astype(np.float64))
     inputs = {"A": A, "B": B}
-    grid = [(128, 8, 8), (128, 16, 8), (128, 32, 8), (64, 16, 4), (64, 32, 4)]
-    for T, BK, R in grid:
-        cfg = mm_config(T=T, BK=BK, R=R)
+    grid = [(128, 8, 8, False), (128, 8, 8, True), (128, 16, 8, False), (128, 16, 8, True),
+            (128, 32, 8, True)]
+    for T, BK, R, rows in grid:
+        cfg = mm_config(T=T, BK=BK, R=R, a_by_rows=rows)
         for pad in (None,):
             try:
                 ms, out = run(cfg, inputs, st, pad)
             except Exception as e:  # noqa: BLE001
-                print(f"T={T} BK={BK} R={R} pad={pad}: {type(e).__name__} {str(e)[:300]}", flush=True)
+                print(f"T={T} BK={BK} R={R} a_by_rows={rows} pad={pad}: {type(e).__name__} {str(e)[:300]}", flush=True)
                 continue
             err = float(np.max(np.abs(out[:64] - ref)))
-            print(f"T={T} BK={BK} R={R} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
+            print(f"T={T} BK={BK} R={R} a_by_rows={rows} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
                   f"max|err| rows 0-63 = {err:.2e}", flush=True)
 
 
+def waves():
+    """In-wave efficiency: problems whose tile count fills exactly 1 or 2
+    waves of 296 resident CTAs (2 per SM), next to 4096^2 (3.46 waves)."""
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    for M, N in ((4736, 1024), (4736, 2048), (4096, 4096)):
+        A = rng.uniform(-1, 1, (M, 4096)).astype(np.float32)
+        B = rng.uniform(-1, 1, (4096, N)).astype(np.float32)
+        cfg = mm_config(M=M, N=N)
+        exe = executable(compile_program(cfg.text, name=cfg.name), cfg.launch, cfg.sigma, float_mode=True)
+        exe.upload("A", A, st)
+        exe.upload("B", B, st)
+        ts = []
+        for i in range(13):
+            RT.lib().dpia_l2_flush(0, st.handle)
+            e0, e1 = RT.Event(0), RT.Event(0)
+            e0.record(st)
+            exe.launch(st)
+            e1.record(st)
+            st.sync()
+            if i >= 3:
+                ts.append(e0.elapsed_ms(e1))
+        ms = statistics.mean(ts)
+        tiles = (M // 128) * (N // 128)
+        print(f"M={M} N={N} K=4096 ({tiles} tiles = {tiles / 296:.2f} waves): {ms * 1e3:8.1f} us  "
+              f"{cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "waves":
+        waves()
+        sys.exit(0)
     main()
