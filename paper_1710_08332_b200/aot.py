@@ -31,8 +31,10 @@ def nvcc_check(src: str, tag: str, verbose: bool = False) -> str:
 def build_all(verbose: bool = False):
     from . import bench_programs as BP
     os.makedirs(RT.KCACHE_DIR, exist_ok=True)
+    keep = set()
     for tag, src in BP.aot_sources():
         key = RT.cubin_key(src)
+        keep.add(key + ".cubin")
         path = os.path.join(RT.KCACHE_DIR, key + ".cubin")
         report = nvcc_check(src, tag)
         if verbose:
@@ -42,3 +44,6 @@ def build_all(verbose: bool = False):
             img = RT.nvrtc_compile(src)
             with open(path, "wb") as f:
                 f.write(img)
+    for stale in set(os.listdir(RT.KCACHE_DIR)) - keep:   # sources changed since
+        if stale.endswith(".cubin"):
+            os.remove(os.path.join(RT.KCACHE_DIR, stale))
