@@ -100,7 +100,7 @@ def gemv_program(M: int, N: int, L: int = 256) -> str:
 
 
 def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
-               a_by_rows: bool = False) -> str:
+               a_by_rows: bool = False, a_sectors: bool = False) -> str:
     """C = A B (row-major), SURVEY.md App. A.4 strategy:
 
     * mapWorkgroup1 / mapWorkgroup over T x T output tiles (blockIdx.y/x);
@@ -118,7 +118,12 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
     * a_by_rows: the A tile's vec4 loads are distributed over work-items
       k-quad-major (transpose before split P), so a warp covers 32 distinct
       rows at one k-quad and its transposed (k-major) shared stores hit 32
-      distinct banks, instead of 4 k-quads of 8 rows (4-way conflicts).
+      distinct banks, instead of 4 k-quads of 8 rows (4-way conflicts);
+    * a_sectors: the A tile's vec4 loads are distributed so a warp covers
+      16 rows x 2 k-quads (one full 32-byte sector per row, 2-way store
+      conflicts): the (row, q) order is permuted to (q / 2, row, q % 2)
+      with split/transpose/join views around the copy and permuted back on
+      the acceptor side.
     """
     P = T // R                       # work-items per dimension
     Q = 4 if R % 4 == 0 else R       # contiguous columns per shared load
@@ -126,6 +131,12 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
     zero_t = f"(array {P} (array {P} (array {R} (array {R} num))))"
     a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
                f" (split {P} (asVector4 (join t))))))))) (fst tiles))")
+    if a_sectors and BK // 4 >= 2:
+        qh = BK // 8
+        perm = f"(join (join (transpose (split {qh} (split 2 (asVector4 (join t)))))))"
+        copied = f"(join (mapLocal1 (lam r (mapLocal (lam v v) r)) (split {P} {perm})))"
+        back = f"(join (join (transpose (split {T} (split 2 {copied})))))"
+        a_stage = f"(toLocal (lam t (transpose (split {BK} (asScalar4 {back})))) (fst tiles))"
     if a_by_rows:
         a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (transpose (split {T} (join"
                    f" (mapLocal1 (lam r (mapLocal (lam v v) r))"
@@ -180,9 +191,9 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
 
 
 def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 16,
-              R: int = 8, a_by_rows: bool = False) -> Config:
+              R: int = 8, a_by_rows: bool = False, a_sectors: bool = False) -> Config:
     P = T // R
-    return Config("mm", mm_program(M, N, K, T, BK, R, a_by_rows), {}, ((N // T, M // T), (P, P)),
+    return Config("mm", mm_program(M, N, K, T, BK, R, a_by_rows, a_sectors), {}, ((N // T, M // T), (P, P)),
                   bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
 
 

@@ -137,6 +137,22 @@ def test_mm_strategy_int_exact(M, N, K, T, BK, R):
     assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
 
 
+@pytest.mark.parametrize("layout", ["rows", "sectors"])
+@pytest.mark.parametrize("BK", [16, 32])
+def test_mm_a_staging_layouts_int_exact(layout, BK):
+    """The alternative A-tile distributions (bench_programs.mm_program
+    a_by_rows / a_sectors: permutation views around the staging copy, undone
+    on the acceptor side) compute the same product."""
+    M, N, K, T, R = 256, 128, 128, 128, 8
+    prog = compile_program(mm_program(M, N, K, T, BK, R, a_by_rows=layout == "rows",
+                                      a_sectors=layout == "sectors"))
+    A = np.random.default_rng(16).integers(-9, 10, (M, K))
+    B = np.random.default_rng(17).integers(-9, 10, (K, N))
+    got = run_program_cuda(prog, {"A": A, "B": B}, launch=((N // T, M // T), (T // R, T // R)),
+                           float_mode=False, flat=True)
+    assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
+
+
 def test_mm_full_size_fp32():
     cfg = mm_config()
     A = blas_np.seeded((4096, 4096), 5, -1.0, 1.0)

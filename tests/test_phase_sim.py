@@ -48,6 +48,11 @@ STRATS = [
     # and its shared tiles rotate between two slices (one barrier per k-step)
     ("mm_pipelined", mm_program(16, 16, 16, 8, 2, 4), {}, ((2, 2), (2, 2)),
      lambda: {"A": [_ints(16, 3 + r) for r in range(16)], "B": [_ints(16, 5 + r) for r in range(16)]}),
+    # alternative A-tile distributions (permutation views around the copy)
+    ("mm_a_rows", mm_program(32, 32, 32, 16, 16, 4, a_by_rows=True), {}, ((2, 2), (4, 4)),
+     lambda: {"A": [_ints(32, 3 + r) for r in range(32)], "B": [_ints(32, 5 + r) for r in range(32)]}),
+    ("mm_a_sectors", mm_program(32, 32, 32, 16, 16, 4, a_sectors=True), {}, ((2, 2), (4, 4)),
+     lambda: {"A": [_ints(32, 3 + r) for r in range(32)], "B": [_ints(32, 5 + r) for r in range(32)]}),
 ]
 
 

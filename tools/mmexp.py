@@ -51,18 +51,18 @@ def main():
     B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
     ref = (A[:64].astype(np.float64) @ B.astype(np.float64))
     inputs = {"A": A, "B": B}
-    grid = [(128, 8, 8, False), (128, 8, 8, True), (128, 16, 8, False), (128, 16, 8, True),
-            (128, 32, 8, True)]
+    grid = [(128, 16, 8, "quads"), (128, 16, 8, "sectors"), (128, 32, 8, "sectors"),
+            (128, 8, 8, "quads")]
     for T, BK, R, rows in grid:
-        cfg = mm_config(T=T, BK=BK, R=R, a_by_rows=rows)
+        cfg = mm_config(T=T, BK=BK, R=R, a_by_rows=rows == "rows", a_sectors=rows == "sectors")
         for pad in (None,):
             try:
                 ms, out = run(cfg, inputs, st, pad)
             except Exception as e:  # noqa: BLE001
-                print(f"T={T} BK={BK} R={R} a_by_rows={rows} pad={pad}: {type(e).__name__} {str(e)[:300]}", flush=True)
+                print(f"T={T} BK={BK} R={R} a_layout={rows} pad={pad}: {type(e).__name__} {str(e)[:300]}", flush=True)
                 continue
             err = float(np.max(np.abs(out[:64] - ref)))
-            print(f"T={T} BK={BK} R={R} a_by_rows={rows} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
+            print(f"T={T} BK={BK} R={R} a_layout={rows} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
                   f"max|err| rows 0-63 = {err:.2e}", flush=True)
 
 
@@ -95,7 +95,53 @@ def waves():
               f"{cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
 
 
+def sts_bound():
+    """Upper bound of what conflict-free transposed A stores would gain: the
+    emitted BK=16 kernel with its A-tile store index replaced by a
+    conflict-free (WRONG-result) one; timing only."""
+    import re
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.launcher import Executable
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    cfg = mm_config()
+    prog = compile_program(cfg.text, name="mm")
+    outs = [(n, t) for n, t, k in prog.params if k == "out"]
+    ins = [(n, t) for n, t, k in prog.params if k == "in"]
+    src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
+    cnt = [0]
+
+    def rep(m):
+        j = cnt[0]
+        cnt[0] += 1
+        return f"{m.group(1)}[2048 * (({m.group(2)}) % 2) + dpia_tid + {256 * j}] = pf"
+    hacked = re.sub(r"(tmp\d+_\d+)\[2048 \* \(\((i_\d+_\d+)\) % 2\) \+ 512 \* [^\]]*\] = pf", rep, src)
+    print("replaced", cnt[0], flush=True)
+    for label, s in (("emitted", src), ("conflict-free A stores (wrong result)", hacked)):
+        exe = Executable(s, sig, 0, True, {}, geometry=cfg.launch).compile().allocate()
+        exe.upload("A", A, st)
+        exe.upload("B", B, st)
+        ts = []
+        for i in range(13):
+            RT.lib().dpia_l2_flush(0, st.handle)
+            e0, e1 = RT.Event(0), RT.Event(0)
+            e0.record(st)
+            exe.launch(st)
+            e1.record(st)
+            st.sync()
+            if i >= 3:
+                ts.append(e0.elapsed_ms(e1))
+        ms = statistics.mean(ts)
+        print(f"{label}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "sts":
+        sts_bound()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "waves":
         waves()
         sys.exit(0)
