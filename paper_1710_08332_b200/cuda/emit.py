@@ -54,6 +54,9 @@ UNROLL_LIMIT = 64
 # work-item loops of a pipelined staging may take up to this many iterations
 # per thread (unrolled into guarded copies, one prefetch register set each)
 PF_MAX_COPIES = 4
+# bank-conflict layout of local buffers whose rows are a multiple of 32
+# scalars (see KernelEmitter._declare_local): swizzle | pad | none
+SMEM_LAYOUT = os.environ.get("DPIA_SMEM_LAYOUT", "swizzle")
 
 
 class NeedLanes(Exception):
@@ -70,6 +73,8 @@ class Buffer:
     dtype: DataType          # full type, hoisting dims included
     prefix: List[Ix] = field(default_factory=list)
     sliced: int = 0
+    pad: int = 0             # scalars added to the innermost row stride (shared-memory banks)
+    swz: Optional[Tuple[int, int, int]] = None   # (unit, div, period): inner ^= unit*((outer/div)%period)
 
     @property
     def dims(self):
@@ -97,9 +102,14 @@ class Alias:
 @dataclass
 class Ref:
     buf: Buffer
-    flat: Optional[Ix]
+    flat: Optional[Ix]       # logical flat index (alignment reasoning)
     suffix: str
     text: str
+    addr: Optional[Ix] = None    # physical flat index when the buffer is swizzled
+
+    @property
+    def at(self) -> Optional[Ix]:
+        return self.addr if self.addr is not None else self.flat
 
 
 @dataclass
@@ -511,12 +521,18 @@ class KernelEmitter:
             self.records.setdefault(buf.key, []).append(
                 (idxs, list(self.loops), self.single_thread, self.decl_depth.get(buf.key, 0)))
         idxs, dims = idxs[buf.sliced:], dims[buf.sliced:]
-        flat = None
+        flat = addr = None
         if dims:
             flat = Ix()
-            for d, i in zip(dims, idxs):
-                flat = flat * self.nat_ix(d) + i
-            base = f"{buf.cname}[{self.r(flat)}]"
+            last = len(dims) - 1
+            for q, (d, i) in enumerate(zip(dims, idxs)):
+                ext = self.nat_ix(d) + buf.pad if q == last and buf.pad else self.nat_ix(d)
+                if q == last and buf.swz and last >= 1:
+                    unit, dv, per = buf.swz
+                    mask = mod(div(idxs[last - 1], dv, self.R), per, self.R) * unit
+                    addr = flat * ext + self._swizzled(i, mask, unit, per)
+                flat = flat * ext + i
+            base = f"{buf.cname}[{self.r(addr if addr is not None else flat)}]"
         else:
             base = buf.cname if buf.space == "private" else f"{buf.cname}[0]"
         suffix = ""
@@ -535,7 +551,38 @@ class KernelEmitter:
                 t = t.elem
             else:
                 raise CudaError(f"index step into scalar of {buf.key}")
-        return Ref(buf, flat, suffix, base + suffix)
+        return Ref(buf, flat, suffix, base + suffix, addr)
+
+    def _swizzled(self, i: Ix, mask: Ix, unit: int, per: int) -> Ix:
+        """i ^ mask (mask a multiple of unit below unit*per), written as
+        Hi + ((Mid) ^ mask) + Lo so that only the bits the mask can touch
+        are inside the XOR: Lo < B with every other term a multiple of B (B
+        the largest such power of two <= unit), Hi a multiple of a power of
+        two P above Mid and the mask.  This keeps unrolled constants and
+        per-thread bases out of the XOR so the C compiler still folds them
+        into immediate offsets and 16-byte accesses."""
+        R = self.R
+        lo, rest = [], list(i.terms)
+        B = unit
+        while B > 1:
+            cand = [t for t in i.terms if t[1] % B]
+            m = IX.max_value(Ix(cand), R)
+            if m is not None and m < B:
+                lo, rest = cand, [t for t in i.terms if t[1] % B == 0]
+                break
+            B //= 2
+        P = unit * per
+        while True:
+            hi = [t for t in rest if t[1] % P == 0]
+            mid = [t for t in rest if t[1] % P]
+            mm = IX.max_value(Ix(mid), R)
+            if mm is None:
+                hi, mid = [], rest
+                break
+            if mm < P:
+                break
+            P *= 2
+        return Ix(hi) + IX.xor(Ix(mid), mask) + Ix(lo)
 
     def binding(self, name: str):
         if name not in self.env:
@@ -622,17 +669,18 @@ class KernelEmitter:
             (_, i) = steps[0]
             ref = self.resolve(args[0], [("i", i * w)])
             aligned = isinstance(ref, Ref) and ref.flat is not None and not ref.suffix \
-                and all(c % w == 0 for _, c in ref.flat.terms)
+                and all(c % w == 0 for _, c in ref.flat.terms) \
+                and not (ref.buf.swz and w > ref.buf.swz[0])
             if len(steps) >= 2:
                 (_, lane), rest = steps[1], steps[2:]
                 if aligned and not rest:
                     # whole-vector load + lane select: redundant loads of the
                     # same vector CSE into one LDG.128/LDS.128
                     return (f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, "
-                            f"{self.r(ref.flat)}).v[{self.r(lane)}]")
+                            f"{self.r(ref.at)}).v[{self.r(lane)}]")
                 return self.resolve(args[0], [("i", i * w + lane)] + rest)
             if aligned:
-                return f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, {self.r(ref.flat)})"
+                return f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, {self.r(ref.at)})"
             lanes = ", ".join(self.exp(args[0], [("i", i * w + k)]) for k in range(w))
             return f"dpia::vec<{self.scalar}, {w}>{{{{{lanes}}}}}"
         if name.startswith("asScalar") and "Acc" not in name:
@@ -694,7 +742,8 @@ class KernelEmitter:
                 return self.acc(args[0], [("i", i * w + lane)] + rest)
             ref = self.acc(args[0], [("i", i * w)])
             if isinstance(ref, Ref) and ref.flat is not None and not ref.suffix \
-                    and all(c % w == 0 for _, c in ref.flat.terms):
+                    and all(c % w == 0 for _, c in ref.flat.terms) \
+                    and not (ref.buf.swz and w > ref.buf.swz[0]):
                 return VStore(ref, w)
             raise NeedLanes()
         raise CudaError(f"no acceptor clause for {name!r}")
@@ -736,7 +785,7 @@ class KernelEmitter:
         buf = target.ref.buf if isinstance(target, VStore) else target.buf
         if isinstance(target, VStore):
             stmt = (f"dpia::vstore<{self.scalar}, {target.width}>({buf.cname}, "
-                    f"{self.r(target.ref.flat)}, {rhs});")
+                    f"{self.r(target.ref.at)}, {rhs});")
         else:
             stmt = f"{target.text} = {rhs};"
         if buf.space != "private" and not self.per_thread:
@@ -812,15 +861,15 @@ class KernelEmitter:
             return False
         mark, nlines = len(self.lines), None
         v = self.fresh(f.binder)
-        self.R[v] = trip
+        self.R[v] = trip // 2
         self.line("#pragma unroll")
-        self.open(f"for (int {v} = 0; {v} < {trip}; {v} += 2)")
-        self.loops.append(Loop("seq", 0, v, trip, n, False))
+        self.open(f"for (int {v} = 0; {v} < {trip // 2}; {v} += 1)")
+        self.loops.append(Loop("seq", 0, v, trip // 2, nat(trip // 2), False))
         old = self.env.get(f.binder)
         stmts = []
         try:
             for k in (0, 1):
-                self.env[f.binder] = Val(Idx(n), ixv=ix(v) + k)
+                self.env[f.binder] = Val(Idx(n), ixv=ix(v) * 2 + k)
                 at = len(self.lines)
                 self.comm(f.body)
                 stmts.append(self.lines[at:])
@@ -854,6 +903,21 @@ class KernelEmitter:
         n = self._elements(full)
         if n is None:
             raise CudaError(f"local buffer {binder} needs a constant size (specialise sizes)")
+        dims, elem = split_array(full)
+        inner = self.nat_int(dims[-1]) if dims else None
+        if isinstance(elem, Num) and len(dims) >= 2 and inner and inner % 32 == 0:
+            # rows of a multiple of 32 scalars all start in bank 0, so a
+            # column-wise access (e.g. the transposed store of a vec4-loaded
+            # tile) hits one bank.  "swizzle": XOR the column with
+            # 8*((row/4)%4) -- a bijection inside each row that keeps 8-aligned
+            # groups (16/32-byte vectors) contiguous and sends the 4 rows of
+            # a vec4's lanes x 8 columns to 32 distinct banks; "pad": 16 bytes
+            # of padding per row (2-way at worst for that pattern)
+            if SMEM_LAYOUT == "swizzle":
+                buf.swz = (8, 4, 4)
+            elif SMEM_LAYOUT == "pad":
+                buf.pad = 4
+                n = n // inner * (inner + 4)
         off = self.alloc_smem(n * self._elem_bytes(split_array(full)[1]))
         ct = self.types.c_elem(split_array(full)[1])
         self.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")

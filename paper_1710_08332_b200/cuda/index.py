@@ -18,7 +18,7 @@ from typing import Dict, Mapping, Optional, Tuple
 
 INT32_MAX = 2 ** 31 - 1
 
-# atom key -> ("v", name) | ("d", Ix, n) | ("m", Ix, n)
+# atom key -> ("v", name) | ("d", Ix, n) | ("m", Ix, n) | ("x", Ix, Ix)  (xor)
 _ATOMS: Dict[str, tuple] = {}
 
 
@@ -122,6 +122,11 @@ def _atom_max(key: str, R) -> Optional[int]:
     if node[0] == "v":
         b = R.get(node[1])
         return None if b is None else b - 1
+    if node[0] == "x":
+        ma, mb = max_value(node[1], R), max_value(node[2], R)
+        if ma is None or mb is None:
+            return None
+        return (1 << max(ma, mb).bit_length()) - 1
     inner = max_value(node[1], R)
     if node[0] == "d":
         return None if inner is None else inner // node[2]
@@ -198,6 +203,15 @@ def mod(e, n: int, R) -> Ix:
     return Ix([((_atom(key, ("m", r, n)),), 1)])
 
 
+def xor(a, b) -> Ix:
+    """a ^ b as an opaque atom (shared-memory swizzles); both non-negative."""
+    a, b = ix(a), ix(b)
+    if not b.terms:
+        return a
+    key = f"({render(a)})^({render(b)})"
+    return Ix([((_atom(key, ("x", a, b)),), 1)])
+
+
 # ---------------------------------------------------------- rendering
 
 def render(e: Ix, R: Optional[Mapping[str, Optional[int]]] = None, wide: Optional[bool] = None) -> str:
@@ -222,6 +236,8 @@ def _render_atom(key: str, R, wide: bool) -> str:
     node = _ATOMS[key]
     if node[0] == "v":
         return node[1]
+    if node[0] == "x":
+        return f"(({render(node[1], R, wide)}) ^ ({render(node[2], R, wide)}))"
     inner_wide = wide or (R is not None and (max_value(node[1], R) is None
                                              or max_value(node[1], R) > INT32_MAX))
     op = "/" if node[0] == "d" else "%"
@@ -238,6 +254,8 @@ def evaluate(e: Ix, env: Mapping[str, int]) -> int:
                 t *= env[node[1]]
             elif node[0] == "d":
                 t *= evaluate(node[1], env) // node[2]
+            elif node[0] == "x":
+                t *= evaluate(node[1], env) ^ evaluate(node[2], env)
             else:
                 t *= evaluate(node[1], env) % node[2]
         total += t
@@ -250,6 +268,8 @@ def free_names(e: Ix) -> set:
         node = _ATOMS[a]
         if node[0] == "v":
             out.add(node[1])
+        elif node[0] == "x":
+            out |= free_names(node[1]) | free_names(node[2])
         else:
             out |= free_names(node[1])
     return out

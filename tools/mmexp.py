@@ -95,6 +95,34 @@ def waves():
               f"{cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
 
 
+def one(variant):
+    """Launch one variant once (for ncu): quads | sectors | rows | hack."""
+    import re
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.launcher import Executable
+    RT.init(0)
+    st = RT.Stream(0)
+    cfg = mm_config(a_by_rows=variant == "rows", a_sectors=variant == "sectors")
+    prog = compile_program(cfg.text, name="mm")
+    outs = [(n, t) for n, t, k in prog.params if k == "out"]
+    ins = [(n, t) for n, t, k in prog.params if k == "in"]
+    src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
+    if variant == "hack":
+        cnt = [0]
+
+        def rep(m):
+            cnt[0] += 1
+            return f"{m.group(1)}[2048 * (({m.group(2)}) % 2) + dpia_tid + {256 * (cnt[0] - 1)}] = pf"
+        src = re.sub(r"(tmp\d+_\d+)\[2048 \* \(\((i_\d+_\d+)\) % 2\) \+ 512 \* [^\]]*\] = pf", rep, src)
+    exe = Executable(src, sig, 0, True, {}, geometry=cfg.launch).compile().allocate()
+    rng = np.random.default_rng(0)
+    exe.upload("A", rng.uniform(-1, 1, (4096, 4096)).astype(np.float32), st)
+    exe.upload("B", rng.uniform(-1, 1, (4096, 4096)).astype(np.float32), st)
+    for _ in range(2):
+        exe.launch(st)
+    st.sync()
+
+
 def sts_bound():
     """Upper bound of what conflict-free transposed A stores would gain: the
     emitted BK=16 kernel with its A-tile store index replaced by a
@@ -139,6 +167,9 @@ def sts_bound():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "one":
+        one(sys.argv[2])
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "sts":
         sts_bound()
         sys.exit(0)
