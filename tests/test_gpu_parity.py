@@ -285,3 +285,18 @@ def test_executable_run_pinned_repeated():
     finally:
         for b_ in bufs:
             b_.free()
+
+
+@pytest.mark.parametrize("launch", [(1, 32), (3, 64)])
+def test_empty_inputs(launch):
+    """n = 0: a map yields the empty array and every reduction its initial
+    value, as the reference's interpreter does (eval_fn over empty lists)."""
+    sq = ("(nat n)\n(param xs (exp (array (* n 4) num)))\n"
+          "(join (mapGlobal (lam (c (exp (array 4 num))) (mapSeq (lam (x (exp num)) (* x x)) c)) (split 4 xs)))")
+    cases = [(sq, {"xs": []}), (dot_program(32, 2), {"xs": [], "ys": []}), (asum_program(32, 2), {"xs": []})]
+    for text, inputs in cases:
+        prog = compile_program(text)
+        want = flatten_value(eval_phrase(prog.source.body, inputs, {"n": 0}))
+        for fm in (False, True):
+            got = run_program_cuda(prog, inputs, sigma={"n": 0}, launch=launch, float_mode=fm, flat=True)
+            assert [float(v) for v in np.atleast_1d(got)] == [float(v) for v in want], (text, fm)
