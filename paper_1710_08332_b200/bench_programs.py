@@ -190,6 +190,78 @@ def mm_program(M: int, N: int, K: int, T: int = 128, BK: int = 8, R: int = 8,
 """
 
 
+def mm_rect_program(M: int, N: int, K: int, TM: int = 128, TN: int = 128, BK: int = 16,
+                    RM: int = 8, RN: int = 16) -> str:
+    """mm_program's strategy with rectangular tiles: a TM x TN output tile
+    per work-group and an RM x RN register tile per work-item, so a
+    work-group has (TN/RN) x (TM/RM) work-items (threadIdx.x / y).  With
+    RN = 16 each k-step does RM*RN/2 = 64 packed FMAs per 6 shared 16-byte
+    loads (8 A values, 16 B values), against 32 per 4 for the square 8 x 8
+    tile.  Work-item (ty, tx) owns rows ty*RM + i and the interleaved
+    columns h*(TN/H) + tx*Q + q (H = RN/Q groups of Q = 4 contiguous
+    columns, one conflict-free LDS.128 each)."""
+    PM, PN = TM // RM, TN // RN
+    Q = 4 if RN % 4 == 0 else RN
+    H = RN // Q
+    assert TM % RM == 0 and TN % RN == 0 and TN == H * PN * Q
+    zero_t = f"(array {PM} (array {PN} (array {RN} (array {RM} num))))"
+    a_stage = (f"(toLocal (lam t (transpose (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {PN} (asVector4 (join t))))))))) (fst tiles))")
+    b_stage = (f"(toLocal (lam t (split {TN} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {PN} (asVector4 (join t)))))))) (snd tiles))")
+    micro = f"""
+          (reduceSeq
+           (lam (ab (exp (pair (array {RM} num) (array {RN} num))))
+            (lam (t (exp (array {RN} (array {RM} num))))
+             (mapSeq (lam (q (exp (pair num (array {RM} num))))
+                      (mapSeq (lam (w (exp (pair num num))) (+ (snd w) (* (fst w) (fst q))))
+                              (zip (fst ab) (snd q))))
+                     (zip (snd ab) t))))
+           (snd pb)
+           (zip (transpose (fst pa)) (transpose (join (fst pb)))))"""
+    return f"""
+(param A (exp (array {M} (array {K} num))))
+(param B (exp (array {K} (array {N} num))))
+(join
+ (mapWorkgroup1
+  (lam (aRows (exp (array {TM} (array {K} num))))
+   (transpose
+    (mapWorkgroup
+     (lam (bCols (exp (array {TN} (array {K} num))))
+      (join
+       (mapLocal1
+        (lam (accRow (exp (array {PN} (array {RN} (array {RM} num)))))
+         (transpose (join (join (transpose
+          (mapLocal (lam (blk (exp (array {RN} (array {RM} num))))
+                     (split {Q} (mapSeq (mapSeq (lam (z (exp num)) z)) blk)))
+                    accRow))))))
+        (reduceSeq
+         (lam (tiles (exp (pair (array {TM} (array {BK} num)) (array {BK} (array {TN} num)))))
+          (lam (acc (exp {zero_t}))
+           (let {b_stage}
+            (lam (bl (exp (array {BK} (array {TN} num))))
+             (mapLocal1
+              (lam (pa (exp (pair (array {RM} (array {BK} num)) (array {PN} (array {RN} (array {RM} num))))))
+               (mapLocal
+                (lam (pb (exp (pair (array {H} (array {Q} (array {BK} num))) (array {RN} (array {RM} num)))))
+                 {micro})
+                (zip (transpose (split {PN} (split {Q} (transpose bl)))) (snd pa))))
+              (zip (split {RM} (transpose {a_stage})) acc))))))
+         (mapLocal1 (lam r (mapLocal (lam b (mapSeq (mapSeq (lam z z)) b)) r)) (as {zero_t} 0))
+         (zip (transpose (split {K // BK} (split {BK} (join aRows))))
+              (split {BK} (transpose bCols)))))))
+     (split {TN} (transpose B)))))
+  (split {TM} A)))
+"""
+
+
+def mm_rect_config(M: int = 4096, N: int = 4096, K: int = 4096, TM: int = 128, TN: int = 128,
+                   BK: int = 16, RM: int = 8, RN: int = 16) -> Config:
+    return Config("mm", mm_rect_program(M, N, K, TM, TN, BK, RM, RN), {},
+                  ((N // TN, M // TM), (TN // RN, TM // RM)),
+                  bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
+
+
 def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 16,
               R: int = 8, a_by_rows: bool = False, a_sectors: bool = False) -> Config:
     P = T // R

@@ -153,6 +153,19 @@ def test_mm_a_staging_layouts_int_exact(layout, BK):
     assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
 
 
+@pytest.mark.parametrize("M,N,K,TM,TN,BK,RM,RN", [(256, 256, 128, 128, 128, 16, 8, 16),
+                                                  (256, 256, 64, 128, 128, 8, 16, 8),
+                                                  (64, 128, 32, 32, 64, 8, 4, 8)])
+def test_mm_rect_strategy_int_exact(M, N, K, TM, TN, BK, RM, RN):
+    from paper_1710_08332_b200.bench_programs import mm_rect_program
+    prog = compile_program(mm_rect_program(M, N, K, TM, TN, BK, RM, RN))
+    A = np.random.default_rng(26).integers(-9, 10, (M, K))
+    B = np.random.default_rng(27).integers(-9, 10, (K, N))
+    got = run_program_cuda(prog, {"A": A, "B": B}, launch=((N // TN, M // TM), (TN // RN, TM // RM)),
+                           float_mode=False, flat=True)
+    assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
+
+
 def test_mm_full_size_fp32():
     cfg = mm_config()
     A = blas_np.seeded((4096, 4096), 5, -1.0, 1.0)

@@ -17,7 +17,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
-from paper_1710_08332_b200.bench_programs import mm_config  # noqa: E402
+from paper_1710_08332_b200.bench_programs import mm_config, mm_rect_config  # noqa: E402
 
 
 def run(cfg, inputs, st, pad_smem=None, reps=10):
@@ -64,6 +64,27 @@ def main():
             err = float(np.max(np.abs(out[:64] - ref)))
             print(f"T={T} BK={BK} R={R} a_layout={rows} pad={pad}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
                   f"max|err| rows 0-63 = {err:.2e}", flush=True)
+
+
+def rect():
+    """Rectangular register tiles (bench_programs.mm_rect_program)."""
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    ref = (A[:64].astype(np.float64) @ B.astype(np.float64))
+    for TM, TN, BK, RM, RN in ((128, 128, 16, 8, 16), (128, 128, 8, 8, 16), (128, 128, 16, 16, 8),
+                               (128, 128, 8, 16, 8), (128, 64, 16, 8, 8), (256, 128, 8, 16, 16)):
+        cfg = mm_rect_config(TM=TM, TN=TN, BK=BK, RM=RM, RN=RN)
+        try:
+            ms, out = run(cfg, {"A": A, "B": B}, st)
+        except Exception as e:  # noqa: BLE001
+            print(f"rect {TM}x{TN} BK={BK} R={RM}x{RN}: {type(e).__name__} {str(e)[:300]}", flush=True)
+            continue
+        err = float(np.max(np.abs(out[:64] - ref)))
+        print(f"rect {TM}x{TN} BK={BK} R={RM}x{RN}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s"
+              f"  max|err| rows 0-63 = {err:.2e}", flush=True)
 
 
 def waves():
@@ -167,6 +188,9 @@ def sts_bound():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "rect":
+        rect()
+        sys.exit(0)
     if len(sys.argv) > 2 and sys.argv[1] == "one":
         one(sys.argv[2])
         sys.exit(0)
