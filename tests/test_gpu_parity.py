@@ -166,6 +166,28 @@ def test_mm_rect_strategy_int_exact(M, N, K, TM, TN, BK, RM, RN):
     assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
 
 
+@pytest.mark.parametrize("variant", ["square", "rows", "sectors", "rect8x16", "rect16x8", "bk8"])
+def test_mm_variants_fp32(variant):
+    """fp32 (the FFMA2 register-tile update, swizzled shared tiles) for every
+    mm strategy variant, against a float64 product; bound 1e-4 * sum|terms|."""
+    from paper_1710_08332_b200.bench_programs import mm_rect_program
+    M, N, K = 256, 256, 512
+    if variant.startswith("rect"):
+        RM, RN = (8, 16) if variant == "rect8x16" else (16, 8)
+        text, launch = mm_rect_program(M, N, K, 128, 128, 16, RM, RN), ((2, 2), (128 // RN, 128 // RM))
+    else:
+        text = mm_program(M, N, K, 128, 8 if variant == "bk8" else 16, 8, a_by_rows=variant == "rows",
+                          a_sectors=variant == "sectors")
+        launch = ((2, 2), (16, 16))
+    A = blas_np.seeded((M, K), 31, -1.0, 1.0)
+    B = blas_np.seeded((K, N), 32, -1.0, 1.0)
+    got = np.asarray(run_program_cuda(compile_program(text), {"A": A, "B": B}, launch=launch,
+                                      flat=True)).reshape(M, N)
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    terms = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
+    assert np.all(np.abs(got - want) <= 1e-4 * terms)
+
+
 def test_mm_full_size_fp32():
     cfg = mm_config()
     A = blas_np.seeded((4096, 4096), 5, -1.0, 1.0)
