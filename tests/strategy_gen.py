@@ -49,7 +49,9 @@ def generate(seed: int):
         x_expr = lambda v: v  # noqa: E731
     params = f"(param xs (exp (array {N} num)))\n" + (f"(param ys (exp (array {N} num)))\n" if two else "")
     acc_t = "(vec 4)" if vec else "num"
-    shape = rng.choice(["reduce", "reduce", "map", "stage", "let", "rows"])
+    shape = rng.choice(["reduce", "reduce", "map", "stage", "let", "rows", "tile", "axpy"])
+    if shape in ("tile", "axpy") and vec:
+        shape = "map"
     top_combine = shape == "reduce" and rng.random() < 0.6
     e = _expr(rng, "v")
     if shape == "reduce":
@@ -75,6 +77,29 @@ def generate(seed: int):
                 f" (join (mapLocal (lam (r (exp (array {K} {acc_t})))"
                 f" (mapSeq (lam (u (exp {acc_t})) {e2}) r)) (transpose (split {L} s))))))")
         out_t = f"(array {C} {acc_t})"
+    elif shape == "tile":
+        # 2-D shared tile [C/32][32] written by rows, read by columns (rows of
+        # 32 scalars: the backend's XOR-swizzled layout once there are >= 4 rows)
+        rows = C // 32
+        body = (f"(let (toLocal (mapLocal (lam (row (exp (array 32 {elem_t})))"
+                f" (mapSeq (lam (q (exp {elem_t})) (let {x_expr('q')} (lam (v (exp {acc_t})) {e}))) row)))"
+                f" (split 32 chunk))"
+                f" (lam (s (exp (array {rows} (array 32 {acc_t}))))"
+                f" (mapLocal (lam (col (exp (array {rows} {acc_t})))"
+                f" (reduceSeq (lam (x (exp {acc_t})) (lam (a (exp {acc_t})) (+ a x))) 0 col))"
+                f" (transpose s))))")
+        out_t = f"(array 32 {acc_t})"
+    elif shape == "axpy":
+        # per work-item array accumulator updated by T[i] := T[i] + X[i] * Y[i]
+        # (the backend's packed FFMA2 pattern in float mode)
+        body = (f"(join (mapLocal (lam (blk (exp (array {K} {elem_t})))"
+                f" (reduceSeq (lam (p (exp {elem_t})) (lam (a (exp (array 4 {acc_t})))"
+                f" (mapSeq (lam (w (exp (pair {acc_t} {acc_t}))) (+ (snd w) (* (fst w) (fst w))))"
+                f" (zip (let {x_expr('p')} (lam (v (exp {acc_t})) (mapSeq (lam (z (exp {acc_t})) (+ v z))"
+                f" (as (array 4 {acc_t}) 1)))) a))))"
+                f" (as (array 4 {acc_t}) 0) blk))"
+                f" (split {K} chunk)))")
+        out_t = f"(array {4 * L} {acc_t})"
     else:  # rows: per work-item sequential reduce over a contiguous row, staged partials
         body = (f"(reduceLocal (+) 0 (toPrivate (mapLocal (lam (row (exp (array {K} {elem_t})))"
                 f" (reduceSeq (lam (p (exp {elem_t})) (lam (a (exp {acc_t})) (+ a {x_expr('p')}))) 0 row)))"
@@ -82,7 +107,7 @@ def generate(seed: int):
         out_t = acc_t
     prog = (f"(mapWorkgroup (lam (chunk (exp (array {C} {elem_t}))) {body})"
             f" (split {C} {src}))")
-    if shape in ("map", "stage", "let"):
+    if shape in ("map", "stage", "let", "tile", "axpy"):
         prog = f"(join {prog})"
         if vec:
             prog = f"(asScalar4 {prog})"

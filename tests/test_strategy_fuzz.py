@@ -31,3 +31,16 @@ def test_strategy_fuzz_gpu(seed):
     prog, inputs, sigma, launch, want = _case(seed)
     got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=False, flat=True)
     assert [int(v) for v in got] == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", range(400))
+def test_strategy_fuzz_gpu_fp32(seed):
+    """The same programs in float mode: the values are small integers, so
+    every fp32 sum and product is exact and the oracle's integer result must
+    come back bit-exact -- this covers the float-only code paths (packed
+    FFMA2 register updates, swizzled shared tiles) on every generated shape."""
+    from paper_1710_08332_b200 import run_program_cuda
+    prog, inputs, sigma, launch, want = _case(seed)
+    got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=True, flat=True)
+    assert [float(v) for v in got] == [float(v) for v in want]
