@@ -2,8 +2,9 @@
 
     python -m paper_1710_08332_b200.cli compile P.dpia --target cuda [-o P.cu]
                                         [--launch G,L] [--int|--float] [--dump-stages]
+                                        [--check-only] [--init-new] [--simplify-indices on|off]
     python -m paper_1710_08332_b200.cli run P.dpia --inputs P.inputs --device cuda
-                                        [--launch G,L] [--int|--float]
+                                        [--launch G,L] [--int|--float] [--reverse]
 
 Flags, input files (`key=value` lines, arrays in brackets) and exit codes (2
 parse error, 3 type error, 70 internal error) follow the reference CLI
@@ -83,6 +84,12 @@ def _parse_inputs(path: str) -> Dict[str, object]:
 
 def _compile(args) -> int:
     prog = _load(args.file)
+    if args.check_only:                       # SRC/cli.py:93-96
+        print(f"{args.file}: OK ({prog.source.body_type})")
+        return 0
+    from .cuda.hierarchy import lint_hierarchy
+    for w in lint_hierarchy(prog.imperative):  # SRC/cli.py:127-128
+        print(f"warning: {w}", file=sys.stderr)
     base = Path(args.file).with_suffix("")
     if args.dump_stages:
         from .pretty import show
@@ -94,8 +101,8 @@ def _compile(args) -> int:
         sigma = {n: int(sigma[n]) for n in prog.source.nat_params}
     src, _sig = emit_cuda(prog.imperative, [("out", prog.out_type)],
                           [(n, t.data) for n, t in prog.source.params],
-                          float_mode=not args.int_mode, name=prog.name, sigma=sigma,
-                          launch=args.launch)
+                          float_mode=not args.int_mode, name=prog.name, init_new=args.init_new,
+                          simplify=args.simplify_indices != "off", sigma=sigma, launch=args.launch)
     out = args.output or f"{base}.cu"
     Path(out).write_text(src)
     print(f"wrote {out}")
@@ -116,6 +123,12 @@ def _run(args) -> int:
         if n not in data:
             raise CliError(f"missing input {n}=...", EXIT_PARSE)
         inputs[n] = data[n]
+    if args.reverse:
+        # the reference's witness that parfor iterations are order-independent
+        # (SRC/cli.py:253-254, eval_imp reverse_parfor); on the GPU the
+        # iterations of every parallel loop already run in no fixed order
+        print("note: --reverse has no effect on the GPU (parallel iterations are unordered)",
+              file=sys.stderr)
     outs = run_kernel(prog.imperative, prog.params, inputs, args.launch or (148, 256), sigma,
                       float_mode=not args.int_mode, device=args.gpu, name=prog.name)
     for k in sorted(outs):
@@ -145,6 +158,11 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--dump-stages", action="store_true")
     c.add_argument("--launch", type=_launch_pair, help="specialise to G,L (or GX,GY,LX,LY)")
     c.add_argument("--sizes", help="key=value file with the nat parameters to specialise")
+    c.add_argument("--init-new", action="store_true",
+                   help="zero-initialize allocations explicitly")
+    c.add_argument("--check-only", action="store_true")
+    c.add_argument("--simplify-indices", choices=["on", "off"], default="on",
+                   help="accepted for compatibility: CUDA subscripts are always range-simplified")
     _mode_flags(c)
     c.set_defaults(fn=_compile)
     r = sub.add_parser("run", help="execute on the GPU")
@@ -153,6 +171,8 @@ def build_parser() -> argparse.ArgumentParser:
     r.add_argument("--device", choices=["cuda"], default="cuda")
     r.add_argument("--gpu", type=int, default=0)
     r.add_argument("--launch", type=_launch_pair)
+    r.add_argument("--reverse", action="store_true",
+                   help="accepted for compatibility (parfor order is never fixed on the GPU)")
     _mode_flags(r)
     r.set_defaults(fn=_run)
     return ap

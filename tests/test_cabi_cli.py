@@ -120,3 +120,20 @@ def test_cli_dump_stages_reparse(tmp_path):
     env = {**dict(sp.params), "out": AccT(sp.body_type.data)}
     for stage in ("stage1", "stage2"):
         parse_phrase(open(str(tmp_path / f"dottiled.{stage}.dpia")).read(), env)
+
+
+def test_cli_reference_compile_flags(tmp_path, capsys):
+    """--check-only / --init-new / --simplify-indices behave like the
+    reference CLI's (SRC/cli.py:93-96, 236-246)."""
+    from conftest import load_golden
+    src = [c for c in load_golden("programs.json") if c["name"] == "dotvec.dpia"][0]["text"]
+    f = _prog(tmp_path, src, "dotvec.dpia")
+    assert main(["compile", f, "--check-only"]) == 0
+    out = capsys.readouterr().out
+    assert "OK" in out and not (tmp_path / "dotvec.cu").exists()
+    assert main(["compile", f, "--init-new", "--simplify-indices", "off", "-o",
+                 str(tmp_path / "x.cu")]) == 0
+    assert "__global__" in (tmp_path / "x.cu").read_text()
+    # the reference-only targets are not the CUDA backend's
+    with pytest.raises(SystemExit):
+        main(["compile", f, "--target", "opencl"])
