@@ -105,6 +105,51 @@ __device__ void body3(const float4* __restrict__ p, long long n4, float* out, un
   for (int o = 16; o; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
   if (threadIdx.x == 0) { out[0] = u; *ctr = 0; }
 }
+// MODE 4: every block but 0 publishes its partial and bumps the counter with
+// a fire-and-forget red.release; block 0 (after its own share) spins on an
+// acquire load of the counter, then combines the partials.
+__device__ void body4(const float4* __restrict__ p, long long n4, float* out, unsigned* ctr) {
+  long long per = n4 / gridDim.x;
+  const float4* q = p + blockIdx.x * per;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = per / blockDim.x;
+  #pragma unroll 16
+  for (int j = 0; j < k; ++j) {
+    float4 v = __ldg(q + (long long)j * blockDim.x + threadIdx.x);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  float s = acc.x + acc.y + acc.z + acc.w;
+  __shared__ float red[32];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+  for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  if (blockIdx.x != 0) {
+    if (threadIdx.x == 0) {
+      out[1 + blockIdx.x] = t;
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    unsigned c;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(ctr) : "memory");
+    } while (c != gridDim.x - 1);
+  }
+  __syncwarp();
+  float u = threadIdx.x == 0 ? t : 0.f;
+  for (int i = 1 + threadIdx.x; i < gridDim.x; i += 32) {
+    float v;
+    asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(out + 1 + i) : "memory");
+    u += v;
+  }
+  for (int o = 16; o; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
+  if (threadIdx.x == 0) { out[0] = u; *ctr = 0; }
+}
+extern "C" __global__ void __launch_bounds__(1024) read4(const float4* p, long long n4, float* out, unsigned* c) { body4(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read3(const float4* p, long long n4, float* out, unsigned* c) { body3(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read0(const float4* p, long long n4, float* out, unsigned* c) { body<0>(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read1(const float4* p, long long n4, float* out, unsigned* c) { body<1>(p, n4, out, c); }
@@ -145,7 +190,8 @@ def main():
     fe = mod.function("empty_k")
     print(f"empty       : {timed(st, lambda: RT.launch(fe, 0, (1, 1), (32, 1), 0, args, st)):7.2f} us",
           flush=True)
-    for name, label in (("read0", "read"), ("read1", "read+block"), ("read2", "read+grid"), ("read3", "read+grid-acqrel")):
+    for name, label in (("read0", "read"), ("read1", "read+block"), ("read2", "read+grid"), ("read3", "read+grid-acqrel"),
+                        ("read4", "read+spin0")):
         fn = mod.function(name)
         for blocks in (256, 512):
             t = timed(st, lambda: RT.launch(fn, 0, (blocks, 1), (1024, 1), 0, args, st))
