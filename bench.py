@@ -500,7 +500,7 @@ def _cfg_desc(cfg, world=1):
                 "scrubbed between steps"}
     return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",
                          "dot": "dot N=2^24 fp32, asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal",
-                         "gemv": "gemv 8192x8192 fp32, row per work-group, toLocal x",
+                         "gemv": "gemv 8192x8192 fp32, row per work-group, x staged toPrivate in the work-items column layout (registers)",
                          "scal": "scal N=2^26 fp32 (read + write), grid-stride mapGlobal over vec4",
                          "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
                                "tiles, toLocal k-tiles of 16, FFMA2"}[cfg.name],

@@ -76,9 +76,33 @@ def asum_program(L: int = 256, K: int = 32) -> str:
 """
 
 
-def gemv_program(M: int, N: int, L: int = 256) -> str:
-    """y = A x, one row per work-group, x staged in shared memory."""
+def gemv_program(M: int, N: int, L: int = 256, x_private: bool = False) -> str:
+    """y = A x, one row per work-group, x staged in shared memory
+    (toLocal, LICM'd out of the row loop).  x_private: x is staged with
+    toPrivate in the work-items' own column layout instead -- each work-item
+    keeps its k vec4 of x in registers (thread-sliced), so the rows need
+    neither shared-memory reads of x nor the staging barrier."""
     k = N // (4 * L)
+    dot4 = ("(+ (+ (idx (* (fst p) (snd p)) 0) (idx (* (fst p) (snd p)) 1))"
+            " (+ (idx (* (fst p) (snd p)) 2) (idx (* (fst p) (snd p)) 3)))")
+    if x_private:
+        return f"""
+(param A (exp (array {M} (array {N} num))))
+(param x (exp (array {N} num)))
+(mapWorkgroup
+ (lam (row (exp (array {N} num)))
+  (let (toPrivate (mapLocal (lam (c (exp (array {k} (vec 4)))) (mapSeq (lam (v (exp (vec 4))) v) c)))
+                  (transpose (split {L} (asVector4 x))))
+   (lam (xs (exp (array {L} (array {k} (vec 4)))))
+    (reduceLocal (+) 0
+     (toPrivate
+      (mapLocal
+       (lam (cc (exp (pair (array {k} (vec 4)) (array {k} (vec 4)))))
+        (reduceSeq (lam (p (exp (pair (vec 4) (vec 4)))) (lam (a (exp num)) (+ a {dot4})))
+                   0 (zip (fst cc) (snd cc)))))
+      (zip (transpose (split {L} (asVector4 row))) xs))))))
+ A)
+"""
     return f"""
 (param A (exp (array {M} (array {N} num))))
 (param x (exp (array {N} num)))
@@ -90,8 +114,7 @@ def gemv_program(M: int, N: int, L: int = 256) -> str:
      (lam (col (exp (array {k} (pair (vec 4) (vec 4)))))
       (reduceSeq
        (lam (p (exp (pair (vec 4) (vec 4)))) (lam (a (exp num))
-        (+ a (+ (+ (idx (* (fst p) (snd p)) 0) (idx (* (fst p) (snd p)) 1))
-                (+ (idx (* (fst p) (snd p)) 2) (idx (* (fst p) (snd p)) 3))))))
+        (+ a {dot4})))
        0 col)))
     (transpose (split {L} (zip (asVector4 row)
                                (asVector4 (toLocal (mapLocal (lam (v (exp num)) v)) x))))))))
@@ -299,8 +322,9 @@ def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 32, blocks=None) -> Co
     return Config("asum", asum_program(L, K), {"n": n}, (blocks or n, L), bytes=4 * N, flops=2 * N)
 
 
-def gemv_config(M: int = 8192, N: int = 8192, L: int = 512, blocks: int = 148 * 4) -> Config:
-    return Config("gemv", gemv_program(M, N, L), {}, (min(blocks, M), L),
+def gemv_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int = 148 * 8,
+                x_private: bool = True) -> Config:
+    return Config("gemv", gemv_program(M, N, L, x_private), {}, (min(blocks, M), L),
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
 

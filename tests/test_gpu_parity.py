@@ -85,9 +85,10 @@ def test_asum_strategy_int_exact(L, K, n, blocks):
     assert got == eval_phrase(prog.source.body, {"xs": xs}, {"n": n})
 
 
+@pytest.mark.parametrize("x_private", [False, True])
 @pytest.mark.parametrize("M,N,L,blocks", [(8, 256, 32, 3), (33, 512, 64, 7), (64, 1024, 256, 64)])
-def test_gemv_strategy_int_exact(M, N, L, blocks):
-    prog = compile_program(gemv_program(M, N, L))
+def test_gemv_strategy_int_exact(M, N, L, blocks, x_private):
+    prog = compile_program(gemv_program(M, N, L, x_private))
     A = np.random.default_rng(4).integers(-9, 10, (M, N))
     x = np.random.default_rng(5).integers(-9, 10, N)
     got = run_program_cuda(prog, {"A": A.tolist(), "x": x.tolist()}, launch=(blocks, L),

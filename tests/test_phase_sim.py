@@ -42,6 +42,8 @@ STRATS = [
     ("asum", asum_program(32, 2), {"n": 2}, (3, 32), lambda: {"xs": _ints(512, 3)}),
     ("gemv", gemv_program(3, 256, 32), {}, (2, 32),
      lambda: {"A": [_ints(256, 3 + r) for r in range(3)], "x": _ints(256, 11)}),
+    ("gemv_xpriv", gemv_program(3, 256, 32, x_private=True), {}, (2, 32),
+     lambda: {"A": [_ints(256, 3 + r) for r in range(3)], "x": _ints(256, 11)}),
     ("mm", mm_program(16, 16, 16, 8, 4, 4), {}, ((2, 2), (2, 2)),
      lambda: {"A": [_ints(16, 3 + r) for r in range(16)], "B": [_ints(16, 5 + r) for r in range(16)]}),
     # one vec4 staging load per work-item: the k-loop is software-pipelined

@@ -1,6 +1,6 @@
 """Strategy/geometry sweep for the HBM-bound benchmark programs (GPU box).
 
-    python tools/sweep.py asum|dot|gemv
+    python tools/sweep.py asum|dot|gemv|gemvp   (gemvp: x staged toPrivate)
 
 Prints achieved GB/s (median of event-timed launches, L2 scrubbed between
 launches) for each (L, K, blocks) strategy parameterisation.
@@ -65,8 +65,9 @@ def main(which):
     else:
         inputs = {"A": rng.uniform(-1, 1, (8192, 8192)).astype(np.float32),
                   "x": rng.uniform(-1, 1, 8192).astype(np.float32)}
+        xp = which == "gemvp"
         grid = [(L, None, b) for L in (128, 256, 512, 1024) for b in (148, 296, 592, 1184, 2368, 8192)]
-        mk = lambda L, K, b: gemv_config(L=L, blocks=b)  # noqa: E731
+        mk = lambda L, K, b: gemv_config(L=L, blocks=b, x_private=xp)  # noqa: E731
     for L, K, b in grid:
         try:
             cfg = mk(L, K, b)
