@@ -169,8 +169,17 @@ class CudaSignature:
         return out
 
 
+MAX_BLOCK_THREADS = 1024
+MAX_GRID = (2 ** 31 - 1, 65535)
+
+
 def normalize_launch(launch):
-    """(G, L) | ((gx, gy), (lx, ly)) -> ((gx, gy), (lx, ly))."""
+    """(G, L) | ((gx, gy), (lx, ly)) -> ((gx, gy), (lx, ly)), the physical
+    CUDA geometry.  The reference accepts any positive (G, L) -- every level
+    is a stride loop, so results never depend on the geometry (SPEC.md:488,
+    SRC/opencl.py:407-409).  CUDA caps a block at 1024 threads and gridDim.y
+    at 65535, so larger requests run as capped blocks/grids whose work-group
+    and work-item loops stride over the remaining iterations."""
     if launch is None:
         return None
     g, l = launch
@@ -178,7 +187,13 @@ def normalize_launch(launch):
     l = (l, 1) if isinstance(l, int) else tuple(l)
     if min(g + l) < 1:
         raise ValueError("launch parameters must be positive")
-    return (g[0], g[1]), (l[0], l[1])
+    lx, ly = l
+    while lx * ly > MAX_BLOCK_THREADS:
+        if ly > 1:
+            ly = max(1, MAX_BLOCK_THREADS // lx) if lx <= MAX_BLOCK_THREADS else 1
+        else:
+            lx = MAX_BLOCK_THREADS
+    return (min(g[0], MAX_GRID[0]), min(g[1], MAX_GRID[1])), (lx, ly)
 
 
 # ----------------------------------------------------- syntactic analyses

@@ -47,6 +47,25 @@ def test_golden_programs(case, launch):
     _check(case, launch)
 
 
+@pytest.mark.parametrize("launch", [(3, 2048), (2, 4096)])
+@pytest.mark.parametrize("case", GOLDEN, ids=lambda c: c["name"])
+def test_golden_programs_oversized_work_groups(case, launch):
+    """The reference accepts any (G, L); work-groups above CUDA's 1024
+    threads run as 1024-thread blocks with striding work-item loops."""
+    _check(case, launch)
+
+
+def test_mm_oversized_2d_launch():
+    """A 64 x 64 work-item request (4096 > 1024) for mm: the block is capped
+    to 64 x 16 and mapLocal1 strides; the product is unchanged."""
+    M = N = K = 128
+    prog = compile_program(mm_program(M, N, K, 128, 8, 8))
+    A = np.random.default_rng(40).integers(-9, 10, (M, K))
+    B = np.random.default_rng(41).integers(-9, 10, (K, N))
+    got = run_program_cuda(prog, {"A": A, "B": B}, launch=((1, 1), (64, 64)), float_mode=False, flat=True)
+    assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
+
+
 @pytest.mark.parametrize("case", FUZZ, ids=lambda c: f"seed{c['seed']}")
 def test_reference_fuzz_programs(case):
     """Kernel-legal programs (the reference simulates them) must run; the

@@ -144,6 +144,50 @@ def one(variant):
     st.sync()
 
 
+def transforms():
+    """Source-level experiments on the emitted default mm kernel (timing
+    only): unroll2 = `#pragma unroll 2` on the k-tile loop (slice offsets of
+    the rotated stagings become constants)."""
+    import re
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.launcher import Executable
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    cfg = mm_config()
+    prog = compile_program(cfg.text, name="mm")
+    outs = [(n, t) for n, t, k in prog.params if k == "out"]
+    ins = [(n, t) for n, t, k in prog.params if k == "in"]
+    src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
+    k_loop = re.search(r"\n(\s*)for \(int (i_\d+_\d+) = 0; \2 < 256; \2 \+= 1\) \{", src)
+    variants = {"emitted": src}
+    if k_loop:
+        variants["unroll2"] = src[:k_loop.start()] + f"\n{k_loop.group(1)}#pragma unroll 2" + src[k_loop.start():]
+        variants["unroll1"] = src[:k_loop.start()] + f"\n{k_loop.group(1)}#pragma unroll 1" + src[k_loop.start():]
+    ref = None
+    for label, s in variants.items():
+        exe = Executable(s, sig, 0, True, {}, geometry=cfg.launch).compile().allocate()
+        exe.upload("A", A, st)
+        exe.upload("B", B, st)
+        ts = []
+        for i in range(13):
+            RT.lib().dpia_l2_flush(0, st.handle)
+            e0, e1 = RT.Event(0), RT.Event(0)
+            e0.record(st)
+            exe.launch(st)
+            e1.record(st)
+            st.sync()
+            if i >= 3:
+                ts.append(e0.elapsed_ms(e1))
+        out = exe.download("out", st)
+        ref = out if ref is None else ref
+        ms = statistics.mean(ts)
+        print(f"{label}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  same={np.array_equal(out, ref)}",
+              flush=True)
+
+
 def sts_bound():
     """Upper bound of what conflict-free transposed A stores would gain: the
     emitted BK=16 kernel with its A-tile store index replaced by a
@@ -188,6 +232,9 @@ def sts_bound():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "xform":
+        transforms()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "rect":
         rect()
         sys.exit(0)
