@@ -13,7 +13,8 @@ from .stage2 import stage2  # noqa: F401
 from .cuda.ctypes_map import CudaError  # noqa: F401
 from .cuda.emit import CudaSignature, emit_cuda  # noqa: F401
 from .launcher import Executable, run_kernel  # noqa: F401
-from .cuda.hierarchy import HoistedBuffer, cuda_legal, hoist_allocations, lint_hierarchy  # noqa: F401
+from .cuda.hierarchy import (HoistedBuffer, WorkItemRace, check_work_item_races, cuda_legal,  # noqa: F401
+                             hoist_allocations, lint_hierarchy)
 from .api import Program, compile_program, executable, run_program_cuda  # noqa: F401
 from .checker import DpiaTypeError, type_check  # noqa: F401
 from .pretty import pretty_print  # noqa: F401
@@ -22,4 +23,5 @@ __all__ = ["parse", "parse_phrase", "translate_program", "stage2", "emit_cuda", 
            "compile_program", "run_program_cuda", "executable", "CudaError", "ParseError",
            "ElabError", "SourceProgram", "Program", "Executable", "CudaSignature",
            "hoist_allocations", "lint_hierarchy", "cuda_legal", "HoistedBuffer",
+           "WorkItemRace", "check_work_item_races",
            "type_check", "DpiaTypeError", "pretty_print"]

@@ -122,3 +122,81 @@ def lint_hierarchy(p: Phrase) -> List[str]:
 
 def cuda_legal(p: Phrase) -> bool:
     return not lint_hierarchy(p)
+
+
+class WorkItemRace(Exception):
+    """Parallel iterations write the same location -- the CUDA counterpart
+    of the reference's `WorkItemRace` (SRC/opencl.py:327-336), which its
+    work-item simulator raises from write footprints (:465-470)."""
+
+    def __init__(self, loop: str, target: str):
+        super().__init__(f"cross-work-item write overlap: every iteration of {loop} writes "
+                         f"{target} at an index that does not depend on the iteration")
+        self.loop, self.target = loop, target
+
+
+def _free_names(q: Phrase) -> set:
+    if isinstance(q, Var):
+        return {q.name}
+    if isinstance(q, Lam):
+        return _free_names(q.body) - {q.binder}
+    return set().union(*[_free_names(c) for c in children(q)]) if children(q) else set()
+
+
+def check_work_item_races(p: Phrase) -> None:
+    """Reject parallel loops whose iterations all write one location of an
+    identifier captured from outside the loop (not through the loop's own
+    acceptor): an assignment rooted at a captured identifier must index it
+    with an expression that depends on the iteration variable somewhere on
+    its access path.  Stage I/II output never does this (the translation is
+    race-free by construction, SRC/checker.py); the reference's hoisted form
+    indexes its hoisted buffers by the loop variable, which passes."""
+
+    def root_and_indices(a: Phrase):
+        idxs = []
+        while True:
+            if isinstance(a, Var):
+                return a.name, idxs
+            if isinstance(a, Proj) and isinstance(a.target, Var):
+                return a.target.name, idxs
+            u = unapply(a)
+            if u is None or not u[2]:
+                return None, idxs
+            name, _targs, args = u
+            if name == "idxAcc" and len(args) == 2:
+                idxs.append(args[1])
+            a = args[0]
+
+    def walk(q: Phrase, loops: List[Tuple[str, str, set]]):
+        u = unapply(q)
+        if u is not None:
+            name, targs, args = u
+            if name in PARFOR_FAMILY and len(args) == 2 and isinstance(args[1], Lam) \
+                    and isinstance(args[1].body, Lam):
+                a, f = args
+                walk(a, loops)
+                for _lname, _ivar, own in loops:
+                    own.update((f.binder, f.body.binder))
+                inner = loops + [(name, f.binder, {f.body.binder})]
+                walk(f.body.body, inner)
+                return
+            if name == ":=" and args and isinstance(args[0], PairP):
+                root, idxs = root_and_indices(args[0].fst)
+                if root is not None:
+                    used = set().union(*[_free_names(e) for e in idxs]) if idxs else set()
+                    for lname, ivar, own in reversed(loops):
+                        if root in own:
+                            break          # written through this loop's acceptor
+                        if ivar not in used:
+                            raise WorkItemRace(f"{lname} over {ivar}", root)
+        if isinstance(q, Lam):
+            # names bound inside a loop (new* buffers, for/inner binders) are
+            # per-iteration, not captured
+            for _lname, _ivar, own in loops:
+                own.add(q.binder)
+            walk(q.body, loops)
+            return
+        for c in children(q):
+            walk(c, loops)
+
+    walk(p, [])

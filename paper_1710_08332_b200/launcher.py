@@ -20,6 +20,7 @@ import numpy as np
 from . import layout as LY
 from . import runtime as RT
 from .cuda.emit import CudaSignature, emit_cuda, normalize_launch
+from .cuda.hierarchy import check_work_item_races
 from .dtypes import DataType
 from .terms import Phrase
 
@@ -146,6 +147,7 @@ def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None
     sigma = dict(sigma or {})
     outs, ins = _split_params(params)
     geom = normalize_launch(launch)
+    check_work_item_races(p)   # the reference simulator's WorkItemRace (SRC/opencl.py:465-470)
     src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name,
                          sigma=sigma if specialize else None, launch=geom if specialize else None)
     exe = Executable(src, sig, device, float_mode, sigma, geometry=geom)

@@ -340,3 +340,22 @@ def test_pretty_print_benchmark_strategies():
         for ph in (sp.body, translate_program(sp.body, sp.body_type.data, "out", "global")):
             q, _ = parse_phrase(show(ph), {**env, "out": AccT(sp.body_type.data)})
             assert alpha_equal(q, ph)
+
+
+def test_run_kernel_reports_cross_item_races():
+    """TST/test_opencl.py:171-178: every work-item writing out[0] is a
+    WorkItemRace, raised before anything is compiled or launched (no GPU
+    needed); writing out[i] is not."""
+    from paper_1710_08332_b200 import WorkItemRace, run_kernel
+    from paper_1710_08332_b200.dtypes import AccT, Array, Num
+    from paper_1710_08332_b200.reader import parse_phrase
+    from paper_1710_08332_b200.sizes import nat
+    from paper_1710_08332_b200.cuda.hierarchy import check_work_item_races
+    t = Array(nat(4), Num())
+    racy, _ = parse_phrase("(parforGlobal out (lam (i (exp (idx 4))) (lam (o (acc num)) (:= (idxAcc out 0) 1))))",
+                           {"out": AccT(t)})
+    with pytest.raises(WorkItemRace):
+        run_kernel(racy, [("out", t, "out")], {}, (2, 2))
+    ok, _ = parse_phrase("(parforGlobal out (lam (i (exp (idx 4))) (lam (o (acc num)) (:= (idxAcc out i) 1))))",
+                         {"out": AccT(t)})
+    check_work_item_races(ok)
