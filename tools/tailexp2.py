@@ -149,6 +149,49 @@ __device__ void body4(const float4* __restrict__ p, long long n4, float* out, un
   for (int o = 16; o; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
   if (threadIdx.x == 0) { out[0] = u; *ctr = 0; }
 }
+// MODE 5: two-level ticket (16 blocks per group counter, then a top
+// counter over the groups): at most 16-way contention per counter.
+__device__ void body5(const float4* __restrict__ p, long long n4, float* out, unsigned* ctr) {
+  long long per = n4 / gridDim.x;
+  const float4* q = p + blockIdx.x * per;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = per / blockDim.x;
+  #pragma unroll 16
+  for (int j = 0; j < k; ++j) {
+    float4 v = __ldg(q + (long long)j * blockDim.x + threadIdx.x);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  float s = acc.x + acc.y + acc.z + acc.w;
+  __shared__ float red[32];
+  __shared__ bool last;
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  float t = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+  for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+  const unsigned G = 16, ngroups = (gridDim.x + G - 1) / G, grp = blockIdx.x / G;
+  const unsigned gsize = min(G, gridDim.x - grp * G);
+  unsigned go = 0;
+  if (threadIdx.x == 0) {
+    out[1 + blockIdx.x] = t;
+    __threadfence();
+    go = atomicAdd(ctr + 1 + grp, 1u) == gsize - 1;
+    if (go) {
+      ctr[1 + grp] = 0;
+      __threadfence();
+      go = atomicAdd(ctr, 1u) == ngroups - 1 ? 2 : 0;
+    }
+  }
+  go = __shfl_sync(0xffffffffu, go, 0);
+  if (go != 2) return;
+  __threadfence();
+  float u = 0.f;
+  for (int i = threadIdx.x; i < gridDim.x; i += 32) u += ((volatile float*)out)[1 + i];
+  for (int o = 16; o; o >>= 1) u += __shfl_down_sync(0xffffffffu, u, o);
+  if (threadIdx.x == 0) { out[0] = u; *ctr = 0; }
+}
+extern "C" __global__ void __launch_bounds__(1024) read5(const float4* p, long long n4, float* out, unsigned* c) { body5(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read4(const float4* p, long long n4, float* out, unsigned* c) { body4(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read3(const float4* p, long long n4, float* out, unsigned* c) { body3(p, n4, out, c); }
 extern "C" __global__ void __launch_bounds__(1024) read0(const float4* p, long long n4, float* out, unsigned* c) { body<0>(p, n4, out, c); }
@@ -191,7 +234,7 @@ def main():
     print(f"empty       : {timed(st, lambda: RT.launch(fe, 0, (1, 1), (32, 1), 0, args, st)):7.2f} us",
           flush=True)
     for name, label in (("read0", "read"), ("read1", "read+block"), ("read2", "read+grid"), ("read3", "read+grid-acqrel"),
-                        ("read4", "read+spin0")):
+                        ("read4", "read+spin0"), ("read5", "read+grid-2level")):
         fn = mod.function(name)
         for blocks in (256, 512):
             t = timed(st, lambda: RT.launch(fn, 0, (blocks, 1), (1024, 1), 0, args, st))
