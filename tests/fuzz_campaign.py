@@ -1,6 +1,6 @@
 """Long GPU differential-fuzz campaign (GPU box; test infrastructure).
 
-    python tools/fuzz_campaign.py START END
+    python tests/fuzz_campaign.py START END
 
 Runs seeds [START, END) of the hierarchical strategy generator
 (tests/strategy_gen.py) through the public API in int and float mode, at the

@@ -1,7 +1,7 @@
 """Workload for compute-sanitizer (GPU box; tests/test_sanitizer.py runs it
 under --tool memcheck / racecheck / synccheck).
 
-    compute-sanitizer --tool racecheck --error-exitcode 1 python tools/sanitize_run.py
+    compute-sanitizer --tool racecheck --error-exitcode 1 python tests/sanitize_run.py
 
 Runs every benchmark strategy at a reduced size, the reference's golden
 programs and a sample of the hierarchical strategy fuzzer (tests/strategy_gen)

@@ -9,7 +9,7 @@ the same guarantee is checked on the hardware.
   views, 64-bit indices, scratch slices);
 * synccheck -- divergent or invalid __syncthreads (fused grid tails).
 
-The workload (tools/sanitize_run.py) also checks every result against the
+The workload (tests/sanitize_run.py) also checks every result against the
 oracle."""
 import os
 import shutil
@@ -32,7 +32,7 @@ def test_compute_sanitizer(tool):
     cmd = [SAN, "--tool", tool, "--error-exitcode", "97"]
     if tool == "racecheck":
         cmd += ["--racecheck-report", "all"]
-    cmd += [sys.executable, os.path.join(ROOT, "tools", "sanitize_run.py")]
+    cmd += [sys.executable, os.path.join(ROOT, "tests", "sanitize_run.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, env=env)
     out = r.stdout + r.stderr
     assert "SANITIZE WORKLOAD DONE" in out, out[-4000:]
@@ -47,7 +47,7 @@ def test_racecheck_detects_missing_barriers():
     if not os.path.exists(SAN):
         pytest.skip("compute-sanitizer not installed")
     cmd = [SAN, "--tool", "racecheck", "--error-exitcode", "97", sys.executable,
-           os.path.join(ROOT, "tools", "sanitize_run.py"), "--broken"]
+           os.path.join(ROOT, "tests", "sanitize_run.py"), "--broken"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     out = r.stdout + r.stderr
     assert "BROKEN WORKLOAD DONE" in out, out[-4000:]
