@@ -278,6 +278,82 @@ def mm_rect_program(M: int, N: int, K: int, TM: int = 128, TN: int = 128, BK: in
 """
 
 
+def mm_rowa_program(M: int, N: int, K: int, T: int = 128, BK: int = 16, R: int = 8) -> str:
+    """mm_program's tiling with the A tile staged *row-major* (no transposed
+    stores: one conflict-free 16-byte shared store per vec4 load) and a
+    micro-kernel that walks each k-tile in k-quads: per quad every work-item
+    reads its R rows of A as R 16-byte vectors and the 4 B rows, then does 4
+    outer-product steps.  The inner step iterates rows outer and columns
+    inner over a transposed view of the (column-major) register tile, so
+    consecutive columns pair up for FFMA2 with the A value broadcast."""
+    P = T // R
+    Q = 4 if R % 4 == 0 else R
+    H = R // Q
+    zero_t = f"(array {P} (array {P} (array {R} (array {R} num))))"
+    a_stage = (f"(toLocal (lam t (split {BK} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {P} (asVector4 (join t)))))))) (fst tiles))")
+    b_stage = (f"(toLocal (lam t (split {T} (asScalar4 (join (mapLocal1 (lam r (mapLocal (lam v v) r))"
+               f" (split {P} (asVector4 (join t)))))))) (snd tiles))")
+    micro = f"""
+          (reduceSeq
+           (lam (ab (exp (pair (array {R} (vec 4)) (array 4 (array {R} num)))))
+            (lam (t (exp (array {R} (array {R} num))))
+             (reduceSeq
+              (lam (ak (exp (pair (array {R} num) (array {R} num))))
+               (lam (t2 (exp (array {R} (array {R} num))))
+                (transpose
+                 (mapSeq (lam (q (exp (pair num (array {R} num))))
+                          (mapSeq (lam (w (exp (pair num num))) (+ (snd w) (* (fst w) (fst q))))
+                                  (zip (snd ak) (snd q))))
+                         (zip (fst ak) (transpose t2))))))
+              t
+              (zip (transpose (split 4 (asScalar4 (fst ab)))) (snd ab)))))
+           (snd pb)
+           (zip (transpose (split {BK // 4} (asVector4 (join (fst pa)))))
+                (split 4 (transpose (join (fst pb))))))"""
+    return f"""
+(param A (exp (array {M} (array {K} num))))
+(param B (exp (array {K} (array {N} num))))
+(join
+ (mapWorkgroup1
+  (lam (aRows (exp (array {T} (array {K} num))))
+   (transpose
+    (mapWorkgroup
+     (lam (bCols (exp (array {T} (array {K} num))))
+      (join
+       (mapLocal1
+        (lam (accRow (exp (array {P} (array {R} (array {R} num)))))
+         (transpose (join (join (transpose
+          (mapLocal (lam (blk (exp (array {R} (array {R} num))))
+                     (split {Q} (mapSeq (mapSeq (lam (z (exp num)) z)) blk)))
+                    accRow))))))
+        (reduceSeq
+         (lam (tiles (exp (pair (array {T} (array {BK} num)) (array {BK} (array {T} num)))))
+          (lam (acc (exp {zero_t}))
+           (let {b_stage}
+            (lam (bl (exp (array {BK} (array {T} num))))
+             (mapLocal1
+              (lam (pa (exp (pair (array {R} (array {BK} num)) (array {P} (array {R} (array {R} num))))))
+               (mapLocal
+                (lam (pb (exp (pair (array {H} (array {Q} (array {BK} num))) (array {R} (array {R} num)))))
+                 {micro})
+                (zip (transpose (split {P} (split {Q} (transpose bl)))) (snd pa))))
+              (zip (split {R} {a_stage}) acc))))))
+         (mapLocal1 (lam r (mapLocal (lam b (mapSeq (mapSeq (lam z z)) b)) r)) (as {zero_t} 0))
+         (zip (transpose (split {K // BK} (split {BK} (join aRows))))
+              (split {BK} (transpose bCols)))))))
+     (split {T} (transpose B)))))
+  (split {T} A)))
+"""
+
+
+def mm_rowa_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int = 16,
+                   R: int = 8) -> Config:
+    P = T // R
+    return Config("mm", mm_rowa_program(M, N, K, T, BK, R), {}, ((N // T, M // T), (P, P)),
+                  bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
+
+
 def mm_rect_config(M: int = 4096, N: int = 4096, K: int = 4096, TM: int = 128, TN: int = 128,
                    BK: int = 16, RM: int = 8, RN: int = 16) -> Config:
     return Config("mm", mm_rect_program(M, N, K, TM, TN, BK, RM, RN), {},

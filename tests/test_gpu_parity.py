@@ -186,13 +186,16 @@ def test_mm_rect_strategy_int_exact(M, N, K, TM, TN, BK, RM, RN):
     assert np.array_equal(np.asarray(got, np.int64).reshape(M, N), A @ B)
 
 
-@pytest.mark.parametrize("variant", ["square", "rows", "sectors", "rect8x16", "rect16x8", "bk8"])
+@pytest.mark.parametrize("variant", ["square", "rows", "sectors", "rect8x16", "rect16x8", "bk8", "rowa"])
 def test_mm_variants_fp32(variant):
     """fp32 (the FFMA2 register-tile update, swizzled shared tiles) for every
     mm strategy variant, against a float64 product; bound 1e-4 * sum|terms|."""
     from paper_1710_08332_b200.bench_programs import mm_rect_program
     M, N, K = 256, 256, 512
-    if variant.startswith("rect"):
+    if variant == "rowa":
+        from paper_1710_08332_b200.bench_programs import mm_rowa_program
+        text, launch = mm_rowa_program(M, N, K, 128, 16, 8), ((2, 2), (16, 16))
+    elif variant.startswith("rect"):
         RM, RN = (8, 16) if variant == "rect8x16" else (16, 8)
         text, launch = mm_rect_program(M, N, K, 128, 128, 16, RM, RN), ((2, 2), (128 // RN, 128 // RM))
     else:

@@ -9,7 +9,7 @@ from oracle.dpia_eval import eval_phrase, flatten_value, from_json
 from oracle.phase_sim import PhaseRace, Sim, simulate
 from paper_1710_08332_b200 import compile_program
 from paper_1710_08332_b200.bench_programs import (asum_program, dot_program, gemv_program,
-                                                  mm_program, mm_rect_program)
+                                                  mm_program, mm_rect_program, mm_rowa_program)
 
 GOLDEN = load_golden("programs.json")
 FUZZ_LEGAL = [c for c in load_golden("fuzz.json") if c["reparses"] and c["opencl_legal"]][:60]
@@ -58,6 +58,9 @@ STRATS = [
     # rectangular output and register tiles (8 x 16 tile, 2 x 8 register tiles)
     ("mm_rect", mm_rect_program(16, 32, 16, 8, 16, 4, 2, 8), {}, ((2, 2), (2, 4)),
      lambda: {"A": [_ints(16, 3 + r) for r in range(16)], "B": [_ints(32, 5 + r) for r in range(16)]}),
+    # row-major A tile, k-quad micro-kernel over a transposed accumulator view
+    ("mm_rowa", mm_rowa_program(32, 32, 32, 16, 8, 4), {}, ((2, 2), (4, 4)),
+     lambda: {"A": [_ints(32, 3 + r) for r in range(32)], "B": [_ints(32, 5 + r) for r in range(32)]}),
 ]
 
 

@@ -17,7 +17,7 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
-from paper_1710_08332_b200.bench_programs import mm_config, mm_rect_config  # noqa: E402
+from paper_1710_08332_b200.bench_programs import mm_config, mm_rect_config, mm_rowa_config  # noqa: E402
 
 
 def run(cfg, inputs, st, pad_smem=None, reps=10):
@@ -144,6 +144,44 @@ def one(variant):
     st.sync()
 
 
+def rowa():
+    """Row-major A staging + k-quad micro-kernel (mm_rowa_program), as
+    emitted and with __launch_bounds__(256, 2)."""
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.launcher import Executable
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    ref = (A[:64].astype(np.float64) @ B.astype(np.float64))
+    for BK in (16, 8):
+        cfg = mm_rowa_config(BK=BK)
+        prog = compile_program(cfg.text, name="mm")
+        outs = [(n, t) for n, t, k in prog.params if k == "out"]
+        ins = [(n, t) for n, t, k in prog.params if k == "in"]
+        src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
+        for label, s in (("emitted", src), ("lb(256,2)", src.replace("__launch_bounds__(256)",
+                                                                     "__launch_bounds__(256, 2)"))):
+            exe = Executable(s, sig, 0, True, {}, geometry=cfg.launch).compile().allocate()
+            exe.upload("A", A, st)
+            exe.upload("B", B, st)
+            ts = []
+            for i in range(13):
+                RT.lib().dpia_l2_flush(0, st.handle)
+                e0, e1 = RT.Event(0), RT.Event(0)
+                e0.record(st)
+                exe.launch(st)
+                e1.record(st)
+                st.sync()
+                if i >= 3:
+                    ts.append(e0.elapsed_ms(e1))
+            out = exe.download("out", st).reshape(4096, 4096)
+            ms = statistics.mean(ts)
+            print(f"rowa BK={BK} {label}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
+                  f"max|err| = {float(np.max(np.abs(out[:64] - ref))):.2e}", flush=True)
+
+
 def transforms():
     """Source-level experiments on the emitted default mm kernel (timing
     only): unroll2 = `#pragma unroll 2` on the k-tile loop (slice offsets of
@@ -232,6 +270,9 @@ def sts_bound():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "rowa":
+        rowa()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "xform":
         transforms()
         sys.exit(0)
