@@ -7,10 +7,12 @@ Headline workload (BASELINE.json configs[1]): asum over N = 2^26 fp32 with
 the vectorised asVector(4) + mapWorkgroup/mapLocal + reduceLocal strategy.
 A "step" is one pass of the emitted program over the resident input (all of
 its kernels, the fused work-group/grid combine included); L2 is flushed
-between steps (2x-L2 memset, outside the timed events).  Multi-GPU (torchrun,
+between steps (a 2x-L2 read, outside the timed events).  Multi-GPU (torchrun,
 one process per GPU): every rank runs the full per-GPU workload on its own
-shard (weak scaling) and the partial sums are combined with an NCCL
-all-reduce inside the step; the time is the max over ranks.
+shard (weak scaling) and the partial sums are combined inside the step --
+by default inside the kernel itself over NVLink (--combine peer: the fused
+cross-GPU combine of paper_1710_08332_b200/peer.py), or with a 4-byte NCCL
+all-reduce after it (--combine nccl); the time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -144,13 +146,17 @@ class Clocks:
 
 # ------------------------------------------------------------ workloads
 
-def make_workload(name, device, rank=0, world=1):
+def make_workload(name, device, rank=0, world=1, combine="nccl"):
     """(config, executable, host inputs or None, prepare(stream))."""
+    allgather = None
+    if world > 1 and combine == "peer":
+        from paper_1710_08332_b200.peer import torch_allgather as allgather
     if name.startswith("scaleout"):
         from paper_1710_08332_b200.bench_programs import Config
         from paper_1710_08332_b200.scaleout import ShardedReduction
         kind = "dot" if name.endswith("dot") else "asum"
-        run = ShardedReduction(kind, 1 << 31, world, rank, device)
+        run = ShardedReduction(kind, 1 << 31, world, rank, device,
+                               combine=combine if world > 1 else "nccl", allgather=allgather)
         cfg = Config(name, "", {"n": run.shard.chunks}, run.exe.sig.launch, bytes=run.bytes,
                      flops=(2 if kind == "dot" else 1) * run.shard.elems)
         return cfg, run.exe, None, run.fill_inputs
@@ -173,7 +179,11 @@ def make_workload(name, device, rank=0, world=1):
     else:
         raise SystemExit(f"unknown workload {name}")
     prog = compile_program(cfg.text, name=name)
-    exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device)
+    peer = None
+    if allgather is not None and name in ("asum", "dot"):
+        from paper_1710_08332_b200.peer import PeerGroup
+        peer = PeerGroup(device, rank, world, 1, allgather)
+    exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device, peer=peer)
 
     def prepare(stream):
         for n, v in inputs.items():
@@ -338,6 +348,9 @@ def main():
     ap.add_argument("--workload", default="asum")
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--combine", choices=["peer", "nccl"], default="peer",
+                    help="cross-GPU combine of the partial sums (N > 1): inside the kernel over "
+                         "NVLink (peer) or a 4-byte ncclAllReduce after it")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -350,7 +363,23 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
-        if args.impl == "ours":
+        if args.impl == "ours" and args.combine == "peer":
+            # collective capability probe: every rank maps every peer's
+            # mailbox (CUDA IPC + NVLink P2P); if any rank cannot, all ranks
+            # fall back to the NCCL combine together
+            ok = 1
+            try:
+                from paper_1710_08332_b200.peer import PeerGroup, torch_allgather
+                RT.init(local)
+                PeerGroup(local, rank, world, 1, torch_allgather).close()
+            except Exception as e:  # noqa: BLE001
+                print(f"rank {rank}: peer combine unavailable ({e}); using NCCL", file=sys.stderr)
+                ok = 0
+            t = torch.tensor([ok], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            if not int(t.item()):
+                args.combine = "nccl"
+        if args.impl == "ours" and args.combine == "nccl":
             import ctypes
             uid = ctypes.create_string_buffer(128)
             if rank == 0:
@@ -384,11 +413,11 @@ def main():
     peak, peak_src = peaks()
 
     def measure(workload, steps, warmup, with_e2e):
-        cfg, exe, inputs, prepare = make_workload(workload, device, rank, world)
+        cfg, exe, inputs, prepare = make_workload(workload, device, rank, world, args.combine)
         prepare(stream)
         stream.sync()
         allreduce = None
-        if world > 1:
+        if world > 1 and exe.peer is None:
             import torch
             outbuf = exe.buffers["out"]
 
@@ -398,11 +427,22 @@ def main():
         if dist is not None:
             dist.barrier()
         RT.lib().dpia_device_sync(device)
+        # keep the GPU under the same load for ~0.6 s so nvidia-smi's 100 ms
+        # sampler sees the clocks of the timed region; every rank does the
+        # same number of launches (the fused peer combine pairs them up)
+        t_b = time.perf_counter()
+        for _ in range(20):
+            RT.lib().dpia_l2_flush(device, stream.handle)
+            exe.launch(stream)
+        stream.sync()
+        batches = max(1, int(0.6 / max(time.perf_counter() - t_b, 1e-4)))
+        if dist is not None:
+            import torch
+            t = torch.tensor([batches], device=f"cuda:{local}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            batches = int(t.item())
         with Clocks(device) as clk:
-            # keep the GPU under the same load for ~0.6 s so nvidia-smi's
-            # 100 ms sampler sees the clocks of the timed region
-            t_soak = time.perf_counter()
-            while time.perf_counter() - t_soak < 0.6:
+            for _ in range(batches):
                 for _ in range(20):
                     RT.lib().dpia_l2_flush(device, stream.handle)
                     exe.launch(stream)
@@ -450,6 +490,8 @@ def main():
                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                           "ms_per_step": round(e2e_ms, 4),
                           "path": "Executable.run (public API): pinned H2D + kernels + D2H + stream sync"}
+        if exe.peer is not None:
+            exe.peer.check()      # no rank timed out waiting for a peer's partial
         return res
 
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
@@ -479,7 +521,8 @@ def main():
             "dtype": "f32",
             "data": ("synthetic (device-side counter hash, per-shard global offsets)" if strong
                      else "synthetic (numpy default_rng uniform, resident in HBM)"),
-            "config": _cfg_desc(cfg, world),
+            "config": dict(_cfg_desc(cfg, world, args.combine),
+                           **({"combine": args.combine} if world > 1 else {})),
             "roofline": head["roofline"], "e2e": head.get("e2e"), "clocks": head["clocks"],
             "gpu_launches": args.steps * (len(exe.sig.kernels) + 1),
             "gpu_launches_breakdown": {"emitted program kernels": args.steps * len(exe.sig.kernels),
@@ -491,11 +534,13 @@ def main():
     print(json.dumps(line), flush=True)
 
 
-def _cfg_desc(cfg, world=1):
+def _cfg_desc(cfg, world=1, combine="nccl"):
     if cfg.name.startswith("scaleout"):
         kind = "dot" if cfg.name.endswith("dot") else "asum"
-        return {"workload": f"{kind} scale-out N=2^31 fp32 total, {world} shard(s), NCCL all-reduce "
-                            "of the 4-byte partials", "sigma_per_rank": cfg.sigma,
+        return {"workload": f"{kind} scale-out N=2^31 fp32 total, {world} shard(s), partials combined "
+                            + ("inside the kernel over NVLink (peer)" if combine == "peer" and world > 1
+                               else "by a 4-byte NCCL all-reduce" if world > 1 else "(one shard)"),
+                "sigma_per_rank": cfg.sigma,
                 "launch": list(cfg.launch), "l2": "inputs (>= 1 GiB per GPU) exceed L2; L2 also "
                 "scrubbed between steps"}
     return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",

@@ -81,6 +81,15 @@ int dpia_fill_hash_f32(int device, uint64_t dptr, uint64_t count, uint64_t offse
                        float lo, float hi, void* stream);
 
 /* ---- multi-GPU (NCCL, loaded at run time from the torch wheel) ---------- */
+/* Peer mailboxes for the fused cross-GPU combine (emit_cuda(..., peer=True)):
+ * a zeroed device allocation exported as a 64-byte CUDA IPC handle, and the
+ * mapping of a peer's handle into this device's context (NVLink P2P, peer
+ * access enabled lazily).  Replaces ncclAllReduce of the per-rank partials
+ * with stores into every peer's mailbox from the kernel. */
+int dpia_ipc_alloc(int device, size_t bytes, uint64_t* dptr, char handle[64]);
+int dpia_ipc_open(int device, const char handle[64], uint64_t* dptr);
+int dpia_ipc_close(int device, uint64_t dptr);
+
 int dpia_nccl_available(void);
 /* 128-byte ncclUniqueId, produced on rank 0 and broadcast by the caller. */
 int dpia_nccl_unique_id(char out[128]);

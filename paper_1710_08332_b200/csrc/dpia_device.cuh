@@ -11,6 +11,10 @@
 // * dpia::fma2          -- two independent scalar FMAs issued as one packed
 //                          Blackwell fma.rn.f32x2 (FFMA2); per lane identical
 //                          to the contracted scalar c + a*b
+// * dpia::peer_sum      -- fused cross-GPU combine: the last block of every
+//                          rank stores its result into every peer's NVLink-
+//                          mapped mailbox and sums all ranks' results in rank
+//                          order (replaces ncclAllReduce of the partials)
 // * dpia::grid_arrive   -- last-block-done detection used to fuse a single
 //                          work-group tail phase into the preceding grid phase
 //
@@ -176,6 +180,49 @@ __device__ __forceinline__ bool grid_arrive(unsigned int* counter, int tid, bool
   __syncthreads();
   if (*flag) __threadfence();
   return *flag;
+}
+
+// Cross-GPU sum of n scalars, run by one thread of the last block of every
+// rank after the rank-local result is in out[0..n).  boxes[p] is rank p's
+// mailbox (mapped into this device through CUDA IPC / NVLink P2P): two
+// parities x world x n slots of 16 bytes {value (8 B), epoch (4 B), pad}.
+// Launch e uses parity e & 1, so a rank that has already moved on to launch
+// e+1 never overwrites a slot another rank is still reading for launch e.
+// The value is published before its epoch with a system-scope release store
+// and read after a system-scope acquire load, so every rank sees every value
+// and sums them in the same (rank) order: the result is identical on all
+// ranks.  A rank that waits longer than ~4e9 cycles for a peer gives up and
+// raises the mailbox's error word (the host checks it) instead of hanging.
+template <class T>
+__device__ void peer_sum(T* out, int n, const unsigned long long* boxes, int rank, int world,
+                         unsigned int epoch) {
+  const int par = static_cast<int>(epoch & 1u);
+  for (int p = 0; p < world; ++p) {
+    char* base = reinterpret_cast<char*>(boxes[p]);
+    for (int k = 0; k < n; ++k) {
+      char* slot = base + (static_cast<size_t>((par * world + rank) * n + k) << 4);
+      *reinterpret_cast<volatile T*>(slot) = out[k];
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot + 8), "r"(epoch) : "memory");
+    }
+  }
+  char* mine = reinterpret_cast<char*>(boxes[rank]);
+  unsigned int* err = reinterpret_cast<unsigned int*>(mine + (static_cast<size_t>(2 * world * n) << 4));
+  for (int k = 0; k < n; ++k) {
+    T acc = T(0);
+    for (int q = 0; q < world; ++q) {
+      char* slot = mine + (static_cast<size_t>((par * world + q) * n + k) << 4);
+      unsigned int e;
+      const long long t0 = clock64();
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(e) : "l"(slot + 8) : "memory");
+        if (e == epoch) break;
+        if (clock64() - t0 > 4000000000LL) { *err = 1u; break; }
+      }
+      const T v = *reinterpret_cast<volatile T*>(slot);
+      acc = q == 0 ? v : acc + v;
+    }
+    out[k] = acc;
+  }
 }
 
 __device__ __forceinline__ void grid_reset(unsigned int* counter, int tid) {

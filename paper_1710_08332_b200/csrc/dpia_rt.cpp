@@ -27,7 +27,8 @@
   X(cuMemcpyHtoD) X(cuMemcpyDtoH) X(cuMemcpyHtoDAsync) X(cuMemcpyDtoHAsync)                  \
   X(cuMemcpyDtoDAsync) X(cuMemsetD8Async) X(cuMemsetD32Async) X(cuLaunchKernel)              \
   X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
-  X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)
+  X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)          \
+  X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle)
 
 namespace drv {
 #define DPIA_DECL(f) decltype(&::f) f = nullptr;
@@ -469,6 +470,37 @@ int dpia_fill_hash_f32(int device, uint64_t dptr, uint64_t count, uint64_t offse
   void* args[] = {&dptr, &n, &off, &seed, &lo, &hi};
   CU(drv::cuLaunchKernel(g_fill_fn[device], 148 * 8, 1, 1, 256, 1, 1, 0,
                     static_cast<CUstream>(stream), args, nullptr));
+  return 0;
+}
+
+// ------------------------------------------------- peer (NVLink) mailboxes
+int dpia_ipc_alloc(int device, size_t bytes, uint64_t* dptr, char handle[64]) {
+  if (int e = bind(device)) return e;
+  CUdeviceptr p = 0;
+  CU(drv::cuMemAlloc(&p, bytes ? bytes : 16));
+  CU(drv::cuMemsetD8Async(p, 0, bytes ? bytes : 16, nullptr));
+  CU(drv::cuCtxSynchronize());
+  CUipcMemHandle h;
+  CU(drv::cuIpcGetMemHandle(&h, p));
+  static_assert(sizeof(CUipcMemHandle) == 64, "CUipcMemHandle is 64 bytes");
+  memcpy(handle, &h, 64);
+  *dptr = static_cast<uint64_t>(p);
+  return 0;
+}
+
+int dpia_ipc_open(int device, const char handle[64], uint64_t* dptr) {
+  if (int e = bind(device)) return e;
+  CUipcMemHandle h;
+  memcpy(&h, handle, 64);
+  CUdeviceptr p = 0;
+  CU(drv::cuIpcOpenMemHandle(&p, h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS));
+  *dptr = static_cast<uint64_t>(p);
+  return 0;
+}
+
+int dpia_ipc_close(int device, uint64_t dptr) {
+  if (int e = bind(device)) return e;
+  CU(drv::cuIpcCloseMemHandle(static_cast<CUdeviceptr>(dptr)));
   return 0;
 }
 

@@ -1400,8 +1400,10 @@ class KernelEmitter:
 
 class ProgramEmitter:
     def __init__(self, outputs, inputs, float_mode=True, name="KERNEL", sigma=None, launch=None,
-                 init_new=False):
+                 init_new=False, peer=False):
         self.outputs, self.inputs = list(outputs), list(inputs)
+        self.peer = peer
+        self.peer_kernel = None
         self.scalar = "float" if float_mode else "long long"
         self.types = TypeTable(self.scalar)
         self.name = "".join(ch if ch.isalnum() or ch == "_" else "_" for ch in name) or "KERNEL"
@@ -1523,6 +1525,15 @@ class ProgramEmitter:
             self.scratch.append(buf)
             self.scratch_names.add(buf.cname)
 
+        if self.peer:
+            # fused cross-GPU combine: appended to the last kernel, which must
+            # end in a single-work-group tail (all of the rank's blocks done)
+            if not kernels or not kernels[-1][1]:
+                raise CudaError("peer combine needs a program that ends in a reduction tail "
+                                "(e.g. a top-level reduceLocal over work-group results)")
+            if self.sigma is None or len(self.outputs) != 1:
+                raise CudaError("peer combine needs specialised sizes and a single output")
+            self.peer_kernel = len(kernels) - 1
         bodies, infos = [], []
         for ki, (grid, tail) in enumerate(kernels):
             text, info = self.emit_kernel(ki, grid, tail, kernel_top.get(ki, []))
@@ -1563,6 +1574,9 @@ class ProgramEmitter:
             args += [("size", s) for s in sizes]
         if grid is not None and tail:
             args.append(("counter", "dpia_counter"))
+        if self.peer and ki == self.peer_kernel:
+            args += [("peer_boxes", "dpia_peer_boxes"), ("peer_rank", "dpia_rank"),
+                     ("peer_world", "dpia_world"), ("peer_epoch", "dpia_epoch")]
         params, views = [], []
         for kind, n in args:
             if kind == "size":
@@ -1570,6 +1584,11 @@ class ProgramEmitter:
                 continue
             if kind == "counter":
                 params.append("unsigned int *dpia_counter")
+                continue
+            if kind.startswith("peer_"):
+                params.append({"peer_boxes": "const unsigned long long * __restrict__ dpia_peer_boxes",
+                               "peer_rank": "int dpia_rank", "peer_world": "int dpia_world",
+                               "peer_epoch": "unsigned int dpia_epoch"}[kind])
                 continue
             ct = self.types.c_elem(split_array(self._arg_type(n))[1])
             q = "const " if kind == "in" else ""
@@ -1674,6 +1693,15 @@ class ProgramEmitter:
                     ke.comm(it)
                     ke.single_thread = False
                     ke.close()
+            if self.peer and ke.kname == f"{self.name}_k{self.peer_kernel}":
+                on, od = self.outputs[0]
+                from ..layout import shape_of
+                nsc = shape_of(od, self.sigma, 4 if self.scalar == "float" else 8)[0] \
+                    // (4 if self.scalar == "float" else 8)
+                ke.line("__syncthreads();")
+                ke.line(f"if (dpia_tid == 0) dpia::peer_sum<{self.scalar}>("
+                        f"reinterpret_cast<{self.scalar}*>({on}), {nsc}, dpia_peer_boxes, dpia_rank, "
+                        "dpia_world, dpia_epoch);")
             if grid is not None:
                 ke.line("dpia::grid_reset(dpia_counter, dpia_tid);")
                 ke.close()
@@ -1727,7 +1755,7 @@ class ProgramEmitter:
 def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple[str, DataType]],
               float_mode: bool = True, name: str = "KERNEL", init_new: bool = False,
               simplify: bool = True, sigma: Optional[Dict[str, int]] = None,
-              launch=None) -> Tuple[str, CudaSignature]:
+              launch=None, peer: bool = False) -> Tuple[str, CudaSignature]:
     """Render an imperative DPIA command as CUDA C for sm_100a.
 
     Drop-in for the reference's `emit_kernel(p, outputs, inputs, float_mode,
@@ -1737,4 +1765,4 @@ def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple
     source (run_kernel always does), which enables single-iteration loops,
     thread slicing and compile-time index arithmetic."""
     del simplify  # subscripts are always range-simplified
-    return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new).emit(p)
+    return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new, peer).emit(p)

@@ -36,6 +36,7 @@ class Executable:
     module: RT.Module = None
     buffers: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
     counters: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
+    peer: object = None             # peer.PeerGroup of the fused cross-GPU combine
     _args: List = field(default_factory=list)
 
     @property
@@ -74,6 +75,14 @@ class Executable:
                     vals.append(RT.C.c_uint64(self.buffers[n].ptr))
                 elif kind == "size":
                     vals.append(RT.C.c_longlong(int(self.sigma[n])))
+                elif kind == "peer_boxes":
+                    vals.append(RT.C.c_uint64(self.peer.boxes.ptr))
+                elif kind == "peer_rank":
+                    vals.append(RT.C.c_int(self.peer.rank))
+                elif kind == "peer_world":
+                    vals.append(RT.C.c_int(self.peer.world))
+                elif kind == "peer_epoch":
+                    vals.append(self.peer.epoch)       # shared; bumped by every launch
                 else:
                     vals.append(RT.C.c_uint64(self.counters[k.name].ptr))
             self._args.append(vals)
@@ -97,6 +106,8 @@ class Executable:
 
     # ------------------------------------------------------------ launch
     def launch(self, stream: Optional[RT.Stream] = None):
+        if self.peer is not None:
+            self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
         for k, vals in zip(self.sig.kernels, self._args):
             grid = g if k.grid == "launch" else (1, 1)
@@ -140,17 +151,19 @@ def _split_params(params):
 
 def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None,
           float_mode: bool = False, device: int = 0, name: str = "KERNEL",
-          specialize: bool = True) -> Executable:
+          specialize: bool = True, peer=None) -> Executable:
     """Emit + compile + allocate (no data movement).  specialize=False keeps
     sizes as kernel arguments and the geometry runtime-only (the source the
-    CLI's `compile` writes without --launch)."""
+    CLI's `compile` writes without --launch).  peer: a peer.PeerGroup -- the
+    program's result is summed over the group's ranks inside the kernel."""
     sigma = dict(sigma or {})
     outs, ins = _split_params(params)
     geom = normalize_launch(launch)
     check_work_item_races(p)   # the reference simulator's WorkItemRace (SRC/opencl.py:465-470)
     src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name,
-                         sigma=sigma if specialize else None, launch=geom if specialize else None)
-    exe = Executable(src, sig, device, float_mode, sigma, geometry=geom)
+                         sigma=sigma if specialize else None, launch=geom if specialize else None,
+                         peer=peer is not None)
+    exe = Executable(src, sig, device, float_mode, sigma, geometry=geom, peer=peer)
     return exe.compile().allocate()
 
 

@@ -57,6 +57,9 @@ _PROTOS = {
     "dpia_event_elapsed": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
     "dpia_l2_flush": (_i, [_i, _vp]),
     "dpia_fill_hash_f32": (_i, [_i, _u64, _u64, _u64, C.c_uint32, C.c_float, C.c_float, _vp]),
+    "dpia_ipc_alloc": (_i, [_i, _sz, C.POINTER(C.c_uint64), C.c_char_p]),
+    "dpia_ipc_open": (_i, [_i, C.c_char_p, C.POINTER(C.c_uint64)]),
+    "dpia_ipc_close": (_i, [_i, _u64]),
     "dpia_nccl_available": (_i, []),
     "dpia_nccl_unique_id": (_i, [C.c_char_p]),
     "dpia_nccl_init": (_i, [_i, _i, _i, C.c_char_p]),

@@ -56,16 +56,28 @@ class ShardedReduction:
     """One rank's part of the sharded dot/asum over hash-generated inputs."""
 
     def __init__(self, kind: str, total_elems: int, world: int = 1, rank: int = 0, device: int = 0,
-                 L: int = 1024, K: int = 32, blocks: Optional[int] = None):
+                 L: int = 1024, K: int = 32, blocks: Optional[int] = None, combine: str = "nccl",
+                 allgather=None):
+        """combine: "peer" -- the kernel sums the ranks' partials itself over
+        NVLink (peer.PeerGroup, one kernel per step); "nccl" -- a 4-byte
+        ncclAllReduce after the kernel (launch(..., allreduce=True))."""
         if kind not in ("asum", "dot"):
             raise ValueError(kind)
+        if combine not in ("peer", "nccl"):
+            raise ValueError(combine)
+        self.combine = combine
         self.kind, self.device = kind, device
         chunk = 4 * K * L
         self.shard = shard_plan(total_elems, chunk, world, rank)
         text = asum_program(L, K) if kind == "asum" else dot_program(L, K)
         prog = compile_program(text, name=f"{kind}_shard")
         n = self.shard.chunks
-        self.exe = executable(prog, (blocks or n, L), {"n": n}, float_mode=True, device=device)
+        self.peer = None
+        if combine == "peer":
+            from .peer import PeerGroup
+            self.peer = PeerGroup(device, rank, world, 1, allgather)
+        self.exe = executable(prog, (blocks or n, L), {"n": n}, float_mode=True, device=device,
+                              peer=self.peer)
         self.bytes = (4 if kind == "asum" else 8) * self.shard.elems
         self.total_bytes = self.bytes * world
 
@@ -79,7 +91,7 @@ class ShardedReduction:
 
     def launch(self, stream, allreduce: bool):
         self.exe.launch(stream)
-        if allreduce:
+        if allreduce and self.combine == "nccl":
             RT.lib().dpia_nccl_allreduce(self.exe.buffers["out"].ptr, 1, 0, stream.handle)
 
     def result(self) -> float:

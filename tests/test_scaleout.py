@@ -115,3 +115,98 @@ def test_nccl_single_rank_allreduce_through_the_c_abi():
     buf.download(out)
     assert out[0] == 2.5
     RT.lib().dpia_nccl_destroy()
+
+
+# ------------------------------------------------ fused peer (NVLink) combine
+
+def test_peer_mailbox_layout_and_emitted_kernel():
+    """CPU: the emitter appends dpia::peer_sum to the reduction tail with the
+    peer parameters, and rejects programs without such a tail."""
+    from paper_1710_08332_b200 import CudaError, compile_program
+    from paper_1710_08332_b200.bench_programs import dot_program, scal_program
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.peer import SLOT_BYTES, mailbox_bytes
+    assert mailbox_bytes(8, 1) == (2 * 8 + 1) * SLOT_BYTES
+    prog = compile_program(dot_program(32, 2))
+    outs = [(n, t) for n, t, k in prog.params if k == "out"]
+    ins = [(n, t) for n, t, k in prog.params if k == "in"]
+    src, sig = emit_cuda(prog.imperative, outs, ins, True, "d", sigma={"n": 4}, launch=(4, 32), peer=True)
+    assert "dpia::peer_sum<float>(reinterpret_cast<float*>(out), 1, dpia_peer_boxes" in src
+    kinds = [k for k, _ in sig.kernels[-1].args]
+    assert kinds[-4:] == ["peer_boxes", "peer_rank", "peer_world", "peer_epoch"]
+    sprog = compile_program(scal_program())
+    outs = [(n, t) for n, t, k in sprog.params if k == "out"]
+    ins = [(n, t) for n, t, k in sprog.params if k == "in"]
+    with pytest.raises(CudaError):
+        emit_cuda(sprog.imperative, outs, ins, True, "s", sigma={"n": 64}, launch=(2, 32), peer=True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["asum", "dot"])
+def test_peer_combine_single_rank(kind):
+    """world = 1: the fused combine publishes to and reads from its own
+    mailbox; repeated launches (epochs, both parities) keep the result."""
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    total = 1 << 24
+    run = ShardedReduction(kind, total, combine="peer")
+    st = RT.Stream(0)
+    run.fill_inputs(st)
+    for _ in range(5):
+        run.launch(st, allreduce=True)
+    st.sync()
+    run.peer.check()
+    want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
+            else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
+    assert blas_np.within(run.result(), want[0], want[1])
+    run.peer.close()
+
+
+def _peer_worker(rank, world, port, total, kind, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.peer import torch_allgather
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    try:
+        run = ShardedReduction(kind, total, world, rank, device=0, combine="peer",
+                               allgather=torch_allgather)
+        st = RT.Stream(0)
+        run.fill_inputs(st)
+        st.sync()
+        dist.barrier()
+        for _ in range(steps):
+            run.launch(st, allreduce=True)
+        st.sync()
+        run.peer.check()
+        q.put((rank, run.result()))
+        dist.barrier()
+        run.peer.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["asum", "dot"])
+def test_peer_combine_two_ranks_sharing_one_gpu(kind):
+    """Two processes (ranks) on the one GPU of this run, each with its own
+    context: the IPC-mapped mailboxes, the release/acquire epoch protocol and
+    the double-buffered parities are the same as across NVLink.  Both ranks
+    must end with the identical total, equal to the oracle's."""
+    total, world, steps = 1 << 24, 2, 6
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, total, kind, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+    assert all(isinstance(v, float) for v in res.values()), res
+    assert res[0] == res[1]
+    want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
+            else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
+    assert blas_np.within(res[0], want[0], want[1]), (res, want)
