@@ -144,6 +144,90 @@ def one(variant):
     st.sync()
 
 
+CP_ASYNC = r"""
+__device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
+}
+#define B_G(k, row) (64 * ((row) % 2) + 4096 * ((row) / 2) + 4 * (int)threadIdx.x + 65536 * (k) + 128 * (int)blockIdx.x)
+#define B_S(k, row) ((((4 * (int)threadIdx.x) ^ (8 * ((row) / 8))) + 2048 * ((k) % 2) + 64 * ((row) % 2) + 128 * ((row) / 2)))
+"""
+
+
+def cpasync_source(src):
+    """Hand edit of the default BK=16 kernel: the B tile is staged with
+    cp.async (no registers, no STS) -- issue for k+1 after the barrier of
+    iteration k, wait_all before the barrier of k+1.  Experiment only."""
+    import re
+    k = src.index('extern "C"')
+    src = src[:k] + CP_ASYNC + src[k:]
+    a = src.index("dpia::vec<float, 4> pf1_0;")
+    b = src.index("float* tmp", a)
+    src = src[:a] + ("cp_async16(tmp16_9 + B_S(0, (int)threadIdx.y), B + B_G(0, (int)threadIdx.y));\n"
+                     "cp_async16(tmp16_9 + B_S(0, (int)threadIdx.y + 16), B + B_G(0, (int)threadIdx.y + 16));\n"
+                     "asm volatile(\"cp.async.commit_group;\" ::: \"memory\");\n") + src[b:]
+    m = re.search(r"for \(int (i_\d+_\d+) = 0; \1 < 256; \1 \+= 1\) \{", src)
+    kv = m.group(1)
+    body = m.end()
+    c0 = src.index("dpia::vstore<float, 4>(tmp16_9", body)
+    c0 = src.rindex("{", 0, src.rindex("{", 0, c0))          # the copy's outer block
+    r0 = src.index("if (" + kv + " + 1 < 256) {", body)
+    # end of the B refill block: the matching brace
+    depth, j = 0, r0
+    while True:
+        if src[j] == "{":
+            depth += 1
+        elif src[j] == "}":
+            depth -= 1
+            if depth == 0:
+                break
+        j += 1
+    src = src[:c0] + "asm volatile(\"cp.async.wait_all;\" ::: \"memory\");\n" + src[j + 1:]
+    sync = src.index("__syncthreads();", src.index(kv, m.start() + 10))
+    issue = (f"\nif ({kv} + 1 < 256) {{ cp_async16(tmp16_9 + B_S({kv} + 1, (int)threadIdx.y), "
+             f"B + B_G({kv} + 1, (int)threadIdx.y)); cp_async16(tmp16_9 + B_S({kv} + 1, (int)threadIdx.y + 16), "
+             f"B + B_G({kv} + 1, (int)threadIdx.y + 16)); asm volatile(\"cp.async.commit_group;\" ::: \"memory\"); }}\n")
+    e = sync + len("__syncthreads();")
+    return src[:e] + issue + src[e:]
+
+
+def cpasync():
+    from paper_1710_08332_b200.cuda.emit import emit_cuda
+    from paper_1710_08332_b200.launcher import Executable
+    RT.init(0)
+    st = RT.Stream(0)
+    rng = np.random.default_rng(0)
+    A = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    B = rng.uniform(-1, 1, (4096, 4096)).astype(np.float32)
+    cfg = mm_config()
+    prog = compile_program(cfg.text, name="mm")
+    outs = [(n, t) for n, t, k in prog.params if k == "out"]
+    ins = [(n, t) for n, t, k in prog.params if k == "in"]
+    src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
+    ref = None
+    cpa = cpasync_source(src)
+    for label, s in (("emitted", src), ("cp.async B", cpa),
+                     ("cp.async B + lb(256,2)", cpa.replace("__launch_bounds__(256)", "__launch_bounds__(256, 2)"))):
+        exe = Executable(s, sig, 0, True, {}, geometry=cfg.launch).compile().allocate()
+        exe.upload("A", A, st)
+        exe.upload("B", B, st)
+        ts = []
+        for i in range(13):
+            RT.lib().dpia_l2_flush(0, st.handle)
+            e0, e1 = RT.Event(0), RT.Event(0)
+            e0.record(st)
+            exe.launch(st)
+            e1.record(st)
+            st.sync()
+            if i >= 3:
+                ts.append(e0.elapsed_ms(e1))
+        out = exe.download("out", st)
+        ref = out if ref is None else ref
+        ms = statistics.mean(ts)
+        print(f"{label}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  same={np.array_equal(out, ref)}",
+              flush=True)
+
+
 def rowa():
     """Row-major A staging + k-quad micro-kernel (mm_rowa_program), as
     emitted and with __launch_bounds__(256, 2)."""
@@ -270,6 +354,9 @@ def sts_bound():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "cpasync":
+        cpasync()
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "rowa":
         rowa()
         sys.exit(0)
