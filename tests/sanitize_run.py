@@ -95,6 +95,22 @@ def main():
                            launch=c.launch, float_mode=False, flat=True)
     assert [int(v) for v in got] == (3 * xs).tolist()
     print("ok scal", flush=True)
+    # fused peer combine, one rank (mailbox protocol under the sanitizer)
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    for kind in ("asum", "dot"):
+        run = ShardedReduction(kind, 1 << 18, L=128, K=4, combine="peer")
+        st = RT.Stream(0)
+        run.fill_inputs(st)
+        vals = []
+        for _ in range(3):
+            run.launch(st, allreduce=True)
+            st.sync()
+            vals.append(run.result())
+        run.peer.check()
+        assert vals[0] == vals[1] == vals[2], vals
+        run.peer.close()
+        print(f"ok peer {kind}", flush=True)
     # the reference's golden programs
     from conftest import load_golden
     for case in load_golden("programs.json"):
