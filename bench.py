@@ -524,9 +524,11 @@ def main():
             "config": dict(_cfg_desc(cfg, world, args.combine),
                            **({"combine": args.combine} if world > 1 else {})),
             "roofline": head["roofline"], "e2e": head.get("e2e"), "clocks": head["clocks"],
-            "gpu_launches": args.steps * (len(exe.sig.kernels) + 1),
-            "gpu_launches_breakdown": {"emitted program kernels": args.steps * len(exe.sig.kernels),
-                                       "dpia_l2_scrub (libdpia_rt, between steps)": args.steps},
+            "gpu_launches": args.steps * len(exe.sig.kernels),
+            "gpu_launches_breakdown": {"emitted program kernels (inside the timed events)":
+                                       args.steps * len(exe.sig.kernels),
+                                       "dpia_l2_scrub (libdpia_rt, between steps, outside the events)":
+                                       args.steps},
             "kernels": exe.kernel_names(),
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
                              if cpu else None),

@@ -284,7 +284,7 @@ def transforms():
     ins = [(n, t) for n, t, k in prog.params if k == "in"]
     src, sig = emit_cuda(prog.imperative, outs, ins, True, "mm", sigma=cfg.sigma, launch=cfg.launch)
     k_loop = re.search(r"\n(\s*)for \(int (i_\d+_\d+) = 0; \2 < 256; \2 \+= 1\) \{", src)
-    variants = {"emitted": src}
+    variants = {"emitted": src, "lb(256,1)": src.replace("__launch_bounds__(256)", "__launch_bounds__(256, 1)")}
     if k_loop:
         variants["unroll2"] = src[:k_loop.start()] + f"\n{k_loop.group(1)}#pragma unroll 2" + src[k_loop.start():]
         variants["unroll1"] = src[:k_loop.start()] + f"\n{k_loop.group(1)}#pragma unroll 1" + src[k_loop.start():]
