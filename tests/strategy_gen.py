@@ -126,3 +126,42 @@ def generate(seed: int):
     desc = f"{shape}{'+vec4' if vec else ''}{'+zip' if two else ''}{'+top' if top_combine else ''} L={L} K={K}"
     del out_t
     return text, inputs, {}, launch, desc
+
+
+def generate2d(seed: int):
+    """2-D hierarchy programs: a tiled transpose of f(X) (or of f(X, Y) for
+    two zipped inputs) through a shared-memory tile -- mapWorkgroup1 /
+    mapWorkgroup over TB x TB tiles, mapLocal1 / mapLocal inside, coalesced
+    tile loads, column reads of the staged tile (XOR-swizzled once the tile
+    rows are 32 scalars).  (text, inputs, sigma, launch, description)."""
+    rng = random.Random(seed ^ 0x2D2D)
+    TB = rng.choice([16, 32])
+    gx, gy = rng.choice([1, 2, 3]), rng.choice([1, 2])
+    R, C = TB * gy, TB * gx
+    N = R * C
+    two = rng.random() < 0.4
+    if two:
+        src = "(zip xs ys)"
+        elem_t = "(pair num num)"
+        x_expr = lambda v: f"(* (fst {v}) (snd {v}))"  # noqa: E731
+    else:
+        src, elem_t = "xs", "num"
+        x_expr = lambda v: v  # noqa: E731
+    e = _expr(rng, "v")
+    text = (f"(param xs (exp (array {N} num)))\n" + (f"(param ys (exp (array {N} num)))\n" if two else "") +
+            f"(transpose (mapWorkgroup1 (lam (rt (exp (array {TB} (array {C} {elem_t}))))"
+            f" (join (mapWorkgroup (lam (t (exp (array {TB} (array {TB} {elem_t}))))"
+            f" (let (toLocal (mapLocal1 (lam (row (exp (array {TB} {elem_t})))"
+            f" (mapLocal (lam (q (exp {elem_t})) (let {x_expr('q')} (lam (v (exp num)) {e}))) row)))"
+            f" (transpose t))"
+            f" (lam (s (exp (array {TB} (array {TB} num))))"
+            f" (mapLocal1 (lam (col (exp (array {TB} num))) (mapLocal (lam (u (exp num)) u) col))"
+            f" (transpose s)))))"
+            f" (split {TB} (transpose rt)))))"
+            f" (split {TB} (split {C} {src}))))")
+    r2 = random.Random(seed ^ 0xD00D)
+    inputs = {"xs": [r2.randint(-5, 5) for _ in range(N)]}
+    if two:
+        inputs["ys"] = [r2.randint(-5, 5) for _ in range(N)]
+    launch = ((rng.choice([1, gx]), rng.choice([1, gy])), (TB, rng.choice([TB, TB // 2, 4])))
+    return text, inputs, {}, launch, f"tile2d TB={TB} {R}x{C}{'+zip' if two else ''}"

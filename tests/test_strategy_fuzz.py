@@ -7,7 +7,7 @@ import pytest
 from oracle.dpia_eval import eval_phrase, flatten_value
 from oracle.phase_sim import simulate
 from paper_1710_08332_b200 import compile_program
-from strategy_gen import generate
+from strategy_gen import generate, generate2d
 
 
 def _case(seed):
@@ -43,4 +43,30 @@ def test_strategy_fuzz_gpu_fp32(seed):
     from paper_1710_08332_b200 import run_program_cuda
     prog, inputs, sigma, launch, want = _case(seed)
     got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=True, flat=True)
+    assert [float(v) for v in got] == [float(v) for v in want]
+
+
+def _case2d(seed):
+    text, inputs, sigma, launch, desc = generate2d(seed)
+    prog = compile_program(text)
+    want = flatten_value(eval_phrase(prog.source.body, inputs, sigma))
+    return prog, inputs, sigma, launch, want
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_strategy_fuzz2d_phase_simulator(seed):
+    prog, inputs, sigma, launch, want = _case2d(seed)
+    got = simulate(prog.imperative, prog.params, inputs, launch, sigma)["out"]
+    assert flatten_value(got) == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("float_mode", [False, True])
+@pytest.mark.parametrize("seed", range(150))
+def test_strategy_fuzz2d_gpu(seed, float_mode):
+    """2-D hierarchy (tiled transposes through swizzled shared tiles), exact
+    in int and fp32 (small-integer values)."""
+    from paper_1710_08332_b200 import run_program_cuda
+    prog, inputs, sigma, launch, want = _case2d(seed)
+    got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=float_mode, flat=True)
     assert [float(v) for v in got] == [float(v) for v in want]
