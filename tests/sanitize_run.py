@@ -134,6 +134,10 @@ def main():
             check(compile_program(text), inputs, sigma, launch, f"fuzz {seed} ({desc})")
         except CudaError as e:
             print(f"skip fuzz {seed}: {e}", flush=True)
+    from strategy_gen import generate2d
+    for seed in range(16):
+        text, inputs, sigma, launch, desc = generate2d(seed)
+        check(compile_program(text), inputs, sigma, launch, f"fuzz2d {seed} ({desc})")
     print("SANITIZE WORKLOAD DONE", flush=True)
 
 
