@@ -72,6 +72,8 @@ int dpia_event_create(int device, void** event);
 int dpia_event_destroy(void* event);
 int dpia_event_record(void* event, void* stream);
 int dpia_event_elapsed(void* start, void* stop, float* ms);
+/* Make `stream` wait for `event` (cross-stream ordering of copy / compute). */
+int dpia_stream_wait_event(void* stream, void* event);
 /* Evict L2: overwrite a device buffer of 2x the L2 capacity on `stream`. */
 int dpia_l2_flush(int device, void* stream);
 /* Fill dptr[0..count) (float) with x_i = lo + (hi-lo) * h(seed, offset+i), h a

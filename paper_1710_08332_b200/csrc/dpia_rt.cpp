@@ -28,7 +28,8 @@
   X(cuMemcpyDtoDAsync) X(cuMemsetD8Async) X(cuMemsetD32Async) X(cuLaunchKernel)              \
   X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
   X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)          \
-  X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle)
+  X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuStreamWaitEvent)   \
+  X(cuCtxGetCurrent)
 
 namespace drv {
 #define DPIA_DECL(f) decltype(&::f) f = nullptr;
@@ -314,6 +315,14 @@ int dpia_free(int device, uint64_t dptr) {
 }
 
 int dpia_host_alloc(size_t bytes, void** ptr) {
+  // page-locked memory belongs to a context: use the current one, or bind
+  // device 0 when the caller has not initialised any device yet
+  if (int e = load_driver()) return e;
+  CU(drv::cuInit(0));
+  CUcontext cur = nullptr;
+  if (drv::cuCtxGetCurrent(&cur) != CUDA_SUCCESS || !cur) {
+    if (int e = bind(0)) return e;
+  }
   CU(drv::cuMemAllocHost(ptr, bytes ? bytes : 16));
   return 0;
 }
@@ -396,6 +405,11 @@ int dpia_event_destroy(void* event) {
 
 int dpia_event_record(void* event, void* stream) {
   CU(drv::cuEventRecord(static_cast<CUevent>(event), static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_stream_wait_event(void* stream, void* event) {
+  CU(drv::cuStreamWaitEvent(static_cast<CUstream>(stream), static_cast<CUevent>(event), 0));
   return 0;
 }
 

@@ -114,6 +114,18 @@ class Executable:
             fn = self.module.function(k.name)
             RT.launch(fn, self.device, grid, l, k.smem, vals, stream)
 
+    def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int]):
+        """Launch with some parameters re-pointed (device addresses), e.g. at
+        windows of larger buffers -- the row chunks of pipeline.RowPipeline."""
+        if self.peer is not None:
+            self.peer.next_epoch()
+        (g, l) = self.sig.launch or self.geometry
+        for k, vals in zip(self.sig.kernels, self._args):
+            vals = [RT.C.c_uint64(ptrs[n]) if kind in ("out", "in") and n in ptrs else v
+                    for (kind, n), v in zip(k.args, vals)]
+            grid = g if k.grid == "launch" else (1, 1)
+            RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream)
+
     def run(self, inputs: Dict[str, object], stream: Optional[RT.Stream] = None,
             out: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:
         """One end-to-end execution from host buffers: copy every input to

@@ -55,6 +55,7 @@ _PROTOS = {
     "dpia_event_destroy": (_i, [_vp]),
     "dpia_event_record": (_i, [_vp, _vp]),
     "dpia_event_elapsed": (_i, [_vp, _vp, C.POINTER(C.c_float)]),
+    "dpia_stream_wait_event": (_i, [_vp, _vp]),
     "dpia_l2_flush": (_i, [_i, _vp]),
     "dpia_fill_hash_f32": (_i, [_i, _u64, _u64, _u64, C.c_uint32, C.c_float, C.c_float, _vp]),
     "dpia_ipc_alloc": (_i, [_i, _sz, C.POINTER(C.c_uint64), C.c_char_p]),
@@ -248,6 +249,17 @@ class DeviceBuffer:
         lib().dpia_memset(self.device, self.ptr, 0, self.nbytes, _sh(stream))
 
 
+class DeviceView:
+    """A window [offset, offset + nbytes) of a DeviceBuffer (not owning)."""
+
+    def __init__(self, base: "DeviceBuffer", offset: int, nbytes: int):
+        assert 0 <= offset and offset + nbytes <= base.nbytes
+        self.device, self.ptr, self.nbytes = base.device, base.ptr + offset, nbytes
+
+    def free(self):
+        pass
+
+
 class PinnedBuffer:
     def __init__(self, nbytes: int):
         p = ctypes.c_void_p()
@@ -284,6 +296,10 @@ class Event:
 
     def record(self, stream: Optional[Stream]):
         lib().dpia_event_record(self.handle, stream.handle if stream else None)
+
+    def wait_on(self, stream: "Stream"):
+        """Make `stream` wait until this event has completed."""
+        lib().dpia_stream_wait_event(stream.handle, self.handle)
 
     def elapsed_ms(self, later: "Event") -> float:
         ms = ctypes.c_float()
