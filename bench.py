@@ -380,12 +380,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # plumbing check on a one-GPU box: every rank on GPU 0, gloo for the host
+    # side (the fused peer combine still runs GPU to GPU through CUDA IPC);
+    # the timings of ranks sharing a GPU are not scaling numbers
+    share = os.environ.get("DPIA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+        args.combine = "peer"
     dist = None
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if share else "nccl")
         if args.impl == "ours" and args.combine == "peer":
             # collective capability probe: every rank maps every peer's
             # mailbox (CUDA IPC + NVLink P2P); if any rank cannot, all ranks
@@ -398,9 +405,7 @@ def main():
             except Exception as e:  # noqa: BLE001
                 print(f"rank {rank}: peer combine unavailable ({e}); using NCCL", file=sys.stderr)
                 ok = 0
-            t = torch.tensor([ok], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MIN)
-            if not int(t.item()):
+            if not int(_allreduce(dist, ok, dist.ReduceOp.MIN, local, share)):
                 args.combine = "nccl"
         if args.impl == "ours" and args.combine == "nccl":
             import ctypes
@@ -461,9 +466,7 @@ def main():
         batches = max(1, int(0.6 / max(time.perf_counter() - t_b, 1e-4)))
         if dist is not None:
             import torch
-            t = torch.tensor([batches], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            batches = int(t.item())
+            batches = int(_allreduce(dist, batches, dist.ReduceOp.MAX, local, share))
         with Clocks(device) as clk:
             for _ in range(batches):
                 for _ in range(20):
@@ -477,9 +480,7 @@ def main():
         mean_ms = statistics.mean(ms)
         if dist is not None:
             import torch
-            t = torch.tensor([mean_ms], device=f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            mean_ms = float(t.item())
+            mean_ms = float(_allreduce(dist, mean_ms, dist.ReduceOp.MAX, local, share))
             dist.barrier()
         kernel_ms = run_timed(exe, stream, min(steps, 10))  # dominant kernel alone, no collective
         kmean = statistics.mean(kernel_ms)
@@ -559,7 +560,9 @@ def main():
             "data": ("synthetic (device-side counter hash, per-shard global offsets)" if strong
                      else "synthetic (numpy default_rng uniform, resident in HBM)"),
             "config": dict(_cfg_desc(cfg, world, args.combine),
-                           **({"combine": args.combine} if world > 1 else {})),
+                           **({"combine": args.combine} if world > 1 else {}),
+                           **({"shared_gpu": "plumbing check: all ranks on GPU 0 (not a scaling number)"}
+                              if share and world > 1 else {})),
             "roofline": head["roofline"], "e2e": head.get("e2e"), "clocks": head["clocks"],
             "gpu_launches": args.steps * len(exe.sig.kernels),
             "gpu_launches_breakdown": {"emitted program kernels (inside the timed events)":
@@ -571,6 +574,14 @@ def main():
                              if cpu else None),
             "suite": suite}
     print(json.dumps(line), flush=True)
+
+
+def _allreduce(dist, value, op, local, share):
+    """Max/min of a host number over the ranks (CPU tensor under gloo)."""
+    import torch
+    t = torch.tensor([value], device="cpu" if share else f"cuda:{local}")
+    dist.all_reduce(t, op=op)
+    return t.item()
 
 
 def _cfg_desc(cfg, world=1, combine="nccl"):
