@@ -421,7 +421,8 @@ def main():
         if rank != 0:
             return
         r = cpu_reference(args.workload, steps=args.steps)
-        line = {"impl": "reference", "metric": METRIC, "unit": "GB/s", "n_gpus": args.gpus,
+        unit = "GFLOP/s" if args.workload == "mm" else "GB/s"
+        line = {"impl": "reference", "metric": METRIC, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": {"workload": f"{args.workload} (reference c-openmp path on host cores)"}}
@@ -430,7 +431,7 @@ def main():
         else:
             line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
                          "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                         "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
                                  "d2h_bytes_per_step": 0}})
         print(json.dumps(line), flush=True)
         return
@@ -553,7 +554,8 @@ def main():
         return
     cfg, exe = head["cfg"], head["exe"]
     strong = args.workload.startswith("scaleout")
-    line = {"metric": METRIC, "value": round(head["value"], 2), "unit": "GB/s", "n_gpus": world,
+    line = {"metric": METRIC, "value": round(head["value"], 2),
+            "unit": "GFLOP/s" if args.workload == "mm" else "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["mean_ms"], 5),
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f32",

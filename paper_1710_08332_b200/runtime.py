@@ -287,6 +287,15 @@ class Stream:
     def sync(self):
         lib().dpia_stream_sync(self.handle)
 
+    def __del__(self):
+        # pending work still completes; CUDA releases the stream afterwards
+        try:
+            if self.handle:
+                _LIB.so.dpia_stream_destroy(self.handle)
+                self.handle = None
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
 
 class Event:
     def __init__(self, device: int = 0):
@@ -305,6 +314,14 @@ class Event:
         ms = ctypes.c_float()
         lib().dpia_event_elapsed(self.handle, later.handle, ctypes.byref(ms))
         return ms.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                _LIB.so.dpia_event_destroy(self.handle)
+                self.handle = None
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
 
 
 def launch(fn, device: int, grid, block, smem: int, arg_values: List, stream: Optional[Stream]):
