@@ -210,3 +210,17 @@ def test_peer_combine_two_ranks_sharing_one_gpu(kind):
     want = (blas_np.hashed_asum(total, SEEDS["x"]) if kind == "asum"
             else blas_np.hashed_dot(total, SEEDS["x"], SEEDS["y"]))
     assert blas_np.within(res[0], want[0], want[1]), (res, want)
+
+
+def test_peer_and_pipeline_argument_checks():
+    """Host-side validation, before any device work (CPU)."""
+    from paper_1710_08332_b200.peer import PeerGroup
+    from paper_1710_08332_b200.pipeline import RowPipeline, mm_pipeline
+    with pytest.raises(ValueError):
+        PeerGroup(0, 2, 2)                 # rank outside the world
+    with pytest.raises(ValueError):
+        PeerGroup(0, 0, 2)                 # multi-rank group without an allgather
+    with pytest.raises(ValueError):
+        RowPipeline(lambda r: "", lambda r: (1, 1), 10, 3, {}, {}, 0)
+    with pytest.raises(ValueError):
+        mm_pipeline(256, 128, 128, chunks=4)   # 64-row chunks are not whole 128-row tiles
