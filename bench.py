@@ -91,6 +91,37 @@ def read_sol(device, nbytes, stream):
     return _SOL_CACHE[nbytes]
 
 
+_FFMA_CACHE = {}
+
+
+def ffma_peak(device, stream):
+    """Measured FP32 FMA ceiling: tools/ffmapeak.py's register-only packed
+    FFMA2 kernel (measurement infrastructure, not product) at 8 CTAs/SM x 256
+    threads, mean of 10 event-timed launches after warm-up (TFLOP/s)."""
+    if device in _FFMA_CACHE:
+        return _FFMA_CACHE[device]
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    from ffmapeak import ITERS, SRC
+    mod = RT.Module(RT.get_cubin(SRC), device)
+    fn = mod.function("ffma2")
+    out = RT.DeviceBuffer(64, device)
+    blocks = RT.device_attribute(device, RT.ATTR_SM_COUNT) * 8
+    args = [RT.C.c_uint64(out.ptr), RT.C.c_float(0.999), RT.C.c_float(1e-4), RT.C.c_int(ITERS)]
+    ts = []
+    for it in range(13):
+        e0, e1 = RT.Event(device), RT.Event(device)
+        e0.record(stream)
+        RT.launch(fn, device, (blocks, 1), (256, 1), 0, args, stream)
+        e1.record(stream)
+        stream.sync()
+        if it >= 3:
+            ts.append(e0.elapsed_ms(e1))
+    out.free()
+    flops = blocks * 256 * ITERS * 16 * 2 * 2
+    _FFMA_CACHE[device] = round(flops / statistics.mean(ts) / 1e9, 2)
+    return _FFMA_CACHE[device]
+
+
 def ncu_traffic(workload):
     """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
     try:
@@ -510,6 +541,9 @@ def main():
                     "unit": "TFLOP/s", "frac": round(achieved / fp32[0], 4),
                     "traffic": ncu_traffic(workload), "peak_source": fp32[1],
                     "algorithmic_flops_per_launch": cfg.flops, "kernel_ms": round(kmean, 5)}
+            meas = ffma_peak(device, stream)
+            roof["measured_ffma2_peak"] = meas
+            roof["frac_of_measured_ffma2_peak"] = round(achieved / meas, 4)
         else:
             achieved = cfg.bytes / (kmean * 1e-3) / 1e9
             value = world * cfg.bytes / (mean_ms * 1e-3) / 1e9
