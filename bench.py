@@ -588,7 +588,7 @@ def main():
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
     suite = {}
     if not args.no_suite and world == 1:
-        for w in ("dot", "asum", "gemv", "mm", "scal"):
+        for w in ("dot", "asum", "gemv", "mm", "scal", "scaleout_asum", "scaleout_dot"):
             if w == args.workload:
                 continue
             r = measure(w, min(args.steps, 20), 3, with_e2e=True)

@@ -57,6 +57,13 @@ void dpia_free_host(void* ptr); /* plain free() for buffers this library malloc'
 int dpia_memcpy_htod(int device, uint64_t dst, const void* src, size_t bytes, void* stream);
 int dpia_memcpy_dtoh(int device, void* dst, uint64_t src, size_t bytes, void* stream);
 int dpia_memcpy_dtod(int device, uint64_t dst, uint64_t src, size_t bytes, void* stream);
+/* pitched copies (height rows of width bytes; row r at src + r*spitch, dst + r*dpitch),
+ * asynchronous on stream: used by the tile pipeline to move column panels of
+ * row-major host matrices (no reference counterpart) */
+int dpia_memcpy2d_htod(int device, uint64_t dst, size_t dpitch, const void* src, size_t spitch,
+                       size_t width, size_t height, void* stream);
+int dpia_memcpy2d_dtoh(int device, void* dst, size_t dpitch, uint64_t src, size_t spitch,
+                       size_t width, size_t height, void* stream);
 int dpia_memset(int device, uint64_t dst, int value, size_t bytes, void* stream);
 
 /* ---- execution (replaces simulate_kernel, SRC/opencl.py:397-472) ------- */

@@ -29,7 +29,7 @@
   X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
   X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)          \
   X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuStreamWaitEvent)   \
-  X(cuCtxGetCurrent)
+  X(cuCtxGetCurrent) X(cuMemcpy2DAsync)
 
 namespace drv {
 #define DPIA_DECL(f) decltype(&::f) f = nullptr;
@@ -343,6 +343,44 @@ int dpia_memcpy_dtoh(int device, void* dst, uint64_t src, size_t bytes, void* st
   if (int e = bind(device)) return e;
   if (stream) CU(drv::cuMemcpyDtoHAsync(dst, src, bytes, static_cast<CUstream>(stream)));
   else CU(drv::cuMemcpyDtoH(dst, src, bytes));
+  return 0;
+}
+
+// Strided (pitched) copies: `height` rows of `width` bytes, consecutive rows
+// `spitch` bytes apart in the source and `dpitch` bytes apart in the
+// destination (a column panel of a row-major host matrix <-> a contiguous
+// device panel).  Asynchronous on `stream`.
+int dpia_memcpy2d_htod(int device, uint64_t dst, size_t dpitch, const void* src, size_t spitch,
+                       size_t width, size_t height, void* stream) {
+  if (int e = bind(device)) return e;
+  CUDA_MEMCPY2D c;
+  std::memset(&c, 0, sizeof(c));
+  c.srcMemoryType = CU_MEMORYTYPE_HOST;
+  c.srcHost = src;
+  c.srcPitch = spitch;
+  c.dstMemoryType = CU_MEMORYTYPE_DEVICE;
+  c.dstDevice = dst;
+  c.dstPitch = dpitch;
+  c.WidthInBytes = width;
+  c.Height = height;
+  CU(drv::cuMemcpy2DAsync(&c, static_cast<CUstream>(stream)));
+  return 0;
+}
+
+int dpia_memcpy2d_dtoh(int device, void* dst, size_t dpitch, uint64_t src, size_t spitch,
+                       size_t width, size_t height, void* stream) {
+  if (int e = bind(device)) return e;
+  CUDA_MEMCPY2D c;
+  std::memset(&c, 0, sizeof(c));
+  c.srcMemoryType = CU_MEMORYTYPE_DEVICE;
+  c.srcDevice = src;
+  c.srcPitch = spitch;
+  c.dstMemoryType = CU_MEMORYTYPE_HOST;
+  c.dstHost = dst;
+  c.dstPitch = dpitch;
+  c.WidthInBytes = width;
+  c.Height = height;
+  CU(drv::cuMemcpy2DAsync(&c, static_cast<CUstream>(stream)));
   return 0;
 }
 

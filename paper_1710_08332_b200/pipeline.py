@@ -108,3 +108,129 @@ def mm_pipeline(M: int, N: int, K: int, chunks: int = 4, device: int = 0, **stra
     launch = lambda r: mm_config(M=r, N=N, K=K, **strategy).launch  # noqa: E731
     return RowPipeline(text, launch, M, chunks, {"A": 4 * M * K}, {"B": 4 * K * N}, 4 * M * N,
                        device=device, name="mm")
+
+
+def tile_schedule(rows: int, cols: int):
+    """(copy-in order, tile order) of a TilePipeline: the row blocks ("A", i)
+    and column panels ("B", j) interleaved in proportion, and the tiles (i, j)
+    sorted by the copy after which both of their operands are in."""
+    order, ia, ib = [], 0, 0
+    while ia < rows or ib < cols:
+        if ib >= cols or (ia < rows and ia * cols <= ib * rows):
+            order.append(("A", ia))
+            ia += 1
+        else:
+            order.append(("B", ib))
+            ib += 1
+    pos = {blk: k for k, blk in enumerate(order)}
+    tiles = sorted(((i, j) for i in range(rows) for j in range(cols)),
+                   key=lambda t: (max(pos[("A", t[0])], pos[("B", t[1])]), t))
+    return order, tiles
+
+
+class TilePipeline:
+    """Two-dimensional tiling for programs whose output block (i, j) depends
+    only on row block i of a "row" input and column panel j of a "column"
+    input (mm: C[i, j] = A[i, :] . B[:, j]).  Output tile (i, j) can start as
+    soon as A's row block i and B's column panel j have arrived, instead of
+    after all of B (RowPipeline):
+
+        copy-in  : A_0, B_0, A_1, B_1, ...  (B panels by pitched H2D copies)
+        compute  : tile (i, j) once A_i and B_j are in, in arrival order,
+                   round-robin over `compute_streams` streams so that several
+                   small tile grids share the GPU
+        copy-out : tile (i, j) by a pitched D2H copy into C, after its kernel
+
+    Device layout: A as given (row blocks are contiguous), B as column panels
+    of K x N/cols contiguous floats, C as contiguous tiles of M/rows x N/cols.
+    Every element of C is computed by the same strategy from the same values
+    as the unchunked program, so the result is bit-identical to it.
+    """
+
+    def __init__(self, text_for_tile: Callable[[int, int], str], launch_for_tile: Callable[[int, int], object],
+                 M: int, N: int, K: int, rows: int, cols: int, row_input: str = "A", col_input: str = "B",
+                 compute_streams: int = 4, elem_bytes: int = 4, float_mode: bool = True, device: int = 0,
+                 name: str = "tile"):
+        if M % rows or N % cols:
+            raise ValueError(f"{M}x{N} does not split into {rows}x{cols} tiles")
+        self.M, self.N, self.K, self.rows, self.cols = M, N, K, rows, cols
+        self.tm, self.tn, self.eb, self.device = M // rows, N // cols, elem_bytes, device
+        self.row_input, self.col_input = row_input, col_input
+        prog = compile_program(text_for_tile(self.tm, self.tn), name=name)
+        self.exe = executable(prog, launch_for_tile(self.tm, self.tn), {}, float_mode=float_mode,
+                              device=device)
+        if compute_streams > 1 and any(kind not in ("out", "in") for k in self.exe.sig.kernels
+                                       for kind, _ in k.args):
+            raise ValueError("tile kernels with scratch buffers or grid counters cannot share "
+                             "them across concurrent streams; use compute_streams=1")
+        eb = elem_bytes
+        self.a = RT.DeviceBuffer(M * K * eb, device)
+        self.b = RT.DeviceBuffer(K * N * eb, device)
+        self.c = RT.DeviceBuffer(M * N * eb, device)
+        self.cin, self.cout = RT.Stream(device), RT.Stream(device)
+        self.comp = [RT.Stream(device) for _ in range(max(1, compute_streams))]
+        self.order, self.tiles = tile_schedule(rows, cols)
+
+    def run(self, host: Dict[str, np.ndarray], out: np.ndarray, stream: Optional[RT.Stream] = None):
+        """host row/column inputs (page-locked for overlap) -> out (page-locked,
+        M x N row-major), synchronised.  `stream`, if given, is ordered before
+        and after the whole pipeline."""
+        dev, eb, tm, tn, K, N = self.device, self.eb, self.tm, self.tn, self.K, self.N
+        streams = [self.cin, self.cout] + self.comp
+        if stream is not None:
+            ev = RT.Event(dev)
+            ev.record(stream)
+            for s in streams:
+                ev.wait_on(s)
+        A, B = host[self.row_input], host[self.col_input]
+        arrived = {}
+        for kind, k in self.order:
+            if kind == "A":
+                nb = tm * K * eb
+                RT.lib().dpia_memcpy_htod(dev, self.a.ptr + k * nb, ctypes.c_void_p(A.ctypes.data + k * nb),
+                                          nb, self.cin.handle)
+            else:
+                RT.lib().dpia_memcpy2d_htod(dev, self.b.ptr + k * K * tn * eb, tn * eb,
+                                            ctypes.c_void_p(B.ctypes.data + k * tn * eb), N * eb,
+                                            tn * eb, K, self.cin.handle)
+            e = RT.Event(dev)
+            e.record(self.cin)
+            arrived[(kind, k)] = e
+        done = []
+        for t, (i, j) in enumerate(self.tiles):
+            s = self.comp[t % len(self.comp)]
+            arrived[("A", i)].wait_on(s)
+            arrived[("B", j)].wait_on(s)
+            cptr = self.c.ptr + (i * self.cols + j) * tm * tn * eb
+            self.exe.launch_with(s, {self.row_input: self.a.ptr + i * tm * K * eb,
+                                     self.col_input: self.b.ptr + j * K * tn * eb, "out": cptr})
+            e = RT.Event(dev)
+            e.record(s)
+            done.append((e, i, j, cptr))
+        for e, i, j, cptr in done:
+            e.wait_on(self.cout)
+            RT.lib().dpia_memcpy2d_dtoh(dev, ctypes.c_void_p(out.ctypes.data + (i * tm * N + j * tn) * eb),
+                                        N * eb, cptr, tn * eb, tn * eb, tm, self.cout.handle)
+        if stream is not None:
+            for s in streams:
+                e = RT.Event(dev)
+                e.record(s)
+                e.wait_on(stream)
+            stream.sync()
+        else:
+            for s in streams:
+                s.sync()
+        return out
+
+
+def mm_tile_pipeline(M: int, N: int, K: int, rows: int = 4, cols: int = 4, compute_streams: int = 4,
+                     device: int = 0, **strategy) -> TilePipeline:
+    """mm (bench_programs.mm_program strategy) over rows x cols output tiles."""
+    from .bench_programs import mm_config
+    T = strategy.get("T", 128)
+    if (M // rows) % T or (N // cols) % T:
+        raise ValueError(f"tiles of {M // rows}x{N // cols} are not whole {T}x{T} work-group tiles")
+    text = lambda m, n: mm_config(M=m, N=n, K=K, **strategy).text  # noqa: E731
+    launch = lambda m, n: mm_config(M=m, N=n, K=K, **strategy).launch  # noqa: E731
+    return TilePipeline(text, launch, M, N, K, rows, cols, compute_streams=compute_streams,
+                        device=device, name="mm")

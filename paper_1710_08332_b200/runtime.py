@@ -43,6 +43,8 @@ _PROTOS = {
     "dpia_free_host": (None, [_vp]),
     "dpia_memcpy_htod": (_i, [_i, _u64, _vp, _sz, _vp]),
     "dpia_memcpy_dtoh": (_i, [_i, _vp, _u64, _sz, _vp]),
+    "dpia_memcpy2d_htod": (_i, [_i, _u64, _sz, _vp, _sz, _sz, _sz, _vp]),
+    "dpia_memcpy2d_dtoh": (_i, [_i, _vp, _sz, _u64, _sz, _sz, _sz, _vp]),
     "dpia_memcpy_dtod": (_i, [_i, _u64, _u64, _sz, _vp]),
     "dpia_memset": (_i, [_i, _u64, _i, _sz, _vp]),
     "dpia_launch": (_i, [_vp, _i, C.c_uint, C.c_uint, C.c_uint, C.c_uint, C.c_uint,

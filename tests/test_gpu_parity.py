@@ -360,6 +360,35 @@ def test_empty_inputs(launch):
             assert [float(v) for v in np.atleast_1d(got)] == [float(v) for v in want], (text, fm)
 
 
+@pytest.mark.parametrize("rows,cols,streams", [(1, 1, 1), (2, 2, 1), (2, 2, 4), (4, 2, 3), (1, 2, 2)])
+def test_mm_tile_pipeline_matches_unchunked(rows, cols, streams):
+    """pipeline.TilePipeline (row blocks of A, pitched column panels of B,
+    tile kernels on several streams, pitched D2H of C tiles) is bit-identical
+    to one launch of the whole product."""
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.bench_programs import mm_config
+    from paper_1710_08332_b200.pipeline import mm_tile_pipeline
+    M, N, K = 512, 256, 384
+    A = blas_np.seeded((M, K), 53, -1.0, 1.0)
+    B = blas_np.seeded((K, N), 54, -1.0, 1.0)
+    cfg = mm_config(M=M, N=N, K=K)
+    whole = np.asarray(run_program_cuda(compile_program(cfg.text), {"A": A, "B": B},
+                                        launch=cfg.launch, flat=True), np.float32)
+    pins = [RT.PinnedBuffer(a.nbytes) for a in (A, B)] + [RT.PinnedBuffer(4 * M * N)]
+    try:
+        ha, hb = pins[0].array(np.float32, A.size), pins[1].array(np.float32, B.size)
+        ha[:], hb[:] = A.ravel(), B.ravel()
+        out = pins[2].array(np.float32, M * N)
+        pipe = mm_tile_pipeline(M, N, K, rows=rows, cols=cols, compute_streams=streams)
+        for _ in range(2):
+            out[:] = np.nan
+            pipe.run({"A": ha, "B": hb}, out, RT.Stream(0))
+            assert np.array_equal(out, whole)
+    finally:
+        for p in pins:
+            p.free()
+
+
 @pytest.mark.parametrize("chunks", [1, 2, 4])
 def test_mm_row_pipeline_matches_unchunked(chunks):
     """pipeline.RowPipeline (row chunks of A / C, copies on their own streams

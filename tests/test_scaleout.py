@@ -224,3 +224,23 @@ def test_peer_and_pipeline_argument_checks():
         RowPipeline(lambda r: "", lambda r: (1, 1), 10, 3, {}, {}, 0)
     with pytest.raises(ValueError):
         mm_pipeline(256, 128, 128, chunks=4)   # 64-row chunks are not whole 128-row tiles
+    from paper_1710_08332_b200.pipeline import mm_tile_pipeline
+    with pytest.raises(ValueError):
+        mm_tile_pipeline(256, 256, 128, rows=2, cols=4)   # 64-column panels are not whole tiles
+    with pytest.raises(ValueError):
+        mm_tile_pipeline(256, 384, 128, rows=2, cols=2)   # 384 / 2 = 192 is not whole tiles
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 1), (4, 4), (4, 2), (1, 3), (5, 2)])
+def test_tile_schedule(rows, cols):
+    """TilePipeline's copy order interleaves A row blocks and B column panels
+    in proportion; every tile appears once, after the copies of both its
+    operands, and tiles are ordered by that copy (CPU)."""
+    from paper_1710_08332_b200.pipeline import tile_schedule
+    order, tiles = tile_schedule(rows, cols)
+    assert sorted(order) == sorted([("A", i) for i in range(rows)] + [("B", j) for j in range(cols)])
+    assert sorted(tiles) == [(i, j) for i in range(rows) for j in range(cols)]
+    pos = {b: k for k, b in enumerate(order)}
+    ready = [max(pos[("A", i)], pos[("B", j)]) for i, j in tiles]
+    assert ready == sorted(ready)
+    assert order[0] == ("A", 0) and ("B", 0) in order[:2 + rows // cols]

@@ -1,6 +1,8 @@
 """mm end to end from page-locked host memory (GPU box): Executable.run
 (copy A, B in; one launch; copy C out) against pipeline.mm_pipeline with
-2/4/8 row chunks (copies overlapped with the chunk kernels).
+2/4/8 row chunks (copies overlapped with the chunk kernels) and
+pipeline.mm_tile_pipeline with rows x cols output tiles on several compute
+streams.
 
     python tools/pipe_exp.py
 """
@@ -14,7 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import mm_config  # noqa: E402
-from paper_1710_08332_b200.pipeline import mm_pipeline  # noqa: E402
+from paper_1710_08332_b200.pipeline import mm_pipeline, mm_tile_pipeline  # noqa: E402
 
 
 def timed(fn, st, reps=6):
@@ -51,6 +53,13 @@ def main():
         C[:] = 0
         ms = timed(lambda: pipe.run({"A": A, "B": B}, C, st), st)
         print(f"mm_pipeline chunks={chunks}: {ms:.3f} ms  {flops / ms / 1e9:.2f} TFLOP/s  "
+              f"same={np.array_equal(C, ref)}", flush=True)
+    for rows, cols, streams in ((2, 2, 2), (4, 4, 1), (4, 4, 2), (4, 4, 4), (4, 4, 8), (8, 4, 4),
+                                (4, 8, 4), (8, 8, 4), (8, 8, 8)):
+        pipe = mm_tile_pipeline(M, N, K, rows=rows, cols=cols, compute_streams=streams)
+        C[:] = 0
+        ms = timed(lambda: pipe.run({"A": A, "B": B}, C, st), st)
+        print(f"mm_tile_pipeline {rows}x{cols} streams={streams}: {ms:.3f} ms  {flops / ms / 1e9:.2f} TFLOP/s  "
               f"same={np.array_equal(C, ref)}", flush=True)
 
 
