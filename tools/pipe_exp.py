@@ -54,11 +54,17 @@ def main():
         ms = timed(lambda: pipe.run({"A": A, "B": B}, C, st), st)
         print(f"mm_pipeline chunks={chunks}: {ms:.3f} ms  {flops / ms / 1e9:.2f} TFLOP/s  "
               f"same={np.array_equal(C, ref)}", flush=True)
-    for rows, cols, streams in ((2, 2, 2), (4, 4, 1), (4, 4, 2), (4, 4, 4), (4, 4, 8), (8, 4, 4),
-                                (4, 8, 4), (8, 8, 4), (8, 8, 8)):
+    import time
+    for rows, cols, streams in ((2, 2, 2), (2, 2, 4), (4, 4, 1), (4, 4, 2), (4, 4, 4), (4, 4, 8), (4, 4, 12),
+                                (4, 4, 16), (2, 4, 8), (4, 2, 8), (8, 4, 8), (4, 8, 8), (8, 8, 8),
+                                (8, 8, 16)):
         pipe = mm_tile_pipeline(M, N, K, rows=rows, cols=cols, compute_streams=streams)
         C[:] = 0
         ms = timed(lambda: pipe.run({"A": A, "B": B}, C, st), st)
+        t0 = time.perf_counter()
+        pipe.run({"A": A, "B": B}, C, st)
+        host = (time.perf_counter() - t0) * 1e3
+        print(f"host wall of one run (enqueue + wait) {host:.3f} ms; ", end="")
         print(f"mm_tile_pipeline {rows}x{cols} streams={streams}: {ms:.3f} ms  {flops / ms / 1e9:.2f} TFLOP/s  "
               f"same={np.array_equal(C, ref)}", flush=True)
 
