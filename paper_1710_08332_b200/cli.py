@@ -129,8 +129,17 @@ def _run(args) -> int:
         # iterations of every parallel loop already run in no fixed order
         print("note: --reverse has no effect on the GPU (parallel iterations are unordered)",
               file=sys.stderr)
-    outs = run_kernel(prog.imperative, prog.params, inputs, args.launch or (148, 256), sigma,
-                      float_mode=not args.int_mode, device=args.gpu, name=prog.name)
+    if args.gpus > 1:
+        from .shard import ShardError, run_sharded
+        try:
+            outs = run_sharded(prog, inputs, args.launch or (148, 256), sigma,
+                               float_mode=not args.int_mode, gpus=args.gpus, name=prog.name,
+                               first_device=args.gpu)
+        except ShardError as e:
+            raise CliError(f"{args.file}: cannot run on {args.gpus} GPUs: {e}", EXIT_PARSE)
+    else:
+        outs = run_kernel(prog.imperative, prog.params, inputs, args.launch or (148, 256), sigma,
+                          float_mode=not args.int_mode, device=args.gpu, name=prog.name)
     for k in sorted(outs):
         print(f"{k} = {_show(outs[k])}")
     return 0
@@ -169,7 +178,10 @@ def build_parser() -> argparse.ArgumentParser:
     r.add_argument("file")
     r.add_argument("--inputs")
     r.add_argument("--device", choices=["cuda"], default="cuda")
-    r.add_argument("--gpu", type=int, default=0)
+    r.add_argument("--gpu", type=int, default=0, help="device (the first of --gpus)")
+    r.add_argument("--gpus", type=int, default=1,
+                   help="split the outermost map over this many GPUs (chunk-local maps and "
+                        "(+)/0 reductions of them; paper_1710_08332_b200/shard.py)")
     r.add_argument("--launch", type=_launch_pair)
     r.add_argument("--reverse", action="store_true",
                    help="accepted for compatibility (parfor order is never fixed on the GPU)")

@@ -1,0 +1,113 @@
+"""`dpia run --gpus K` (paper_1710_08332_b200/shard.py): which programs split
+over devices (CPU), and that a split run equals the oracle on the whole input
+(GPU; the shards share the box's one GPU through the explicit `devices`
+list, the code path a K-GPU node runs with K distinct devices)."""
+import numpy as np
+import pytest
+
+from oracle.dpia_eval import eval_phrase, flatten_value
+from paper_1710_08332_b200 import compile_program
+from paper_1710_08332_b200.bench_programs import (asum_program, dot_program, gemv_config, mm_config,
+                                                  scal_config)
+from paper_1710_08332_b200.shard import ShardError, shard_spec
+
+SQUARE_MAP = """
+(nat n)
+(param xs (exp (array (* n 4) num)))
+(asScalar4 (mapGlobal (lam (v (exp (vec 4))) (* v v)) (asVector4 xs)))
+"""
+CHUNK_MAP = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(param ys (exp (array (* n 8) num)))
+(join (mapWorkgroup (lam (c (exp (array 8 (pair num num))))
+  (mapLocal (lam (p (exp (pair num num))) (+ (* (fst p) 3) (snd p))) c))
+  (split 8 (zip xs ys))))
+"""
+PRODUCT = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(reduceLocal (*) 1 (mapGlobal (lam (c (exp (array 8 num))) (reduce (+) 0 c)) (split 8 xs)))
+"""
+OFFSET_SUM = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(reduceLocal (+) 1 (mapGlobal (lam (c (exp (array 8 num))) (reduce (+) 0 c)) (split 8 xs)))
+"""
+TRANSPOSED = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(join (mapGlobal (lam (c (exp (array 8 num))) (mapSeq (lam (x (exp num)) (+ x 1)) c))
+  (transpose (split n xs))))
+"""
+
+
+@pytest.mark.parametrize("text,kind", [
+    (dot_program(32, 2), "sum"), (asum_program(32, 2), "sum"), (SQUARE_MAP, "map"), (CHUNK_MAP, "map")])
+def test_shard_spec_accepts(text, kind):
+    assert shard_spec(compile_program(text)).kind == kind
+
+
+@pytest.mark.parametrize("text", [gemv_config(1024, 1024).text, mm_config(128, 128, 128).text,
+                                  scal_config().text, PRODUCT, OFFSET_SUM, TRANSPOSED])
+def test_shard_spec_rejects(text):
+    """No size parameter (gemv, mm), an unsplittable input (scal's alpha
+    splat), a combine that is not (+)/0, and a map over a transposed view
+    (its chunks interleave the input) are refused, never split."""
+    with pytest.raises(ShardError):
+        shard_spec(compile_program(text))
+
+
+def test_cli_gpus_refuses_unshardable(tmp_path):
+    from paper_1710_08332_b200.cli import main
+    f = tmp_path / "p.dpia"
+    f.write_text(PRODUCT)
+    inp = tmp_path / "p.inputs"
+    inp.write_text("n=2\nxs=[" + ",".join(["1"] * 16) + "]\n")
+    assert main(["run", str(f), "--inputs", str(inp), "--gpus", "2", "--int"]) == 2
+
+
+def _inputs(text, n, seed):
+    prog = compile_program(text)
+    rng = np.random.default_rng(seed)
+    data = {}
+    for name, t in prog.source.params:
+        size = t.data.size.evaluate({"n": n})
+        data[name] = rng.integers(-9, 10, size).tolist()
+    return prog, data
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("text,n,launch", [
+    (dot_program(32, 2), 16, (4, 32)), (asum_program(32, 2), 16, (4, 32)),
+    (SQUARE_MAP, 64, (4, 32)), (CHUNK_MAP, 32, (8, 8))])
+@pytest.mark.parametrize("shards", [1, 2, 4])
+def test_sharded_run_matches_oracle(text, n, launch, shards):
+    """int mode: bit-exact against eval_phrase over the whole input."""
+    from paper_1710_08332_b200.shard import run_sharded
+    prog, data = _inputs(text, n, 7 + shards)
+    got = run_sharded(prog, data, launch, {"n": n}, float_mode=False, gpus=shards, devices=[0] * shards)
+    want = eval_phrase(prog.source.body, data, {"n": n})
+    assert flatten_value(got["out"]) == flatten_value(want)
+
+
+@pytest.mark.gpu
+def test_sharded_dot_float_within_tolerance():
+    from paper_1710_08332_b200.shard import run_sharded
+    text, n = dot_program(32, 2), 32
+    prog = compile_program(text)
+    rng = np.random.default_rng(3)
+    size = 4 * 64 * n
+    data = {"xs": rng.uniform(0, 1, size).astype(np.float32),
+            "ys": rng.uniform(0, 1, size).astype(np.float32)}
+    got = run_sharded(prog, data, (8, 32), {"n": n}, float_mode=True, gpus=4, devices=[0] * 4)
+    want = float(np.dot(data["xs"].astype(np.float64), data["ys"].astype(np.float64)))
+    assert abs(float(flatten_value(got["out"])[0]) - want) <= 1e-4 * want
+
+
+def test_sharded_run_uneven_split_is_refused():
+    """Checked before any device work (CPU)."""
+    from paper_1710_08332_b200.shard import run_sharded
+    prog, data = _inputs(SQUARE_MAP, 6, 1)
+    with pytest.raises(ShardError):
+        run_sharded(prog, data, (4, 32), {"n": 6}, float_mode=False, gpus=4, devices=[0] * 4)
