@@ -53,7 +53,19 @@ def executable(prog: Program, launch, sigma: Optional[Dict[str, int]] = None,
 
 
 def run_program_cuda(prog: Program, inputs: Dict[str, object], sigma=None, launch=(148, 256),
-                     float_mode: bool = True, device: int = 0, flat: bool = False):
+                     float_mode: bool = True, device: int = 0, flat: bool = False, gpus: int = 1):
+    """Run a compiled program on the GPU and return its output value.
+    gpus > 1 splits the outermost map over devices device .. device+gpus-1
+    (shard.run_sharded; chunk-local maps and (+)/0 reductions of them)."""
+    if gpus > 1:
+        from .shard import run_sharded
+        val = run_sharded(prog, inputs, launch, dict(sigma or {}), float_mode, gpus, prog.name,
+                          first_device=device)["out"]
+        if flat:
+            from . import layout as LY
+            import numpy as np
+            return np.asarray(LY.flatten(val))
+        return val
     out = run_kernel(prog.imperative, prog.params, inputs, launch, sigma, float_mode, device,
                      prog.name, flat=flat)
     return out["out"]

@@ -111,3 +111,20 @@ def test_sharded_run_uneven_split_is_refused():
     prog, data = _inputs(SQUARE_MAP, 6, 1)
     with pytest.raises(ShardError):
         run_sharded(prog, data, (4, 32), {"n": 6}, float_mode=False, gpus=4, devices=[0] * 4)
+
+
+@pytest.mark.gpu
+def test_run_program_cuda_gpus():
+    """The Program-level API: gpus=2 runs on two devices when the node has
+    them (checked against the oracle); on a one-GPU node it is refused with
+    ShardError before any launch."""
+    from paper_1710_08332_b200 import run_program_cuda
+    from paper_1710_08332_b200 import runtime as RT
+    prog, data = _inputs(dot_program(32, 2), 8, 5)
+    if RT.device_count() >= 2:
+        got = run_program_cuda(prog, data, {"n": 8}, (4, 32), float_mode=False, gpus=2, flat=True)
+        want = eval_phrase(prog.source.body, data, {"n": 8})
+        assert [int(v) for v in got] == flatten_value(want)
+    else:
+        with pytest.raises(ShardError):
+            run_program_cuda(prog, data, {"n": 8}, (4, 32), float_mode=False, gpus=2)
