@@ -71,6 +71,12 @@ int dpia_memset(int device, uint64_t dst, int value, size_t bytes, void* stream)
  * shared memory, `args` = array of pointers to each argument value. */
 int dpia_launch(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
                 unsigned smem, void** args, void* stream);
+/* the same with programmatic dependent launch allowed (cuLaunchKernelEx,
+ * CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION): the kernel may
+ * start before the previous kernel on the stream finishes and waits for it
+ * with griddepcontrol.wait */
+int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
+                    unsigned smem, void** args, void* stream);
 int dpia_stream_create(int device, void** stream);
 int dpia_stream_destroy(void* stream);
 int dpia_stream_sync(void* stream);

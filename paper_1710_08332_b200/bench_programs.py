@@ -391,7 +391,7 @@ def dot_config(N: int = 1 << 24, L: int = 1024, K: int = 16, blocks=None) -> Con
     return Config("dot", dot_program(L, K), {"n": n}, (blocks or n, L), bytes=8 * N, flops=2 * N)
 
 
-def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 32, blocks=None) -> Config:
+def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
     n = N // per_wg

@@ -29,7 +29,7 @@
   X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
   X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)          \
   X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuStreamWaitEvent)   \
-  X(cuCtxGetCurrent) X(cuMemcpy2DAsync)
+  X(cuCtxGetCurrent) X(cuMemcpy2DAsync) X(cuLaunchKernelEx)
 
 namespace drv {
 #define DPIA_DECL(f) decltype(&::f) f = nullptr;
@@ -401,6 +401,33 @@ int dpia_launch(void* function, int device, unsigned gx, unsigned gy, unsigned b
   if (int e = bind(device)) return e;
   CU(drv::cuLaunchKernel(static_cast<CUfunction>(function), gx, gy, 1, bx, by, 1, smem,
                     static_cast<CUstream>(stream), args, nullptr));
+  return 0;
+}
+
+// Launch with programmatic dependent launch allowed: the kernel may start
+// while the previous kernel on `stream` is still running; it must execute
+// griddepcontrol.wait before touching that kernel's results, and the previous
+// kernel may trigger it early with griddepcontrol.launch_dependents.
+int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
+                    unsigned smem, void** args, void* stream) {
+  if (int e = bind(device)) return e;
+  CUlaunchAttribute attr[1];
+  std::memset(attr, 0, sizeof(attr));
+  attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+  attr[0].value.programmaticStreamSerializationAllowed = 1;
+  CUlaunchConfig cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDimX = gx;
+  cfg.gridDimY = gy;
+  cfg.gridDimZ = 1;
+  cfg.blockDimX = bx;
+  cfg.blockDimY = by;
+  cfg.blockDimZ = 1;
+  cfg.sharedMemBytes = smem;
+  cfg.hStream = static_cast<CUstream>(stream);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU(drv::cuLaunchKernelEx(&cfg, static_cast<CUfunction>(function), args, nullptr));
   return 0;
 }
 

@@ -49,6 +49,8 @@ _PROTOS = {
     "dpia_memset": (_i, [_i, _u64, _i, _sz, _vp]),
     "dpia_launch": (_i, [_vp, _i, C.c_uint, C.c_uint, C.c_uint, C.c_uint, C.c_uint,
                          C.POINTER(_vp), _vp]),
+    "dpia_launch_pdl": (_i, [_vp, _i, C.c_uint, C.c_uint, C.c_uint, C.c_uint, C.c_uint,
+                             C.POINTER(_vp), _vp]),
     "dpia_stream_create": (_i, [_i, C.POINTER(_vp)]),
     "dpia_stream_destroy": (_i, [_vp]),
     "dpia_stream_sync": (_i, [_vp]),
@@ -326,9 +328,11 @@ class Event:
             pass
 
 
-def launch(fn, device: int, grid, block, smem: int, arg_values: List, stream: Optional[Stream]):
-    """arg_values: list of ctypes scalars (c_uint64 pointers / c_longlong sizes)."""
+def launch(fn, device: int, grid, block, smem: int, arg_values: List, stream: Optional[Stream],
+           pdl: bool = False):
+    """arg_values: list of ctypes scalars (c_uint64 pointers / c_longlong sizes).
+    pdl: programmatic dependent launch (dpia_launch_pdl)."""
     arr = (ctypes.c_void_p * len(arg_values))(*[ctypes.cast(ctypes.byref(v), ctypes.c_void_p)
                                                   for v in arg_values])
-    lib().dpia_launch(fn, device, grid[0], grid[1], block[0], block[1], smem, arr,
-                      stream.handle if stream else None)
+    (lib().dpia_launch_pdl if pdl else lib().dpia_launch)(
+        fn, device, grid[0], grid[1], block[0], block[1], smem, arr, stream.handle if stream else None)

@@ -41,6 +41,26 @@ def main(which):
         inputs = {"xs": rng.uniform(-1, 1, 1 << 26).astype(np.float32)}
         grid = [(L, K, b) for L in (512, 1024) for K in (16, 32, 64, 128) for b in (None, 592, 1184)]
         mk = lambda L, K, b: asum_config(L=L, K=K, blocks=b)  # noqa: E731
+    elif which in ("dotx", "asumx"):
+        # small work-groups and exactly balanced grids: n chunks over G = n / k
+        # groups (k chunks each, grid-stride), one wave or less
+        if which == "dotx":
+            inputs = {"xs": rng.uniform(0, 1, 1 << 24).astype(np.float32),
+                      "ys": rng.uniform(0, 1, 1 << 24).astype(np.float32)}
+            total, mkc = 1 << 24, dot_config
+        else:
+            inputs = {"xs": rng.uniform(-1, 1, 1 << 26).astype(np.float32)}
+            total, mkc = 1 << 26, asum_config
+        grid = []
+        for L in (128, 256, 512, 1024):
+            for K in (2, 4, 8, 16, 32):
+                n = total // (4 * K * L)
+                for per in (1, 2, 4, 8):
+                    G = n // per
+                    if G * L <= 148 * 2048 and G >= 148 and n % per == 0:
+                        grid.append((L, K, None if per == 1 else G))
+        mk = lambda L, K, b: mkc(L=L, K=K, blocks=b)  # noqa: E731
+        which = which[:-1]
     elif which == "dot":
         inputs = {"xs": rng.uniform(0, 1, 1 << 24).astype(np.float32),
                   "ys": rng.uniform(0, 1, 1 << 24).astype(np.float32)}

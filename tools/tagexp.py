@@ -14,6 +14,9 @@ timed like bench.py (L2 scrubbed, events on the launching stream, mean of
                  relaxed loads until every generation matches, combines them
                  in the same fixed order, and bumps the generation word
   tagged-ns   -- tagged with a __nanosleep(64) back-off between polls
+  part+comb   -- two kernels: partials, then a one-block combine launched
+                 with programmatic dependent launch (pdl=True; part_trig
+                 triggers the dependent launch at block start) or plainly
 """
 import os
 import statistics
@@ -101,6 +104,35 @@ __device__ __forceinline__ void tagged_body(const float4* p, long long n4, float
   float u = block_sum(v, red);
   if (threadIdx.x == 0) { out[0] = u; *gen_word = gen; }
 }
+// two kernels: partials, then a one-block combine.  With PDL the combine is
+// launched while the partials kernel runs (every partials block triggers
+// griddepcontrol.launch_dependents at its start) and waits in
+// griddepcontrol.wait until the partials grid has completed and flushed.
+template <int TRIGGER>
+__device__ __forceinline__ void part_body(const float4* p, long long n4, float* out) {
+  if (TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  __shared__ float red[32];
+  float t = block_sum(read_part(p, n4), red);
+  if (threadIdx.x == 0) out[1 + blockIdx.x] = t;
+}
+extern "C" __global__ void __launch_bounds__(1024) part_trig(const float4* p, long long n4, float* out,
+                                                             unsigned* ctr, unsigned long long* slots) {
+  part_body<1>(p, n4, out);
+}
+extern "C" __global__ void __launch_bounds__(1024) part_plain(const float4* p, long long n4, float* out,
+                                                              unsigned* ctr, unsigned long long* slots) {
+  part_body<0>(p, n4, out);
+}
+extern "C" __global__ void __launch_bounds__(1024) comb(const float4* p, long long nparts, float* out,
+                                                        unsigned* ctr, unsigned long long* slots) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __shared__ float red[32];
+  float v = 0.f;
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) v += out[1 + i];
+  float u = block_sum(v, red);
+  if (threadIdx.x == 0) out[0] = u;
+}
+
 extern "C" __global__ void __launch_bounds__(1024) tagged(const float4* p, long long n4, float* out,
                                                           unsigned* ctr, unsigned long long* slots) {
   tagged_body<0>(p, n4, out, ctr + 64, slots);
@@ -143,8 +175,22 @@ def main():
         slots.zero(st)
         args = [RT.C.c_uint64(buf.ptr), RT.C.c_longlong(nbytes // 16), RT.C.c_uint64(out.ptr),
                 RT.C.c_uint64(ctr.ptr), RT.C.c_uint64(slots.ptr)]
+        fc = mod.function("comb")
         for rnd in range(2):
-            for name in ("rblock", "ticket", "tagged", "tagged_ns"):
+            for pname, pdl in (("part_trig", True), ("part_plain", True), ("part_plain", False)):
+                fp = mod.function(pname)
+                for blocks in (256, 512):
+                    cargs = [args[0], RT.C.c_longlong(blocks)] + args[2:]
+
+                    def two():
+                        RT.launch(fp, 0, (blocks, 1), (1024, 1), 0, args, st)
+                        RT.launch(fc, 0, (1, 1), (1024, 1), 0, cargs, st, pdl=pdl)
+                    t = timed(st, two)
+                    o = np.zeros(1, np.float32)
+                    out.download(o)
+                    print(f"{nbytes >> 20:4d} MiB round {rnd} {pname}+comb pdl={pdl!s:5s}: {t:7.2f} us  "
+                          f"{nbytes / t / 1e3:6.0f} GB/s  blocks={blocks} out[0]={o[0]:.0f}", flush=True)
+            for name in ("rblock", "ticket"):
                 fn = mod.function(name)
                 for blocks in (256, 512):
                     t = timed(st, lambda: RT.launch(fn, 0, (blocks, 1), (1024, 1), 0, args, st))
