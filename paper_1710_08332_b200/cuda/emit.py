@@ -1608,6 +1608,12 @@ class ProgramEmitter:
         else:
             head.append("  const int dpia_nthreads = (int)(blockDim.x * blockDim.y);")
         head.append("  const int dpia_tid = (int)(threadIdx.y * blockDim.x + threadIdx.x);")
+        if ki > 0:
+            # launched with programmatic dependent launch (launcher.Executable):
+            # the grid may be scheduled while the previous phase's kernel still
+            # runs and waits here until that grid has completed and its memory
+            # is visible (a no-op under an ordinary launch)
+            head.append('  asm volatile("griddepcontrol.wait;" ::: "memory");')
         if ke.uses_gid:
             wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
             it = "long long" if wide else "int"

@@ -109,10 +109,13 @@ class Executable:
         if self.peer is not None:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
-        for k, vals in zip(self.sig.kernels, self._args):
+        for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
             grid = g if k.grid == "launch" else (1, 1)
             fn = self.module.function(k.name)
-            RT.launch(fn, self.device, grid, l, k.smem, vals, stream)
+            # later phases: programmatic dependent launch (their first
+            # statement is griddepcontrol.wait), which hides their launch
+            # latency behind the previous phase
+            RT.launch(fn, self.device, grid, l, k.smem, vals, stream, pdl=i > 0)
 
     def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int]):
         """Launch with some parameters re-pointed (device addresses), e.g. at
@@ -120,11 +123,12 @@ class Executable:
         if self.peer is not None:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
-        for k, vals in zip(self.sig.kernels, self._args):
+        for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
             vals = [RT.C.c_uint64(ptrs[n]) if kind in ("out", "in") and n in ptrs else v
                     for (kind, n), v in zip(k.args, vals)]
             grid = g if k.grid == "launch" else (1, 1)
-            RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream)
+            RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream,
+                      pdl=i > 0)
 
     def run(self, inputs: Dict[str, object], stream: Optional[RT.Stream] = None,
             out: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:

@@ -137,3 +137,27 @@ def test_cli_reference_compile_flags(tmp_path, capsys):
     # the reference-only targets are not the CUDA backend's
     with pytest.raises(SystemExit):
         main(["compile", f, "--target", "opencl"])
+
+
+def test_later_phases_wait_for_the_previous_grid():
+    """Kernels after the first are launched with programmatic dependent
+    launch (Executable.launch), so each must begin with griddepcontrol.wait
+    and the first must not (CPU: emitted text only)."""
+    import json
+    import re
+    from paper_1710_08332_b200 import compile_program, emit_cuda
+    seen = 0
+    for v in json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fuzz.json")))[:400]:
+        try:
+            p = compile_program(v["text"])
+            src, sig = emit_cuda(p.imperative, [("out", p.out_type)],
+                                 [(n, t.data) for n, t in p.source.params], float_mode=False, name="t",
+                                 launch=(4, 32), sigma=v.get("sigma"))
+        except Exception:  # noqa: BLE001 -- programs the backend rejects are not the point here
+            continue
+        bodies = re.split(r'extern "C" __global__', src)[1:]
+        assert len(bodies) == len(sig.kernels)
+        for i, b in enumerate(bodies):
+            assert ("griddepcontrol.wait" in b) == (i > 0)
+        seen += len(bodies) > 1
+    assert seen > 10

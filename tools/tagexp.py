@@ -14,6 +14,9 @@ timed like bench.py (L2 scrubbed, events on the launching stream, mean of
                  relaxed loads until every generation matches, combines them
                  in the same fixed order, and bumps the generation word
   tagged-ns   -- tagged with a __nanosleep(64) back-off between polls
+  ticket_first -- the ticket is taken before publishing; the non-last
+                 blocks publish tagged 64-bit words without a fence and the
+                 last block polls them (no fence on the critical path)
   part+comb   -- two kernels: partials, then a one-block combine launched
                  with programmatic dependent launch (pdl=True; part_trig
                  triggers the dependent launch at block start) or plainly
@@ -104,6 +107,48 @@ __device__ __forceinline__ void tagged_body(const float4* p, long long n4, float
   float u = block_sum(v, red);
   if (threadIdx.x == 0) { out[0] = u; *gen_word = gen; }
 }
+// ticket first: every block takes its ticket with a relaxed atomic before
+// publishing; the non-last blocks then publish {value, generation} in one
+// 64-bit store (no fence), and the last block -- which never has to publish
+// its own partial -- polls only the slots whose owners already hold a ticket.
+extern "C" __global__ void __launch_bounds__(1024) ticket_first(const float4* p, long long n4, float* out,
+                                                                unsigned* ctr, unsigned long long* slots) {
+  __shared__ float red[32];
+  __shared__ unsigned tk;
+  __shared__ float mine;
+  unsigned* gen_word = ctr + 64;
+  const unsigned gen = *((volatile unsigned*)gen_word) + 1u;
+  float t = block_sum(read_part(p, n4), red);
+  if (threadIdx.x == 0) {
+    tk = atomicAdd(ctr, 1u);
+    mine = t;
+  }
+  __syncthreads();
+  if (tk != gridDim.x - 1) {
+    if (threadIdx.x == 0) {
+      unsigned long long w = ((unsigned long long)gen << 32) | __float_as_uint(t);
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" :: "l"(slots + blockIdx.x), "l"(w) : "memory");
+    }
+    return;
+  }
+  float v = 0.f;
+  if (threadIdx.x < gridDim.x) {
+    if (threadIdx.x == blockIdx.x) {
+      v = mine;
+    } else {
+      unsigned long long w;
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(slots + threadIdx.x) : "memory");
+        if ((unsigned)(w >> 32) == gen) break;
+      }
+      v = __uint_as_float((unsigned)w);
+    }
+  }
+  __syncthreads();
+  float u = block_sum(v, red);
+  if (threadIdx.x == 0) { out[0] = u; *ctr = 0; *gen_word = gen; }
+}
+
 // two kernels: partials, then a one-block combine.  With PDL the combine is
 // launched while the partials kernel runs (every partials block triggers
 // griddepcontrol.launch_dependents at its start) and waits in
@@ -190,7 +235,7 @@ def main():
                     out.download(o)
                     print(f"{nbytes >> 20:4d} MiB round {rnd} {pname}+comb pdl={pdl!s:5s}: {t:7.2f} us  "
                           f"{nbytes / t / 1e3:6.0f} GB/s  blocks={blocks} out[0]={o[0]:.0f}", flush=True)
-            for name in ("rblock", "ticket"):
+            for name in ("rblock", "ticket", "ticket_first"):
                 fn = mod.function(name)
                 for blocks in (256, 512):
                     t = timed(st, lambda: RT.launch(fn, 0, (blocks, 1), (1024, 1), 0, args, st))
