@@ -344,7 +344,7 @@ def ref_lib():
     return lib
 
 
-def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None):
+def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1):
     """Time the reference's own CPU path (its c-openmp emission of the same
     strategy, compiled by oracle/build_ref.py) on all host threads."""
     import ctypes
@@ -388,7 +388,8 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None):
         nbytes = None
     else:
         return None
-    call()
+    for _ in range(max(1, warmup if nbytes is not None else min(warmup, 1))):
+        call()
     times = []
     t_start = time.perf_counter()
     while True:
@@ -473,12 +474,18 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        r = cpu_reference(args.workload, steps=args.steps)
+        r = cpu_reference(args.workload, steps=args.steps, warmup=args.warmup)
         unit = "GFLOP/s" if args.workload == "mm" else "GB/s"
+        from paper_1710_08332_b200.bench_programs import CONFIGS
+        cfg_line = (dict({k: v for k, v in _cfg_desc(CONFIGS[args.workload]()).items() if k != "l2"},
+                         reference_path="the reference's c-openmp emission of the same workload on the "
+                                        "host cores (oracle/_ref)")
+                    if args.workload in CONFIGS else
+                    {"workload": f"{args.workload} (reference c-openmp path on host cores)"})
         line = {"impl": "reference", "metric": METRIC, "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": f"{args.workload} (reference c-openmp path on host cores)"}}
+                "config": cfg_line}
         if r is None:
             line.update({"unavailable": "oracle/_ref/libref_cpu.so not built (needs /root/reference at build)"})
         else:

@@ -161,3 +161,42 @@ def test_later_phases_wait_for_the_previous_grid():
             assert ("griddepcontrol.wait" in b) == (i > 0)
         seen += len(bodies) > 1
     assert seen > 10
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the reference's own c-openmp CPU path) prints
+    one JSON line with the arm's metric, unit and config (CPU; skipped when
+    oracle/_ref was not built)."""
+    import json
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libref_cpu.so")):
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", "dot", "--steps", "2", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "GB/s" and line["value"] > 0
+    assert line["config"]["workload"].startswith("dot N=2^24")
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "reference"
+
+
+@pytest.mark.gpu
+def test_bench_json_contract():
+    """One short `bench.py` run on the GPU: every key of the driver's contract
+    is present and consistent."""
+    import json
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--no-suite", "--no-cpu"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "scaling", "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "clocks",
+              "gpu_launches", "cpu_baseline"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["value"] > 0 and line["gpu_launches"] >= 3
+    roof = line["roofline"]
+    assert roof["bound"] == "hbm" and roof["unit"] == "GB/s" and 0 < roof["frac"] < 1.5
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-3
+    e2e = line["e2e"]
+    assert e2e["h2d_bytes_per_step"] == 4 << 26 and e2e["value"] > 0
+    assert line["clocks"]["sm_max_mhz"] > 0
