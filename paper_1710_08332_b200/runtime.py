@@ -106,10 +106,36 @@ _LIB: Optional[_Lib] = None
 _LOCK = threading.Lock()
 
 
+def build_lib(out: str = LIB_PATH, verbose: bool = False) -> str:
+    """Compile csrc/dpia_rt.cpp into libdpia_rt.so with the host C++
+    compiler (the recipe __graft_entry__.build() uses)."""
+    import subprocess
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    root = os.path.dirname(PKG)
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cmd = ["g++", "-O2", "-shared", "-fPIC", "-std=c++17", "-Wall",
+           "-I", os.path.join(root, "include"), "-I", os.path.join(cuda, "include"),
+           os.path.join(PKG, "csrc", "dpia_rt.cpp"),
+           "-L", os.path.join(cuda, "lib64"), "-lnvrtc", "-ldl",
+           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", out]
+    if verbose:
+        print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def lib() -> _Lib:
+    """The loaded runtime.  A checkout without the built library (it is not
+    in version control) builds it once from csrc/ before loading; a failed
+    build raises DpiaRuntimeError -- there is no CPU fallback."""
     global _LIB
     with _LOCK:
         if _LIB is None:
+            if not os.path.exists(LIB_PATH):
+                try:
+                    build_lib()
+                except Exception as e:  # noqa: BLE001
+                    raise DpiaRuntimeError(-1, f"{LIB_PATH} is missing and could not be built: {e}")
             _LIB = _Lib()
         return _LIB
 
