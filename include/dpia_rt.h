@@ -74,7 +74,8 @@ int dpia_launch(void* function, int device, unsigned gx, unsigned gy, unsigned b
 /* the same with programmatic dependent launch allowed (cuLaunchKernelEx,
  * CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION): the kernel may
  * start before the previous kernel on the stream finishes and waits for it
- * with griddepcontrol.wait */
+ * with griddepcontrol.wait; used for the later phases of multi-kernel
+ * programs (no reference counterpart: the reference simulator has no launches) */
 int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
                     unsigned smem, void** args, void* stream);
 int dpia_stream_create(int device, void** stream);
