@@ -29,12 +29,15 @@
   X(cuStreamCreate) X(cuStreamDestroy) X(cuStreamSynchronize) X(cuEventCreate)               \
   X(cuEventDestroy) X(cuEventRecord) X(cuEventSynchronize) X(cuEventElapsedTime)          \
   X(cuIpcGetMemHandle) X(cuIpcOpenMemHandle) X(cuIpcCloseMemHandle) X(cuStreamWaitEvent)   \
-  X(cuCtxGetCurrent) X(cuMemcpy2DAsync) X(cuLaunchKernelEx)
+  X(cuCtxGetCurrent) X(cuMemcpy2DAsync)
 
 namespace drv {
 #define DPIA_DECL(f) decltype(&::f) f = nullptr;
 DPIA_DRIVER_FUNCS(DPIA_DECL)
 #undef DPIA_DECL
+// optional: without it, dpia_launch_pdl degrades to an ordinary launch (the
+// kernels' griddepcontrol.wait is then a no-op and ordering is the stream's)
+decltype(&::cuLaunchKernelEx) cuLaunchKernelEx = nullptr;
 }  // namespace drv
 
 namespace {
@@ -62,6 +65,8 @@ int load_driver() {
   if (!drv::f) return fail(-1, "CUDA driver lacks %s", DPIA_STR(f));
   DPIA_DRIVER_FUNCS(DPIA_LOAD)
 #undef DPIA_LOAD
+  drv::cuLaunchKernelEx =
+      reinterpret_cast<decltype(drv::cuLaunchKernelEx)>(dlsym(g_libcuda, DPIA_STR(cuLaunchKernelEx)));
   return 0;
 }
 
@@ -411,6 +416,8 @@ int dpia_launch(void* function, int device, unsigned gx, unsigned gy, unsigned b
 int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsigned bx, unsigned by,
                     unsigned smem, void** args, void* stream) {
   if (int e = bind(device)) return e;
+  if (!drv::cuLaunchKernelEx)
+    return dpia_launch(function, device, gx, gy, bx, by, smem, args, stream);
   CUlaunchAttribute attr[1];
   std::memset(attr, 0, sizeof(attr));
   attr[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
