@@ -46,6 +46,21 @@ def test_strategy_fuzz_gpu_fp32(seed):
     assert [float(v) for v in got] == [float(v) for v in want]
 
 
+@pytest.mark.gpu
+def test_strategy_fuzz_fp32_beyond_exact_range():
+    """Seed 5487 of the long campaign cubes products of products (|values|
+    up to 2e9 > 2^24): int mode stays exact; fp32 rounds, and every element
+    is within 2^-20 relative of the exact value (fuzz_campaign.same_values)."""
+    from fuzz_campaign import same_values
+    from paper_1710_08332_b200 import run_program_cuda
+    prog, inputs, sigma, launch, want = _case(5487)
+    assert max(abs(w) for w in want) > 1 << 24
+    got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=False, flat=True)
+    assert [int(v) for v in got] == want
+    got = run_program_cuda(prog, inputs, sigma=sigma, launch=launch, float_mode=True, flat=True)
+    assert same_values([float(v) for v in got], [float(v) for v in want], True)
+
+
 def _case2d(seed):
     text, inputs, sigma, launch, desc = generate2d(seed)
     prog = compile_program(text)
