@@ -64,6 +64,11 @@ int dpia_memcpy2d_htod(int device, uint64_t dst, size_t dpitch, const void* src,
                        size_t width, size_t height, void* stream);
 int dpia_memcpy2d_dtoh(int device, void* dst, size_t dpitch, uint64_t src, size_t spitch,
                        size_t width, size_t height, void* stream);
+/* TMA descriptor (CUtensorMap, 128 bytes at out) of a row-major fp32 matrix,
+ * boxes of box_rows x box_cols, no swizzle (tools/mmtma.py experiment; no
+ * reference counterpart) */
+int dpia_tensor_map_2d_f32(void* out, uint64_t base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                           unsigned box_rows, unsigned box_cols);
 int dpia_memset(int device, uint64_t dst, int value, size_t bytes, void* stream);
 
 /* ---- execution (replaces simulate_kernel, SRC/opencl.py:397-472) ------- */

@@ -38,6 +38,7 @@ DPIA_DRIVER_FUNCS(DPIA_DECL)
 // optional: without it, dpia_launch_pdl degrades to an ordinary launch (the
 // kernels' griddepcontrol.wait is then a no-op and ordering is the stream's)
 decltype(&::cuLaunchKernelEx) cuLaunchKernelEx = nullptr;
+decltype(&::cuTensorMapEncodeTiled) cuTensorMapEncodeTiled = nullptr;
 }  // namespace drv
 
 namespace {
@@ -67,6 +68,8 @@ int load_driver() {
 #undef DPIA_LOAD
   drv::cuLaunchKernelEx =
       reinterpret_cast<decltype(drv::cuLaunchKernelEx)>(dlsym(g_libcuda, DPIA_STR(cuLaunchKernelEx)));
+  drv::cuTensorMapEncodeTiled = reinterpret_cast<decltype(drv::cuTensorMapEncodeTiled)>(
+      dlsym(g_libcuda, DPIA_STR(cuTensorMapEncodeTiled)));
   return 0;
 }
 
@@ -435,6 +438,24 @@ int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsign
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   CU(drv::cuLaunchKernelEx(&cfg, static_cast<CUfunction>(function), args, nullptr));
+  return 0;
+}
+
+// TMA descriptor of a row-major fp32 matrix (rows x cols, row pitch in
+// bytes) read in boxes of box_rows x box_cols, no swizzle, into the 128-byte
+// CUtensorMap at `out` (passed to kernels by value).
+int dpia_tensor_map_2d_f32(void* out, uint64_t base, uint64_t rows, uint64_t cols, uint64_t pitch,
+                           unsigned box_rows, unsigned box_cols) {
+  if (int e = load_driver()) return e;
+  if (!drv::cuTensorMapEncodeTiled) return fail(-1, "CUDA driver lacks cuTensorMapEncodeTiled");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CU(drv::cuTensorMapEncodeTiled(static_cast<CUtensorMap*>(out), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                 reinterpret_cast<void*>(base), dims, strides, box, estr,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   return 0;
 }
 

@@ -51,6 +51,7 @@ _PROTOS = {
                          C.POINTER(_vp), _vp]),
     "dpia_launch_pdl": (_i, [_vp, _i, C.c_uint, C.c_uint, C.c_uint, C.c_uint, C.c_uint,
                              C.POINTER(_vp), _vp]),
+    "dpia_tensor_map_2d_f32": (_i, [_vp, _u64, _u64, _u64, _u64, C.c_uint, C.c_uint]),
     "dpia_stream_create": (_i, [_i, C.POINTER(_vp)]),
     "dpia_stream_destroy": (_i, [_vp]),
     "dpia_stream_sync": (_i, [_vp]),
