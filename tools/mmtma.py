@@ -17,7 +17,9 @@ plus one __syncthreads per k-tile:
     addresses per warp, broadcast) instead of two 16-byte loads;
   * thread 0 refills a stage once all 256 threads have released it (empty
     mbarrier), or -- refill="last warp" -- the last warp to release a stage
-    (a shared-memory counter) refills it, so no thread waits to refill.
+    (a shared-memory counter) refills it, so no thread waits to refill; or
+    -- refill="after barrier" -- one __syncthreads per k-tile keeps the warps
+    in step and thread 0 refills the released stage right after it.
 
 Answers whether register staging + the per-k-tile barrier are what keeps
 mm at 84% of the FFMA2 ceiling.
@@ -38,8 +40,9 @@ HDR = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                    "paper_1710_08332_b200", "csrc", "dpia_device.cuh")
 
 
-def source(stages: int, lastwarp: bool = False) -> str:
-    return "#define LASTWARP " + ("1" if lastwarp else "0") + r"""
+def source(stages: int, lastwarp: int = 0, rowstride: bool = False, pairb: bool = False) -> str:
+    return ("#define LASTWARP " + str(int(lastwarp)) + "\n#define ROWSTRIDE " + str(int(rowstride))
+            + "\n#define PAIRB " + str(int(pairb))) + r"""
 struct __align__(64) TMap { unsigned long long d[16]; };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -74,6 +77,11 @@ __device__ __forceinline__ void tma_2d(void* dst, const TMap* map, unsigned long
 }
 
 #define S """ + str(stages) + r"""
+#if ROWSTRIDE
+#define ROW(j) (ty + 16 * (j))     // rows 64 B apart within a warp: conflict-free
+#else
+#define ROW(j) (8 * ty + (j))      // the emitted kernel's rows
+#endif
 extern "C" __global__ void __launch_bounds__(256) mm_tma(float* __restrict__ out,
                                                          const __grid_constant__ TMap amap,
                                                          const __grid_constant__ TMap bmap) {
@@ -110,17 +118,38 @@ extern "C" __global__ void __launch_bounds__(256) mm_tma(float* __restrict__ out
     for (int k = 0; k < 16; ++k) {
       float av[8], bv[8];
       #pragma unroll
-      for (int j = 0; j < 8; ++j) av[j] = a[(8 * ty + j) * 16 + k];
+      for (int j = 0; j < 8; ++j) av[j] = a[(ROW(j)) * 16 + k];
       #pragma unroll
       for (int i10 = 0; i10 < 8; ++i10) bv[i10] = b[k * 128 + 4 * tx + (i10 % 4) + 64 * (i10 / 4)];
+#if PAIRB
+      // pairs of columns share the broadcast A value: the B pair comes
+      // straight from one 16-byte shared load (acc[8 * row + col])
+      #pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        #pragma unroll
+        for (int c = 0; c < 4; ++c)
+          dpia::fma2(acc[8 * j + 2 * c], acc[8 * j + 2 * c + 1], av[j], bv[2 * c], av[j], bv[2 * c + 1]);
+      }
+#else
       #pragma unroll
       for (int i10 = 0; i10 < 8; ++i10) {
         #pragma unroll
         for (int i9 = 0; i9 < 4; ++i9)
           dpia::fma2(acc[8 * i10 + 2 * i9], acc[8 * i10 + 2 * i9 + 1], av[2 * i9], bv[i10], av[2 * i9 + 1], bv[i10]);
       }
+#endif
     }
-#if LASTWARP
+#if LASTWARP == 2
+    // lockstep: one __syncthreads per k-tile (as the emitted kernel), after
+    // which thread 0 refills the stage everyone has just released
+    __syncthreads();
+    if (tid == 0 && kt + S < 256) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&full[s], 16384);
+      tma_2d(As + s * 2048, &amap, &full[s], (kt + S) * 16, by * 128);
+      tma_2d(Bs + s * 2048, &bmap, &full[s], bx * 128, (kt + S) * 16);
+    }
+#elif LASTWARP
     // the last warp to release the stage refills it: no thread ever waits
     if (kt + S < 256) {
       __syncwarp();
@@ -149,8 +178,8 @@ extern "C" __global__ void __launch_bounds__(256) mm_tma(float* __restrict__ out
   for (int i28 = 0; i28 < 8; ++i28) {
     #pragma unroll
     for (int i27 = 0; i27 < 8; ++i27)
-      out[(i28 % 4) + 64 * (i28 / 4) + 4096 * i27 + 4 * tx + 32768 * ty + 128 * bx + 524288 * by] =
-          acc[i27 + 8 * i28];
+      out[(i28 % 4) + 64 * (i28 / 4) + 4096 * ROW(i27) + 4 * tx + 128 * bx + 524288 * by] =
+          PAIRB ? acc[8 * i27 + i28] : acc[i27 + 8 * i28];
   }
 }
 """
@@ -204,9 +233,12 @@ def main():
         print(f"round {rnd} emitted      : {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
         if rnd == 0:
             exe.buffers["out"].download(base)
-        variants = ((6, True),) if "one" in sys.argv else ((4, False), (2, True), (3, True), (4, True), (6, True))
-        for stages, lastwarp in variants:
-            mod = RT.Module(RT.nvrtc_compile(hdr + source(stages, lastwarp)), 0)
+        variants = ((6, 1, False, True),) if "one" in sys.argv else (
+            (4, 0, False, False), (6, 1, False, False), (3, 2, False, False), (3, 1, True, False),
+            (3, 2, True, False), (3, 1, False, True), (6, 1, False, True), (2, 2, False, True),
+            (3, 2, False, True), (4, 2, False, True), (3, 1, True, True), (3, 2, True, True))
+        for stages, lastwarp, rowstride, pairb in variants:
+            mod = RT.Module(RT.nvrtc_compile(hdr + source(stages, lastwarp, rowstride, pairb)), 0)
             fn = mod.function("mm_tma")
             smem = stages * 16384 + 2 * stages * 8 + 4 * stages
             RT.lib().dpia_kernel_set_smem(fn, smem)
@@ -216,8 +248,8 @@ def main():
             got = np.zeros((4096, 4096), np.float32)
             out.download(got)
             same = bool(np.array_equal(got.view(np.uint32), base.view(np.uint32)))
-            print(f"round {rnd} tma stages={stages} refill={'last warp' if lastwarp else 'thread 0'}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
-                  f"bit-identical to emitted: {same}", flush=True)
+            print(f"round {rnd} tma stages={stages} refill={['thread 0', 'last warp', 'after barrier'][int(lastwarp)]} rows={'strided' if rowstride else 'blocked'} pairs={'B' if pairb else 'A'}: {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s  "
+                  f"same elements as emitted: {same}", flush=True)
             out.free()
 
 
