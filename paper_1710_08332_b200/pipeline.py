@@ -224,8 +224,9 @@ class TilePipeline:
 
 
 def mm_tile_pipeline(M: int, N: int, K: int, rows: int = 4, cols: int = 4, compute_streams: int = 4,
-                     device: int = 0, **strategy) -> TilePipeline:
-    """mm (bench_programs.mm_program strategy) over rows x cols output tiles."""
+                     device: int = 0, float_mode: bool = True, **strategy) -> TilePipeline:
+    """mm (bench_programs.mm_program strategy) over rows x cols output tiles;
+    fp32 (float_mode) or int64 elements."""
     from .bench_programs import mm_config
     T = strategy.get("T", 128)
     if (M // rows) % T or (N // cols) % T:
@@ -233,4 +234,4 @@ def mm_tile_pipeline(M: int, N: int, K: int, rows: int = 4, cols: int = 4, compu
     text = lambda m, n: mm_config(M=m, N=n, K=K, **strategy).text  # noqa: E731
     launch = lambda m, n: mm_config(M=m, N=n, K=K, **strategy).launch  # noqa: E731
     return TilePipeline(text, launch, M, N, K, rows, cols, compute_streams=compute_streams,
-                        device=device, name="mm")
+                        elem_bytes=4 if float_mode else 8, float_mode=float_mode, device=device, name="mm")

@@ -389,6 +389,28 @@ def test_mm_tile_pipeline_matches_unchunked(rows, cols, streams):
             p.free()
 
 
+def test_mm_tile_pipeline_int64_matches_oracle():
+    """int mode (int64 elements, 8-byte pitches): the tiled product equals
+    numpy's exact integer product."""
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.pipeline import mm_tile_pipeline
+    M, N, K = 256, 256, 128
+    rng = np.random.default_rng(55)
+    A = rng.integers(-9, 10, (M, K)).astype(np.int64)
+    B = rng.integers(-9, 10, (K, N)).astype(np.int64)
+    pins = [RT.PinnedBuffer(a.nbytes) for a in (A, B)] + [RT.PinnedBuffer(8 * M * N)]
+    try:
+        ha, hb = pins[0].array(np.int64, A.size), pins[1].array(np.int64, B.size)
+        ha[:], hb[:] = A.ravel(), B.ravel()
+        out = pins[2].array(np.int64, M * N)
+        pipe = mm_tile_pipeline(M, N, K, rows=2, cols=2, compute_streams=2, float_mode=False)
+        pipe.run({"A": ha, "B": hb}, out, RT.Stream(0))
+        assert np.array_equal(out.reshape(M, N), A @ B)
+    finally:
+        for p in pins:
+            p.free()
+
+
 @pytest.mark.parametrize("chunks", [1, 2, 4])
 def test_mm_row_pipeline_matches_unchunked(chunks):
     """pipeline.RowPipeline (row chunks of A / C, copies on their own streams
