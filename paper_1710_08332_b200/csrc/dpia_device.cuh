@@ -182,46 +182,82 @@ __device__ __forceinline__ bool grid_arrive(unsigned int* counter, int tid, bool
   return *flag;
 }
 
-// Cross-GPU sum of n scalars, run by one thread of the last block of every
-// rank after the rank-local result is in out[0..n).  boxes[p] is rank p's
-// mailbox (mapped into this device through CUDA IPC / NVLink P2P): two
-// parities x world x n slots of 16 bytes {value (8 B), epoch (4 B), pad}.
+// Cross-GPU sum of n scalars, run by warp 0 (lanes tid < min(32, nthreads))
+// of the last block of every rank after the rank-local result is in
+// out[0..n).  boxes[p] is rank p's mailbox (mapped into this device through
+// CUDA IPC / NVLink P2P): two parities x world x n slots of 16 bytes.
 // Launch e uses parity e & 1, so a rank that has already moved on to launch
 // e+1 never overwrites a slot another rank is still reading for launch e.
-// The value is published before its epoch with a system-scope release store
-// and read after a system-scope acquire load, so every rank sees every value
-// and sums them in the same (rank) order: the result is identical on all
-// ranks.  A rank that waits longer than ~4e9 cycles for a peer gives up and
-// raises the mailbox's error word (the host checks it) instead of hanging.
+//
+// Publish: lane l writes the slots of ranks l, l+32, ... in parallel.  A
+// 4-byte value travels with its epoch in ONE single-copy-atomic 64-bit word
+// {value bits, epoch} (no ordering needed between them); an 8-byte value is
+// stored first and its epoch (offset 8) after it with a system-scope
+// release.  One system-scope fence per lane (world > 1) then pushes the
+// stores out, so
+// the exchange costs about one NVLink round trip whatever the world size
+// (a single thread publishing rank by rank paid one release per peer).
+// Gather: lane q polls rank q's slot in this rank's mailbox (relaxed /
+// acquire, system scope); the values meet in lane order through shuffles, so
+// every rank sums them in the same rank order and holds the identical total.
+// A lane that waits longer than ~4e9 cycles raises the mailbox's error word
+// (the host checks it) instead of hanging.
 template <class T>
 __device__ void peer_sum(T* out, int n, const unsigned long long* boxes, int rank, int world,
-                         unsigned int epoch) {
+                         unsigned int epoch, int lane, int nthreads) {
+  const int nl = nthreads < 32 ? nthreads : 32;
+  const unsigned mask = nl == 32 ? 0xffffffffu : ((1u << nl) - 1u);
   const int par = static_cast<int>(epoch & 1u);
-  for (int p = 0; p < world; ++p) {
+  for (int p = lane; p < world; p += nl) {
     char* base = reinterpret_cast<char*>(boxes[p]);
     for (int k = 0; k < n; ++k) {
       char* slot = base + (static_cast<size_t>((par * world + rank) * n + k) << 4);
-      *reinterpret_cast<volatile T*>(slot) = out[k];
-      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot + 8), "r"(epoch) : "memory");
+      if constexpr (sizeof(T) == 4) {
+        const unsigned int bits = *reinterpret_cast<const unsigned int*>(&out[k]);
+        const unsigned long long w = (static_cast<unsigned long long>(epoch) << 32) | bits;
+        asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(slot), "l"(w) : "memory");
+      } else {
+        *reinterpret_cast<volatile T*>(slot) = out[k];
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(slot + 8), "r"(epoch) : "memory");
+      }
     }
   }
+  // push the relaxed words out to the peers (one fence per lane, overlapped);
+  // a lone rank reads back its own store in program order and needs none
+  if (sizeof(T) == 4 && world > 1) __threadfence_system();
   char* mine = reinterpret_cast<char*>(boxes[rank]);
   unsigned int* err = reinterpret_cast<unsigned int*>(mine + (static_cast<size_t>(2 * world * n) << 4));
   for (int k = 0; k < n; ++k) {
     T acc = T(0);
-    for (int q = 0; q < world; ++q) {
-      char* slot = mine + (static_cast<size_t>((par * world + q) * n + k) << 4);
-      unsigned int e;
-      const long long t0 = clock64();
-      for (;;) {
-        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(e) : "l"(slot + 8) : "memory");
-        if (e == epoch) break;
-        if (clock64() - t0 > 4000000000LL) { *err = 1u; break; }
+    for (int q0 = 0; q0 < world; q0 += nl) {
+      const int q = q0 + lane;
+      T v = T(0);
+      if (q < world) {
+        char* slot = mine + (static_cast<size_t>((par * world + q) * n + k) << 4);
+        const long long t0 = clock64();
+        for (;;) {
+          if constexpr (sizeof(T) == 4) {
+            unsigned long long w;
+            asm volatile("ld.relaxed.sys.global.b64 %0, [%1];" : "=l"(w) : "l"(slot) : "memory");
+            if (static_cast<unsigned int>(w >> 32) == epoch) {
+              const unsigned int bits = static_cast<unsigned int>(w);
+              v = *reinterpret_cast<const T*>(&bits);
+              break;
+            }
+          } else {
+            unsigned int e;
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(e) : "l"(slot + 8) : "memory");
+            if (e == epoch) { v = *reinterpret_cast<volatile T*>(slot); break; }
+          }
+          if (clock64() - t0 > 4000000000LL) { *err = 1u; break; }
+        }
       }
-      const T v = *reinterpret_cast<volatile T*>(slot);
-      acc = q == 0 ? v : acc + v;
+      for (int j = 0; j < nl && q0 + j < world; ++j) {
+        const T vj = __shfl_sync(mask, v, j);
+        acc = (q0 + j == 0) ? vj : acc + vj;
+      }
     }
-    out[k] = acc;
+    if (lane == 0) out[k] = acc;
   }
 }
 

@@ -1705,9 +1705,9 @@ class ProgramEmitter:
                 nsc = shape_of(od, self.sigma, 4 if self.scalar == "float" else 8)[0] \
                     // (4 if self.scalar == "float" else 8)
                 ke.line("__syncthreads();")
-                ke.line(f"if (dpia_tid == 0) dpia::peer_sum<{self.scalar}>("
+                ke.line(f"if (dpia_tid < 32) dpia::peer_sum<{self.scalar}>("
                         f"reinterpret_cast<{self.scalar}*>({on}), {nsc}, dpia_peer_boxes, dpia_rank, "
-                        "dpia_world, dpia_epoch);")
+                        "dpia_world, dpia_epoch, dpia_tid, dpia_nthreads);")
             if grid is not None:
                 ke.line("dpia::grid_reset(dpia_counter, dpia_tid);")
                 ke.close()

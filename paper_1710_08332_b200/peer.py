@@ -11,8 +11,10 @@ order (`dpia::peer_sum` in csrc/dpia_device.cuh).  Every rank therefore ends
 with the same, deterministically ordered total, one kernel per step, no
 collective launch.
 
-Mailbox of one rank: 2 parities x world x n slots of 16 bytes {value, epoch}
-plus a 16-byte error word.  Launch e writes parity e & 1 with epoch e (epochs
+Mailbox of one rank: 2 parities x world x n slots of 16 bytes (a 4-byte value
+and its epoch packed in the first 8 bytes; an 8-byte value at offset 0 with
+its epoch at offset 8) plus a 16-byte error word.  Warp 0 serves the peers in
+parallel, one lane per peer.  Launch e writes parity e & 1 with epoch e (epochs
 start at 1; the mailbox is zeroed), so ranks may drift by one launch without
 overwriting a slot that a slower rank still has to read.
 
