@@ -1,0 +1,255 @@
+"""Unit behaviour of the re-implemented front end, one property per test, in
+the shape of the reference's own unit suites (TST/test_parser.py,
+TST/test_nat.py, TST/test_checker.py, TST/test_translate.py,
+TST/test_lower.py): the same API names, the same error classes, the same
+structural outcomes -- on this repository's own example programs (CPU)."""
+import pytest
+from hypothesis import given, settings
+from hypothesis import strategies as st
+
+from paper_1710_08332_b200.checker import DpiaTypeError, type_check
+from paper_1710_08332_b200.dtypes import (AccT, Array, CommT, ExpT, Num, ProdT, Vector, is_passive,
+                                          var_t)
+from paper_1710_08332_b200.pretty import pretty_print
+from paper_1710_08332_b200.reader import ElabError, ParseError, parse, parse_phrase
+from paper_1710_08332_b200.signatures import MAP_FAMILY, MAPI_FAMILY, PARFOR_FAMILY
+from paper_1710_08332_b200.sizes import (nat, nat_divide, nat_equal, nat_eval, nat_free_vars,
+                                         nat_normalize, nat_str)
+from paper_1710_08332_b200.stage1 import translate_program
+from paper_1710_08332_b200.stage2 import is_purely_imperative, stage2
+from paper_1710_08332_b200.terms import Prim, alpha_equal, subtree_iter
+
+SAXPY = """
+(param a (exp (array 16 num)))
+(param b (exp (array 16 num)))
+(map (lam p (+ (* 2 (fst p)) (snd p))) (zip a b))
+"""
+NORM2 = """
+(param v (exp (array 16 num)))
+(reduce (+) 0 (map (lam x (* x x)) v))
+"""
+
+
+# ------------------------------------------------------------------ reader
+
+def test_reader_types_the_body():
+    sp = parse(SAXPY)
+    assert [n for n, _ in sp.params] == ["a", "b"]
+    assert sp.body_type == ExpT(Array(nat(16), Num()))
+
+
+def test_reader_skips_comments_anywhere():
+    assert parse(";; head\n" + NORM2 + ";; tail\n").body_type == ExpT(Num())
+
+
+def test_reader_size_parameters():
+    sp = parse("(nat k)\n(param v (exp (array (* 2 k) num)))\n(map (lam x (* x 3)) v)")
+    assert sp.nat_params == ["k"]
+    assert isinstance(sp.body_type.data, Array)
+
+
+def test_reader_vector_types():
+    assert parse("(param w (exp (vec 2)))\n(* w w)").body_type == ExpT(Vector(2))
+    with pytest.raises(ParseError):
+        parse("(param w (exp (vec 6)))\nw")
+
+
+@pytest.mark.parametrize("text", [
+    "(param v (exp (array 4 num))\nv",                       # unbalanced
+    "(param v (exp num))\n(param v (exp num))\nv",           # duplicate parameter
+    "(param v (exp num))",                                   # no body
+])
+def test_reader_syntax_errors_are_not_type_errors(text):
+    with pytest.raises(ParseError) as ei:
+        parse(text)
+    assert not isinstance(ei.value, ElabError)
+
+
+@pytest.mark.parametrize("text", [
+    "(param v (exp (array 4 num)))\n(* v 2)",                # arithmetic on an array
+    "(param v (exp num))\n(snd v)",                          # projection of a scalar
+    "(param v (exp num))\nw",                                # unbound identifier
+    "(param v (exp (array 6 num)))\n(split 4 v)",            # 6 is not a multiple of 4
+    "(param v (exp (array 4 num)))\n(param w (exp (array 2 num)))\n(zip v w)",
+    "(param v (exp (array 4 num)))\n(idx v 7)",              # literal index out of bounds
+])
+def test_reader_type_errors_are_elab_errors(text):
+    with pytest.raises(ElabError):
+        parse(text)
+
+
+def test_reader_three_argument_split_is_symbolic():
+    sp = parse("(nat k)\n(param v (exp (array (* 8 k) num)))\n(split 8 k v)")
+    t = sp.body_type.data
+    assert isinstance(t.elem, Array) and t.elem.size == nat(8) and nat_equal(t.size, nat("k"))
+
+
+def test_reader_pairs():
+    assert parse("(param v (exp num))\n(snd (pair 1 v))").body_type == ExpT(Num())
+
+
+@pytest.mark.parametrize("text", [SAXPY, NORM2,
+                                  "(param v (exp (array 8 num)))\n"
+                                  "(asScalar4 (map (lam w (* w w)) (asVector4 v)))"])
+def test_reader_pretty_print_round_trip(text):
+    sp = parse(text)
+    body, t = parse_phrase(pretty_print(sp.body), dict(sp.params))
+    assert alpha_equal(body, sp.body) and t == sp.body_type
+
+
+# ------------------------------------------------------------------ sizes
+
+VARS = ("n", "m", "k")
+
+
+def _terms():
+    leaf = st.one_of(st.integers(0, 7).map(nat), st.sampled_from(VARS).map(nat))
+    return st.recursive(leaf, lambda sub: st.tuples(sub, sub, st.booleans()).map(
+        lambda t: t[0] + t[1] if t[2] else t[0] * t[1]), max_leaves=8)
+
+
+@settings(max_examples=60, deadline=None)
+@given(_terms(), st.lists(st.integers(0, 40), min_size=3, max_size=3))
+def test_sizes_canonical_form_keeps_the_value(e, vals):
+    sigma = dict(zip(VARS, vals))
+    assert nat_eval(nat_normalize(e), sigma) == nat_eval(e, sigma)
+    assert nat_normalize(nat_normalize(e)) == nat_normalize(e)
+    assert nat_str(e) == nat_str(nat_normalize(e))
+
+
+def test_sizes_equality_is_semantic():
+    n, m, k = nat("n"), nat("m"), nat("k")
+    assert nat_equal((n + k) * m, n * m + m * k)
+    assert not nat_equal(n * m, n + m)
+
+
+def test_sizes_free_variables_and_unbound_evaluation():
+    assert nat_free_vars(nat("k") * (nat("n") + 3)) == {"k", "n"}
+    with pytest.raises(KeyError):
+        nat_eval(nat("z"), {"n": 1})
+
+
+def test_sizes_exact_division():
+    n, m = nat("n"), nat("m")
+    assert nat_equal(nat_divide(nat(6) * n, 6), n)
+    assert nat_divide(n + 1, 2) is None
+    assert nat_divide(nat(20), nat(5)) == nat(4)
+    assert nat_equal(nat_divide(n * m * 2, m), n * 2)
+
+
+# ------------------------------------------------------------------ checker
+
+def _check(text):
+    sp = parse(text)
+    return type_check(sp.body, delta=sp.delta, pi=sp.pi, gamma=sp.gamma)
+
+
+def test_checker_expression_parameters_are_passive():
+    t, uses = _check(NORM2)
+    assert t == ExpT(Num()) and uses.active == set() and uses.passive == {"v"}
+
+
+def test_checker_parfor_writes_through_its_own_acceptor():
+    t, uses = _check("(param y (acc (array 8 num)))\n(param s (exp num))\n"
+                     "(parfor y (lam (j (exp (idx 8))) (lam (o (acc num)) (:= o (+ s 1)))))")
+    assert isinstance(t, CommT) and uses.active == {"y"}
+
+
+def test_checker_rejects_a_captured_acceptor_in_parfor():
+    with pytest.raises(DpiaTypeError) as ei:
+        _check("(param y (acc (array 8 num)))\n(param c (acc num))\n"
+               "(parfor y (lam (j (exp (idx 8))) (lam (o (acc num)) (:= c 0))))")
+    assert "passive" in str(ei.value) and "'c'" in str(ei.value)
+
+
+def test_checker_sequencing_may_share_an_acceptor():
+    t, uses = _check("(param c (acc num))\n(seq (:= c 3) (:= c 4))")
+    assert isinstance(t, CommT) and uses.active == {"c"}
+
+
+def test_checker_new_scopes_its_variable():
+    t, uses = _check("(param r (acc num))\n"
+                     "(new num (lam t (seq (:= (proj1 t) 5) (:= r (proj2 t)))))")
+    assert isinstance(t, CommT) and uses.active == {"r"}
+
+
+def test_checker_zones_and_passivity():
+    sp = parse("(param v (exp num))\nv")
+    with pytest.raises(DpiaTypeError):
+        type_check(sp.body, pi={"v": ExpT(Num())}, gamma={"v": ExpT(Num())})
+    body, _ = parse_phrase("(:= r 2)", {"r": AccT(Num())})
+    with pytest.raises(DpiaTypeError):
+        type_check(body)
+    with pytest.raises(DpiaTypeError) as ei:
+        type_check(body, pi={"r": AccT(Num())})
+    assert "passive" in str(ei.value)
+    assert is_passive(ExpT(Num())) and is_passive(ProdT(ExpT(Num()), ExpT(Num())))
+    assert not is_passive(AccT(Num())) and not is_passive(CommT()) and not is_passive(var_t(Num()))
+
+
+# ------------------------------------------------------------------ Stage I / Stage II
+
+def _count(p, names):
+    return sum(1 for s in subtree_iter(p) if isinstance(s, Prim) and s.name in names)
+
+
+def _stage1(text, **kw):
+    sp = parse(text)
+    return sp, translate_program(sp.body, sp.body_type.data, out="out", **kw)
+
+
+def _recheck(sp, s1):
+    gamma = dict(sp.gamma)
+    gamma["out"] = AccT(sp.body_type.data)
+    return type_check(s1, delta=sp.delta, pi=sp.pi, gamma=gamma)[0]
+
+
+HIER = ("(param v (exp (array 16 num)))\n"
+        "(join (mapWorkgroup (lam (c (exp (array 8 num))) (mapLocal (lam x (* x 5)) c)) (split 8 v)))")
+
+
+def test_stage1_is_a_well_typed_command():
+    for text in (SAXPY, NORM2, HIER):
+        sp, s1 = _stage1(text)
+        assert isinstance(_recheck(sp, s1), CommT)
+
+
+def test_stage1_one_mapi_per_map_and_one_reducei_per_reduce():
+    _, s1 = _stage1(SAXPY)
+    assert _count(s1, {"mapI"}) == 1 and _count(s1, MAP_FAMILY) == 0
+    _, s1 = _stage1(NORM2)
+    assert _count(s1, {"reduceI"}) == 1
+
+
+def test_stage1_keeps_the_hierarchy():
+    _, s1 = _stage1(HIER)
+    assert _count(s1, {"mapIWorkgroup"}) == 1 and _count(s1, {"mapILocal"}) == 1
+
+
+def test_stage1_temporaries():
+    _, s1 = _stage1("(param v (exp num))\n(* v 4)")
+    assert _count(s1, {"new"}) == 0 and _count(s1, {":="}) == 1
+    _, s1 = _stage1(NORM2)
+    assert _count(s1, {"new"}) >= 1                      # the map feeding reduce is materialised
+    _, s1 = _stage1(NORM2, default_space="global")
+    assert _count(s1, {"new"}) == 0 and _count(s1, {"newGlobal"}) >= 1
+
+
+def test_stage2_loops():
+    _, s1 = _stage1(SAXPY)
+    s2 = stage2(s1)
+    assert _count(s2, MAPI_FAMILY) == 0 and _count(s2, {"parfor"}) == 1
+    _, s1 = _stage1("(param v (exp (array 16 num)))\n(mapSeq (lam x (+ x 2)) v)")
+    s2 = stage2(s1)
+    assert _count(s2, PARFOR_FAMILY) == 0 and _count(s2, {"for"}) == 1
+    s2 = stage2(_stage1(HIER)[1])
+    assert _count(s2, {"parforWorkgroup"}) == 1 and _count(s2, {"parforLocal"}) == 1
+
+
+def test_stage2_accumulators_and_purity():
+    s2 = stage2(_stage1(NORM2)[1])
+    assert _count(s2, {"reduceI"}) == 0 and _count(s2, {"for"}) >= 1 and _count(s2, {"new"}) >= 1
+    assert is_purely_imperative(s2)
+    s2 = stage2(_stage1(NORM2, default_space="global")[1], accum_space="private")
+    assert _count(s2, {"new"}) == 0 and _count(s2, {"newPrivate"}) >= 1
+    assert is_purely_imperative(s2)
