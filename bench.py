@@ -333,6 +333,27 @@ def e2e_pipelined_mm(inputs, stream, steps, chunks=4, tiles=None):
     return statistics.mean(times[1:]), A.nbytes + B.nbytes, 4 * M * N
 
 
+def e2e_pipelined_scal(inputs, stream, steps, chunks=8):
+    from paper_1710_08332_b200.pipeline import scal_pipeline
+    xs, alpha = inputs["xs"], inputs["alpha"]
+    N = xs.size
+    pins = [RT.PinnedBuffer(16), RT.PinnedBuffer(xs.nbytes), RT.PinnedBuffer(xs.nbytes)]
+    ha, hx, out = pins[0].array(np.float32, 4), pins[1].array(np.float32, N), pins[2].array(np.float32, N)
+    ha[:], hx[:] = alpha, xs
+    pipe = scal_pipeline(N, chunks=chunks)
+    times = []
+    for _ in range(steps + 1):
+        e0, e1 = RT.Event(0), RT.Event(0)
+        e0.record(stream)
+        pipe.run({"alpha": ha, "xs": hx}, out, stream)
+        e1.record(stream)
+        stream.sync()
+        times.append(e0.elapsed_ms(e1))
+    for p in pins:
+        p.free()
+    return statistics.mean(times[1:]), 16 + xs.nbytes, xs.nbytes
+
+
 # ------------------------------------------------------------ CPU legs
 
 def ref_lib():
@@ -581,6 +602,17 @@ def main():
                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                           "ms_per_step": round(e2e_ms, 4),
                           "path": "Executable.run (public API): pinned H2D + kernels + D2H + stream sync"}
+        if with_e2e and workload == "scal" and world == 1:
+            # read + write: the public row pipeline overlaps the H2D of block
+            # i+1 and the D2H of block i-1 with block i's kernel
+            pms, ph2d, pd2h = e2e_pipelined_scal(inputs, stream, min(steps, 5))
+            res["e2e_unpipelined"] = res.get("e2e")
+            res["e2e"] = {"value": round(cfg.bytes / (pms * 1e-3) / 1e9, 3), "unit": "GB/s",
+                          "h2d_bytes_per_step": ph2d, "d2h_bytes_per_step": pd2h,
+                          "ms_per_step": round(pms, 4),
+                          "path": "pipeline.scal_pipeline(8 blocks).run (public API): pinned H2D of x "
+                                  "blocks, block kernels, D2H of y blocks, overlapped on three streams "
+                                  "(PCIe carries both directions at once), stream sync"}
         if with_e2e and workload == "mm" and world == 1:
             # compute-bound: the public row pipeline overlaps the copies with
             # the chunk kernels (pipeline.mm_pipeline); the plain

@@ -18,7 +18,7 @@ from .cuda.hierarchy import (HoistedBuffer, WorkItemRace, check_work_item_races,
 from .api import Program, compile_program, executable, run_program_cuda  # noqa: F401
 from .checker import DpiaTypeError, type_check  # noqa: F401
 from .pretty import pretty_print  # noqa: F401
-from .pipeline import RowPipeline, TilePipeline, mm_pipeline, mm_tile_pipeline  # noqa: F401
+from .pipeline import RowPipeline, TilePipeline, mm_pipeline, mm_tile_pipeline, scal_pipeline  # noqa: F401
 from .peer import PeerGroup  # noqa: F401
 
 __all__ = ["parse", "parse_phrase", "translate_program", "stage2", "emit_cuda", "run_kernel",
@@ -26,5 +26,5 @@ __all__ = ["parse", "parse_phrase", "translate_program", "stage2", "emit_cuda", 
            "ElabError", "SourceProgram", "Program", "Executable", "CudaSignature",
            "hoist_allocations", "lint_hierarchy", "cuda_legal", "HoistedBuffer",
            "WorkItemRace", "check_work_item_races", "RowPipeline", "mm_pipeline", "TilePipeline",
-           "mm_tile_pipeline", "PeerGroup",
+           "mm_tile_pipeline", "scal_pipeline", "PeerGroup",
            "type_check", "DpiaTypeError", "pretty_print"]

@@ -29,15 +29,19 @@ from .api import compile_program, executable
 class RowPipeline:
     def __init__(self, text_for_rows: Callable[[int], str], launch_for_rows: Callable[[int], object],
                  rows: int, chunks: int, row_inputs: Dict[str, int], shared_inputs: Dict[str, int],
-                 out_bytes: int, float_mode: bool = True, device: int = 0, name: str = "pipe"):
-        """text_for_rows(r) -> program text for r rows; row_inputs / shared
-        inputs: name -> total bytes; out_bytes: total bytes of the output."""
+                 out_bytes: int, float_mode: bool = True, device: int = 0, name: str = "pipe",
+                 sigma_for_rows: Optional[Callable[[int], Dict[str, int]]] = None):
+        """text_for_rows(r) -> program text for r rows (sigma_for_rows(r) ->
+        its size parameters, if it has any); row_inputs / shared inputs:
+        name -> total bytes; out_bytes: total bytes of the output."""
         if rows % chunks:
             raise ValueError(f"{rows} rows do not split into {chunks} chunks")
         self.rows, self.chunks, self.device = rows, chunks, device
         self.crows = rows // chunks
         prog = compile_program(text_for_rows(self.crows), name=name)
-        self.exe = executable(prog, launch_for_rows(self.crows), {}, float_mode=float_mode, device=device)
+        sigma = sigma_for_rows(self.crows) if sigma_for_rows else {}
+        self.exe = executable(prog, launch_for_rows(self.crows), sigma, float_mode=float_mode,
+                              device=device)
         self.row_inputs, self.shared_inputs, self.out_bytes = dict(row_inputs), dict(shared_inputs), out_bytes
         self.full = {n: RT.DeviceBuffer(b, device) for n, b in {**row_inputs, "out": out_bytes}.items()}
         for n, b in shared_inputs.items():
@@ -108,6 +112,18 @@ def mm_pipeline(M: int, N: int, K: int, chunks: int = 4, device: int = 0, **stra
     launch = lambda r: mm_config(M=r, N=N, K=K, **strategy).launch  # noqa: E731
     return RowPipeline(text, launch, M, chunks, {"A": 4 * M * K}, {"B": 4 * K * N}, 4 * M * N,
                        device=device, name="mm")
+
+
+def scal_pipeline(N: int, chunks: int = 8, device: int = 0, **geometry) -> RowPipeline:
+    """scal (y = alpha * x, bench_programs.scal_program) over `chunks`
+    contiguous blocks of x / y: the H2D of block i+1 and the D2H of block
+    i-1 overlap block i's kernel, and PCIe carries both directions at once."""
+    from .bench_programs import scal_config
+    if N % (4 * chunks):
+        raise ValueError(f"{N} elements do not split into {chunks} blocks of whole vec4s")
+    cfg = lambda r: scal_config(N=r, **geometry)  # noqa: E731
+    return RowPipeline(lambda r: cfg(r).text, lambda r: cfg(r).launch, N, chunks, {"xs": 4 * N},
+                       {"alpha": 16}, 4 * N, device=device, name="scal", sigma_for_rows=lambda r: cfg(r).sigma)
 
 
 def tile_schedule(rows: int, cols: int):

@@ -389,6 +389,34 @@ def test_mm_tile_pipeline_matches_unchunked(rows, cols, streams):
             p.free()
 
 
+@pytest.mark.parametrize("chunks", [1, 2, 8])
+def test_scal_pipeline_matches_unchunked(chunks):
+    """pipeline.scal_pipeline (blocks of x / y, H2D, kernels and D2H on their
+    own streams) is bit-identical to one launch over the whole vector."""
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.bench_programs import scal_config
+    from paper_1710_08332_b200.pipeline import scal_pipeline
+    N = 1 << 16
+    xs = blas_np.seeded(N, 57, -1.0, 1.0)
+    alpha = np.full(4, 1.25, np.float32)
+    cfg = scal_config(N=N)
+    whole = np.asarray(run_program_cuda(compile_program(cfg.text), {"alpha": alpha, "xs": xs},
+                                        sigma=cfg.sigma, launch=cfg.launch, flat=True), np.float32)
+    pins = [RT.PinnedBuffer(16), RT.PinnedBuffer(4 * N), RT.PinnedBuffer(4 * N)]
+    try:
+        ha, hx, out = (pins[0].array(np.float32, 4), pins[1].array(np.float32, N),
+                       pins[2].array(np.float32, N))
+        ha[:], hx[:] = alpha, xs
+        pipe = scal_pipeline(N, chunks=chunks)
+        for _ in range(2):
+            out[:] = np.nan
+            pipe.run({"alpha": ha, "xs": hx}, out, RT.Stream(0))
+            assert np.array_equal(out, whole)
+    finally:
+        for p in pins:
+            p.free()
+
+
 def test_mm_tile_pipeline_int64_matches_oracle():
     """int mode (int64 elements, 8-byte pitches): the tiled product equals
     numpy's exact integer product."""
