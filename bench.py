@@ -594,14 +594,18 @@ def main():
                "value": value, "roofline": roof}
         if with_e2e and inputs is not None:
             e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
+            if dist is not None:   # whole job: every rank's bytes over the slowest rank's time
+                e2e_ms = float(_allreduce(dist, e2e_ms, dist.ReduceOp.MAX, local, share))
             work, unit = (cfg.flops, "GFLOP/s") if workload == "mm" else (cfg.bytes, "GB/s")
-            res["e2e"] = {"value": round(work / (e2e_ms * 1e-3) / 1e9, 3), "unit": unit,
+            res["e2e"] = {"value": round(world * work / (e2e_ms * 1e-3) / 1e9, 3), "unit": unit,
                           "h2d_link_gbs": _LINK_GBS,
                           "h2d_link_note": "pinned H2D of the same input bytes alone, measured in the "
-                                           "same run: the ceiling of a streaming e2e",
-                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                                           "same run: the ceiling of a streaming e2e (one GPU's link)",
+                          "h2d_bytes_per_step": world * h2d, "d2h_bytes_per_step": world * d2h,
                           "ms_per_step": round(e2e_ms, 4),
-                          "path": "Executable.run (public API): pinned H2D + kernels + D2H + stream sync"}
+                          "path": "Executable.run (public API): pinned H2D + kernels + D2H + stream sync"
+                                  + (f"; {world} ranks, each its own inputs over its own link, max over "
+                                     "ranks" if world > 1 else "")}
         if with_e2e and workload == "scal" and world == 1:
             # read + write: the public row pipeline overlaps the H2D of block
             # i+1 and the D2H of block i-1 with block i's kernel
