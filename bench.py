@@ -527,8 +527,11 @@ def main():
         prepare(stream)
         stream.sync()
         allreduce = None
-        if world > 1 and exe.peer is None:
-            import torch
+        reduces = workload in ("asum", "dot") or workload.startswith("scaleout")
+        if world > 1 and exe.peer is None and reduces:
+            # gemv / mm / scal shard with no collective (independent rows)
+            if args.combine != "nccl":
+                raise SystemExit("internal: a reduction without the peer combine needs --combine nccl")
             outbuf = exe.buffers["out"]
 
             def allreduce(s):  # NCCL sum of the per-rank partial, on our stream
