@@ -95,13 +95,15 @@ _FFMA_CACHE = {}
 
 
 def ffma_peak(device, stream):
-    """Measured FP32 FMA ceiling: tools/ffmapeak.py's register-only packed
-    FFMA2 kernel (measurement infrastructure, not product) at 8 CTAs/SM x 256
-    threads, mean of 10 event-timed launches after warm-up (TFLOP/s)."""
+    """(measured FP32 FMA ceiling, mm inner-loop ceiling) in TFLOP/s:
+    tools/ffmapeak.py's register-only packed FFMA2 kernel at 8 CTAs/SM x 256
+    threads, and its `mmloop` (mm's k-step from a shared tile, no staging,
+    no barrier) at 2 CTAs/SM -- measurement infrastructure, not product;
+    means of 10 event-timed launches after warm-up."""
     if device in _FFMA_CACHE:
         return _FFMA_CACHE[device]
     sys.path.insert(0, os.path.join(ROOT, "tools"))
-    from ffmapeak import ITERS, SRC
+    from ffmapeak import ITERS, SRC, mmloop
     mod = RT.Module(RT.get_cubin(SRC), device)
     fn = mod.function("ffma2")
     out = RT.DeviceBuffer(64, device)
@@ -116,9 +118,10 @@ def ffma_peak(device, stream):
         stream.sync()
         if it >= 3:
             ts.append(e0.elapsed_ms(e1))
+    inner = mmloop(mod, stream, RT.device_attribute(device, RT.ATTR_SM_COUNT), out)
     out.free()
     flops = blocks * 256 * ITERS * 16 * 2 * 2
-    _FFMA_CACHE[device] = round(flops / statistics.mean(ts) / 1e9, 2)
+    _FFMA_CACHE[device] = (round(flops / statistics.mean(ts) / 1e9, 2), round(inner, 2))
     return _FFMA_CACHE[device]
 
 
@@ -577,9 +580,13 @@ def main():
                     "unit": "TFLOP/s", "frac": round(achieved / fp32[0], 4),
                     "traffic": ncu_traffic(workload), "peak_source": fp32[1],
                     "algorithmic_flops_per_launch": cfg.flops, "kernel_ms": round(kmean, 5)}
-            meas = ffma_peak(device, stream)
+            meas, inner = ffma_peak(device, stream)
             roof["measured_ffma2_peak"] = meas
             roof["frac_of_measured_ffma2_peak"] = round(achieved / meas, 4)
+            # the strategy's own k-step (shared fragment loads + FFMA2) with
+            # no global staging and no barrier, at mm's occupancy
+            roof["inner_loop_ceiling"] = inner
+            roof["frac_of_inner_loop_ceiling"] = round(achieved / inner, 4)
         else:
             achieved = cfg.bytes / (kmean * 1e-3) / 1e9
             value = world * cfg.bytes / (mean_ms * 1e-3) / 1e9

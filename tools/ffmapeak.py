@@ -54,7 +54,68 @@ extern "C" __global__ void __launch_bounds__(256) ffma2(float* out, float a, flo
   }
   if (s == 1.2345f) out[0] = s;
 }
+
+// mm's inner loop alone: the same 16 k-steps of fragment loads from shared
+// memory (2 x LDS.128 for 8 A values, 2 x LDS.128 for 8 B values) and 32
+// FFMA2 per thread and k-step, over a tile filled once -- no global
+// staging, no barrier in the loop.  The ceiling of the LDS + FFMA2 mix at
+// mm's occupancy (256 threads, 2 CTAs per SM).
+extern "C" __global__ void __launch_bounds__(256) mmloop(float* out, float a, float b, int iters) {
+  __shared__ __align__(16) float As[16 * 128];
+  __shared__ __align__(16) float Bs[16 * 128];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  for (int i = threadIdx.x; i < 16 * 128; i += 256) { As[i] = a * i; Bs[i] = b * i; }
+  __syncthreads();
+  float acc[64];
+  #pragma unroll
+  for (int i = 0; i < 64; ++i) acc[i] = 0.0f;
+  for (int it = 0; it < iters; ++it) {
+    #pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[((8 * ty) ^ (8 * (k / 4))) + 128 * k]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[((8 * ty) ^ (8 * (k / 4))) + 128 * k + 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[((4 * tx) ^ (8 * (k / 4))) + 128 * k]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[((4 * tx) ^ (8 * (k / 4))) + 128 * k + 64]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+      #pragma unroll
+      for (int i10 = 0; i10 < 8; ++i10) {
+        #pragma unroll
+        for (int i9 = 0; i9 < 4; ++i9) {
+          unsigned long long c, x, y;
+          asm("mov.b64 %0, {%1,%2};" : "=l"(c) : "f"(acc[8 * i10 + 2 * i9]), "f"(acc[8 * i10 + 2 * i9 + 1]));
+          asm("mov.b64 %0, {%1,%2};" : "=l"(x) : "f"(av[2 * i9]), "f"(av[2 * i9 + 1]));
+          asm("mov.b64 %0, {%1,%1};" : "=l"(y) : "f"(bv[i10]));
+          asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(c) : "l"(x), "l"(y));
+          asm("mov.b64 {%0,%1}, %2;" : "=f"(acc[8 * i10 + 2 * i9]), "=f"(acc[8 * i10 + 2 * i9 + 1]) : "l"(c));
+        }
+      }
+    }
+  }
+  float s = 0.f;
+  #pragma unroll
+  for (int i = 0; i < 64; ++i) s += acc[i];
+  if (s == 1.2345f) out[0] = s;
+}
 """
+
+
+def mmloop(mod, st, sms, out):
+    """TFLOP/s of the mm inner loop alone at 2 CTAs/SM x 256 threads."""
+    fn = mod.function("mmloop")
+    blocks, iters = sms * 2, 256
+    args = [RT.C.c_uint64(out.ptr), RT.C.c_float(1e-3), RT.C.c_float(2e-3), RT.C.c_int(iters)]
+    ts = []
+    for it in range(13):
+        e0, e1 = RT.Event(0), RT.Event(0)
+        e0.record(st)
+        RT.launch(fn, 0, (blocks, 1), (256, 1), 0, args, st)
+        e1.record(st)
+        st.sync()
+        if it >= 3:
+            ts.append(e0.elapsed_ms(e1))
+    flops = blocks * 256 * iters * 16 * 64 * 2
+    return flops / statistics.mean(ts) / 1e9
 
 
 def main():
@@ -81,6 +142,8 @@ def main():
             flops = blocks * 256 * ITERS * 16 * lanes * 2
             print(f"{name:6s} {per_sm} CTAs/SM x 256: {ms * 1e3:8.1f} us  {flops / ms / 1e9:7.2f} TFLOP/s",
                   flush=True)
+    print(f"mm inner loop (shared fragments + FFMA2), 2 CTAs/SM x 256: {mmloop(mod, st, sms, out):7.2f} TFLOP/s",
+          flush=True)
 
 
 if __name__ == "__main__":
