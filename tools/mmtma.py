@@ -185,6 +185,80 @@ extern "C" __global__ void __launch_bounds__(256) mm_tma(float* __restrict__ out
 """
 
 
+def source_wide(stages: int) -> str:
+    """8 x 16 register tile, 128 threads (16 row groups x 8 column groups),
+    TMA ring refilled by the last of the 4 warps to release a stage (no CTA
+    barrier in the k-loop), FFMA2 pairing B columns against a broadcast A.
+    Thread (ty, tx) owns rows 8*ty + j and columns 4*tx + 32*q + c (q < 4,
+    c < 4): each 16-byte B load of a warp covers 128 contiguous bytes."""
+    return source(stages, 1, False, True).split("#define S ")[0] + "#define S " + str(stages) + r"""
+extern "C" __global__ void __launch_bounds__(128) mm_tma_wide(float* __restrict__ out,
+                                                              const __grid_constant__ TMap amap,
+                                                              const __grid_constant__ TMap bmap) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* As = reinterpret_cast<float*>(smem);                 // S x [128 rows][16 k]
+  float* Bs = reinterpret_cast<float*>(smem + S * 8192);      // S x [16 k][128 cols]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + S * 16384);
+  unsigned* cnt = reinterpret_cast<unsigned*>(full + S);
+  const int tid = threadIdx.x, tx = tid % 8, ty = tid / 8, bx = blockIdx.x, by = blockIdx.y;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); cnt[s] = 0u; }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_expect_tx(&full[s], 16384);
+      tma_2d(As + s * 2048, &amap, &full[s], s * 16, by * 128);
+      tma_2d(Bs + s * 2048, &bmap, &full[s], bx * 128, s * 16);
+    }
+  }
+  float acc[128];                       // acc[16 * j + c16]: row j, column slot c16
+  #pragma unroll
+  for (int i = 0; i < 128; ++i) acc[i] = 0.0f;
+  for (int kt = 0; kt < 256; ++kt) {
+    const int s = kt % S;
+    mbar_wait(&full[s], (kt / S) & 1);
+    const float* a = As + s * 2048;
+    const float* b = Bs + s * 2048;
+    #pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float av[8], bv[16];
+      #pragma unroll
+      for (int j = 0; j < 8; ++j) av[j] = a[(8 * ty + j) * 16 + k];
+      #pragma unroll
+      for (int c16 = 0; c16 < 16; ++c16) bv[c16] = b[k * 128 + 4 * tx + 32 * (c16 / 4) + (c16 % 4)];
+      #pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        #pragma unroll
+        for (int c = 0; c < 8; ++c)
+          dpia::fma2(acc[16 * j + 2 * c], acc[16 * j + 2 * c + 1], av[j], bv[2 * c], av[j], bv[2 * c + 1]);
+      }
+    }
+    if (kt + S < 256) {
+      __syncwarp();
+      if ((tid & 31) == 0) {
+        __threadfence_block();
+        if (atomicAdd(&cnt[s], 1u) == 3u) {
+          cnt[s] = 0u;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&full[s], 16384);
+          tma_2d(As + s * 2048, &amap, &full[s], (kt + S) * 16, by * 128);
+          tma_2d(Bs + s * 2048, &bmap, &full[s], bx * 128, (kt + S) * 16);
+        }
+      }
+    }
+  }
+  #pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    #pragma unroll
+    for (int c16 = 0; c16 < 16; ++c16)
+      out[4096 * (128 * by + 8 * ty + j) + 128 * bx + 4 * tx + 32 * (c16 / 4) + (c16 % 4)] = acc[16 * j + c16];
+  }
+}
+"""
+
+
 class TMap(ctypes.Structure):
     _fields_ = [("d", ctypes.c_uint64 * 16)]
 
@@ -233,6 +307,22 @@ def main():
         print(f"round {rnd} emitted      : {ms * 1e3:8.1f} us  {cfg.flops / ms / 1e9:6.2f} TFLOP/s", flush=True)
         if rnd == 0:
             exe.buffers["out"].download(base)
+        for stages in (3, 4, 6):
+            mod = RT.Module(RT.nvrtc_compile(hdr + source_wide(stages)), 0)
+            fn = mod.function("mm_tma_wide")
+            smem = stages * 16384 + 8 * stages + 4 * stages
+            RT.lib().dpia_kernel_set_smem(fn, smem)
+            out = RT.DeviceBuffer(4096 * 4096 * 4)
+            args = [RT.C.c_uint64(out.ptr), amap, bmap]
+            ms = timed(st, lambda: RT.launch(fn, 0, (32, 32), (128, 1), smem, args, st))
+            got = np.zeros((4096, 4096), np.float32)
+            out.download(got)
+            same = bool(np.array_equal(got.view(np.uint32), base.view(np.uint32)))
+            print(f"round {rnd} tma wide 8x16 x 128 threads, stages={stages}: {ms * 1e3:8.1f} us  "
+                  f"{cfg.flops / ms / 1e9:6.2f} TFLOP/s  same elements as emitted: {same}", flush=True)
+            out.free()
+        if "wide" in sys.argv:
+            continue
         variants = ((6, 1, False, True),) if "one" in sys.argv else (
             (4, 0, False, False), (6, 1, False, False), (3, 2, False, False), (3, 1, True, False),
             (3, 2, True, False), (3, 1, False, True), (6, 1, False, True), (2, 2, False, True),
