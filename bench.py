@@ -511,7 +511,9 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": cfg_line}
         if r is None:
-            line.update({"unavailable": "oracle/_ref/libref_cpu.so not built (needs /root/reference at build)"})
+            why = ("oracle/_ref/libref_cpu.so not built (needs /root/reference at build)" if ref_lib() is None
+                   else f"the reference's c-openmp path has no program for workload {args.workload!r}")
+            line.update({"unavailable": why})
         else:
             line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
                          "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
