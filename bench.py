@@ -397,6 +397,14 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         fn.argtypes = [vp, vp, vp]
         call = lambda: fn(out.ctypes.data, A.ctypes.data, x.ctypes.data)  # noqa: E731
         nbytes, sample = 4 * (8192 * 8192 + 2 * 8192), "gemv 8192x8192 fp32, full size"
+    elif workload == "scal":
+        n = (1 << 26) // 1024
+        xs = _seeded(1 << 26, 7, -1.0, 1.0)
+        ys = np.zeros(1 << 26, np.float32)
+        fn = lib.scal
+        fn.argtypes = [vp, ctypes.c_float, vp, ci]
+        call = lambda: fn(ys.ctypes.data, 1.5, xs.ctypes.data, n)  # noqa: E731
+        nbytes, sample = 8 << 26, "scal (y = alpha x) over 2^26 fp32, full size (read + write)"
     elif workload == "mm":
         A, B = _seeded((4096, 4096), 5, -1.0, 1.0), _seeded((4096, 4096), 6, -1.0, 1.0)
         Bt = np.ascontiguousarray(B.T)

@@ -21,7 +21,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 OUT = os.path.join(HERE, "_ref")
 REF_SRC = "/root/reference/pkg/src"
-PROGRAMS = ("asum_proxy", "dot", "gemv", "mm_bt")
+PROGRAMS = ("asum_proxy", "dot", "gemv", "mm_bt", "scal")
 LIB = os.path.join(OUT, "libref_cpu.so")
 
 HARNESS = r"""

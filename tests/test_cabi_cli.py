@@ -200,3 +200,37 @@ def test_bench_json_contract():
     e2e = line["e2e"]
     assert e2e["h2d_bytes_per_step"] == 4 << 26 and e2e["value"] > 0
     assert line["clocks"]["sm_max_mhz"] > 0
+
+
+def test_reference_cpu_path_computes_the_workloads():
+    """The reference's own c-openmp emissions (oracle/_ref, the CPU baseline
+    and the --impl reference arm) compute what the GPU workloads compute
+    (CPU; checked against float64 numpy, fp32 tolerance)."""
+    import ctypes
+    import numpy as np
+    lib_path = os.path.join(ROOT, "oracle", "_ref", "libref_cpu.so")
+    if not os.path.exists(lib_path):
+        pytest.skip("oracle/_ref not built")
+    lib = ctypes.CDLL(lib_path)
+    vp, ci = ctypes.c_void_p, ctypes.c_int
+    rng = np.random.default_rng(9)
+    n = 16
+    xs = rng.uniform(-1, 1, 1024 * n).astype(np.float32)
+    ys = rng.uniform(-1, 1, 1024 * n).astype(np.float32)
+    out = np.zeros(8192, np.float32)
+    lib.asum_proxy.argtypes = [vp, vp, ci]
+    lib.asum_proxy(out.ctypes.data, xs.ctypes.data, n)
+    assert abs(out[0] - xs.astype(np.float64).sum()) <= 1e-4 * np.abs(xs).sum()
+    lib.dot.argtypes = [vp, vp, vp, ci]
+    lib.dot(out.ctypes.data, xs.ctypes.data, ys.ctypes.data, n)
+    assert abs(out[0] - xs.astype(np.float64) @ ys) <= 1e-4 * np.abs(xs * ys).sum()
+    lib.scal.argtypes = [vp, ctypes.c_float, vp, ci]
+    y = np.zeros_like(xs)
+    lib.scal(y.ctypes.data, 1.5, xs.ctypes.data, n)
+    assert np.array_equal(y, np.float32(1.5) * xs)
+    A = rng.uniform(-1, 1, (8192, 8192)).astype(np.float32)
+    x = rng.uniform(-1, 1, 8192).astype(np.float32)
+    lib.gemv.argtypes = [vp, vp, vp]
+    lib.gemv(out.ctypes.data, A.ctypes.data, x.ctypes.data)
+    want = A.astype(np.float64) @ x
+    assert np.all(np.abs(out - want) <= 1e-4 * (np.abs(A) @ np.abs(x)))
