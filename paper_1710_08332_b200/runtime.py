@@ -114,14 +114,22 @@ def build_lib(out: str = LIB_PATH, verbose: bool = False) -> str:
     cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
     root = os.path.dirname(PKG)
     os.makedirs(os.path.dirname(out), exist_ok=True)
+    # build into a private file and rename it into place: several processes
+    # (one per GPU) may find the library missing at the same time
+    tmp = f"{out}.{os.getpid()}.tmp"
     cmd = ["g++", "-O2", "-shared", "-fPIC", "-std=c++17", "-Wall",
            "-I", os.path.join(root, "include"), "-I", os.path.join(cuda, "include"),
            os.path.join(PKG, "csrc", "dpia_rt.cpp"),
            "-L", os.path.join(cuda, "lib64"), "-lnvrtc", "-ldl",
-           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", out]
+           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", tmp]
     if verbose:
-        print("+", " ".join(cmd), flush=True)
-    subprocess.run(cmd, check=True)
+        print("+", " ".join(cmd[:-1] + [out]), flush=True)
+    try:
+        subprocess.run(cmd, check=True)
+        os.replace(tmp, out)
+    finally:
+        if os.path.exists(tmp):
+            os.remove(tmp)
     return out
 
 
