@@ -218,10 +218,13 @@ def get_cubin(src: str, arch: str = ARCH, opts: Sequence[str] = NVRTC_OPTS) -> b
             return _CUBINS[key]
     img = nvrtc_compile(src, arch=arch, opts=opts)
     _CUBINS[key] = img
-    try:
+    try:   # private file + atomic rename: concurrent ranks never read a partial cubin
         os.makedirs(USER_CACHE, exist_ok=True)
-        with open(os.path.join(USER_CACHE, key + ".cubin"), "wb") as f:
+        final = os.path.join(USER_CACHE, key + ".cubin")
+        tmp = f"{final}.{os.getpid()}.tmp"
+        with open(tmp, "wb") as f:
             f.write(img)
+        os.replace(tmp, final)
     except OSError:
         pass
     return img
