@@ -359,6 +359,17 @@ def e2e_pipelined_scal(inputs, stream, steps, chunks=8):
 
 # ------------------------------------------------------------ CPU legs
 
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def ref_lib():
     import ctypes
     path = os.path.join(ROOT, "oracle", "_ref", "libref_cpu.so")
@@ -435,12 +446,12 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
     best = min(times)
     if nbytes is None:  # mm: flop rate
         return {"value": round(flops / statistics.median(times) / 1e9, 3), "unit": "GFLOP/s",
-                "cores": int(lib.ref_threads()), "kind": "reference",
+                "cores": int(lib.ref_threads()), "cpu_model": _cpu_model(), "kind": "reference",
                 "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
                           f"median of {len(times)} calls",
                 "ms_per_call": round(1e3 * statistics.median(times), 4)}
     return {"value": round(nbytes / statistics.median(times) / 1e9, 3), "unit": "GB/s",
-            "cores": int(lib.ref_threads()), "kind": "reference",
+            "cores": int(lib.ref_threads()), "cpu_model": _cpu_model(), "kind": "reference",
             "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
                       f"median of {len(times)} calls, best {nbytes / best / 1e9:.1f} GB/s",
             "ms_per_call": round(1e3 * statistics.median(times), 4)}
@@ -524,7 +535,7 @@ def main():
             line.update({"unavailable": why})
         else:
             line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
-                         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
                          "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
                                  "d2h_bytes_per_step": 0}})
         print(json.dumps(line), flush=True)
@@ -675,7 +686,7 @@ def main():
                     suite[w][extra] = r[extra]
             if not args.no_cpu:
                 c = cpu_reference(w)
-                suite[w]["cpu_baseline"] = ({k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                suite[w]["cpu_baseline"] = ({k: c[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
                                             if c else None)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -702,7 +713,7 @@ def main():
                                        "dpia_l2_scrub (libdpia_rt, between steps, outside the events)":
                                        args.steps},
             "kernels": exe.kernel_names(),
-            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
                              if cpu else None),
             "suite": suite}
     print(json.dumps(line), flush=True)
