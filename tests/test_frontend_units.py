@@ -253,3 +253,23 @@ def test_stage2_accumulators_and_purity():
     s2 = stage2(_stage1(NORM2, default_space="global")[1], accum_space="private")
     assert _count(s2, {"new"}) == 0 and _count(s2, {"newPrivate"}) >= 1
     assert is_purely_imperative(s2)
+
+
+def test_golden_fixtures_regenerate_identically(tmp_path):
+    """Where the reference is importable (the build container), re-running
+    tests/golden/make_golden.py on the reference reproduces every committed
+    fixture byte for byte: the oracle's pinning is reproducible (CPU)."""
+    import os
+    import shutil
+    import subprocess
+    import sys
+    if not os.path.isdir("/root/reference/pkg/src/dpia"):
+        pytest.skip("the reference is not present on this machine")
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    shutil.copy(os.path.join(here, "make_golden.py"), tmp_path)
+    subprocess.run([sys.executable, str(tmp_path / "make_golden.py")], check=True, cwd=tmp_path,
+                   env=dict(os.environ, PYTHONPATH="/root/reference/pkg/src"), capture_output=True,
+                   timeout=600)
+    for name in ("programs.json", "fuzz.json", "fuzz_float.json", "index.json"):
+        with open(os.path.join(here, name), "rb") as a, open(tmp_path / name, "rb") as b:
+            assert a.read() == b.read(), name
