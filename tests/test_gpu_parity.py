@@ -115,6 +115,37 @@ def test_gemv_strategy_int_exact(M, N, L, blocks, x_private):
     assert [int(v) for v in got] == (A @ x).tolist()
 
 
+@pytest.mark.parametrize("workload", ["dot", "asum", "gemv", "mm"])
+def test_benchmark_configs_full_size_int64_exact(workload):
+    """The bench's exact programs and launches at BASELINE.json's full sizes
+    in int mode (int64 values in -9..9): bit-exact against numpy's integer
+    arithmetic (mm on 64 sampled rows)."""
+    from paper_1710_08332_b200.bench_programs import CONFIGS
+    cfg = CONFIGS[workload]()
+    prog = compile_program(cfg.text)
+    rng = np.random.default_rng(77)
+    if workload == "dot":
+        xs, ys = rng.integers(-9, 10, 1 << 24), rng.integers(-9, 10, 1 << 24)
+        got = run_program_cuda(prog, {"xs": xs, "ys": ys}, sigma=cfg.sigma, launch=cfg.launch,
+                               float_mode=False, flat=True)
+        assert int(got[0]) == int(xs @ ys)
+    elif workload == "asum":
+        xs = rng.integers(-9, 10, 1 << 26)
+        got = run_program_cuda(prog, {"xs": xs}, sigma=cfg.sigma, launch=cfg.launch, float_mode=False,
+                               flat=True)
+        assert int(got[0]) == int(np.abs(xs).sum())
+    elif workload == "gemv":
+        A, x = rng.integers(-9, 10, (8192, 8192)), rng.integers(-9, 10, 8192)
+        got = run_program_cuda(prog, {"A": A, "x": x}, launch=cfg.launch, float_mode=False, flat=True)
+        assert np.array_equal(np.asarray(got, np.int64), A @ x)
+    else:
+        A, B = rng.integers(-9, 10, (4096, 4096)), rng.integers(-9, 10, (4096, 4096))
+        got = np.asarray(run_program_cuda(prog, {"A": A, "B": B}, launch=cfg.launch, float_mode=False,
+                                          flat=True), np.int64).reshape(4096, 4096)
+        rows = rng.choice(4096, 64, replace=False)
+        assert np.array_equal(got[rows], A[rows] @ B)
+
+
 def test_dot_full_size_fp32():
     cfg = dot_config()
     N = 1 << 24
