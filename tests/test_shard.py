@@ -128,3 +128,23 @@ def test_run_program_cuda_gpus():
     else:
         with pytest.raises(ShardError):
             run_program_cuda(prog, data, {"n": 8}, (4, 32), float_mode=False, gpus=2)
+
+
+@pytest.mark.gpu
+def test_cli_run_gpus(tmp_path, capsys):
+    """`run --gpus 2` on a shardable program: prints the oracle's value on a
+    node with two GPUs; on a one-GPU node exits 2 with the device count."""
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.cli import main
+    prog, data = _inputs(dot_program(32, 2), 8, 11)
+    f = tmp_path / "dot.dpia"
+    f.write_text(dot_program(32, 2))
+    inp = tmp_path / "dot.inputs"
+    inp.write_text("n=8\n" + "".join(f"{k}=[{','.join(str(v) for v in vs)}]\n" for k, vs in data.items()))
+    rc = main(["run", str(f), "--inputs", str(inp), "--gpus", "2", "--int", "--launch", "4,32"])
+    out = capsys.readouterr()
+    if RT.device_count() >= 2:
+        want = eval_phrase(prog.source.body, data, {"n": 8})
+        assert rc == 0 and f"out = {want}" in out.out
+    else:
+        assert rc == 2 and "present" in out.err
