@@ -1,3 +1,8 @@
+"""gemv staging variants (x in shared memory vs x_private registers) across
+work-group sizes and grid sizes, checked against float64 numpy (GPU box).
+
+    python tools/gemv_focus.py
+"""
 import os, sys, statistics
 sys.path.insert(0, os.getcwd())
 import numpy as np
