@@ -33,7 +33,8 @@ sys.path.insert(0, ROOT)
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
-                                                  gemv_config, mm_config, scal_config)
+                                                  dot_literal_config, gemv_config, mm_config,
+                                                  scal_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
 
@@ -182,7 +183,9 @@ class Clocks:
 # ------------------------------------------------------------ workloads
 
 def make_workload(name, device, rank=0, world=1, combine="nccl"):
-    """(config, executable, host inputs or None, prepare(stream))."""
+    """(config, executable, host inputs or None, prepare(stream), program).
+    The program is returned so a peer-combined executable can be checked
+    against its combine-free twin (peer.cross_check)."""
     allgather = None
     if world > 1 and combine == "peer":
         from paper_1710_08332_b200.peer import torch_allgather as allgather
@@ -194,7 +197,7 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
                                combine=combine if world > 1 else "nccl", allgather=allgather)
         cfg = Config(name, "", {"n": run.shard.chunks}, run.exe.sig.launch, bytes=run.bytes,
                      flops=(2 if kind == "dot" else 1) * run.shard.elems)
-        return cfg, run.exe, None, run.fill_inputs
+        return cfg, run.exe, None, run.fill_inputs, run.prog
     if name == "asum":
         cfg = asum_config()
         inputs = {"xs": _seeded(1 << 26, 2 + 1000 * rank, -1.0, 1.0)}
@@ -202,8 +205,13 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
         cfg = dot_config()
         inputs = {"xs": _seeded(1 << 24, 0 + 1000 * rank, 0.0, 1.0),
                   "ys": _seeded(1 << 24, 1 + 1000 * rank, 0.0, 1.0)}
-    elif name == "gemv":
-        cfg = gemv_config()
+    elif name == "dot_literal":
+        cfg = dot_literal_config()
+        inputs = {"xs": _seeded(1 << 24, 0 + 1000 * rank, 0.0, 1.0),
+                  "ys": _seeded(1 << 24, 1 + 1000 * rank, 0.0, 1.0)}
+    elif name in ("gemv", "gemv_xprivate"):
+        cfg = gemv_config(x_private=name == "gemv_xprivate")
+        cfg.name = name
         inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
     elif name == "scal":
         cfg = scal_config()
@@ -215,7 +223,7 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
         raise SystemExit(f"unknown workload {name}")
     prog = compile_program(cfg.text, name=name)
     peer = None
-    if allgather is not None and name in ("asum", "dot"):
+    if allgather is not None and name in ("asum", "dot", "dot_literal"):
         from paper_1710_08332_b200.peer import PeerGroup
         peer = PeerGroup(device, rank, world, 1, allgather)
     exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device, peer=peer)
@@ -223,7 +231,7 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
     def prepare(stream):
         for n, v in inputs.items():
             exe.upload(n, v, stream)
-    return cfg, exe, inputs, prepare
+    return cfg, exe, inputs, prepare, prog
 
 
 def _seeded(shape, seed, lo, hi):
@@ -370,45 +378,84 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+_REF_LIB = None
+
+
 def ref_lib():
-    import ctypes
-    path = os.path.join(ROOT, "oracle", "_ref", "libref_cpu.so")
-    if not os.path.exists(path):
+    """The reference's CPU path (oracle/_ref): its c-openmp emissions of the
+    strategy programs.  On the benchmark host they are recompiled once with
+    -march=native (oracle/build_ref.py native; the generated .c files travel
+    with the snapshot), else the prebuilt x86-64-v3 library is used."""
+    global _REF_LIB
+    if _REF_LIB is not None:
+        return _REF_LIB
+    sys.path.insert(0, ROOT)
+    from oracle import build_ref
+    path, march = build_ref.native_lib()
+    if path is None:
         return None
     lib = ctypes.CDLL(path)
+    lib.march = march
+    _REF_LIB = lib
     return lib
 
 
+# what the reference's CPU path runs for each workload (oracle/ref_programs/*.dpia
+# through the reference's own `compile --target c-openmp`)
+REF_STRATEGY = {
+    "asum": ("asum N=2^26 fp32", "asum_proxy.dpia: mapGlobal over 1024-element chunks, sequential "
+             "reduce per chunk, sequential top-level reduce of the partials; a plain sum -- the "
+             "reference language has no abs -- with asum's exact traffic"),
+    "dot": ("dot N=2^24 fp32", "dot.dpia (BASELINE config 1): mapGlobal over 1024-element chunks of "
+            "zip xs ys, sequential reduce per chunk, sequential top-level reduce"),
+    "gemv": ("gemv 8192x8192 fp32", "gemv.dpia: row per work-group, x staged toLocal, 256 items x "
+             "32-element chunks, partials combined sequentially"),
+    "scal": ("scal N=2^26 fp32 (read + write)", "scal.dpia: mapGlobal over 1024-element chunks, mapSeq"),
+    "mm": ("mm 4096^3 fp32", "mm_bt.dpia: B passed pre-transposed (the reference language has no "
+           "transpose), one row of A per work-item, sequential reduce per output element"),
+}
+REF_STRATEGY["dot_literal"] = REF_STRATEGY["dot"]
+REF_STRATEGY["gemv_xprivate"] = REF_STRATEGY["gemv"]
+
+
 def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1):
-    """Time the reference's own CPU path (its c-openmp emission of the same
-    strategy, compiled by oracle/build_ref.py) on all host threads."""
-    import ctypes
+    """Time the reference's own CPU path (its c-openmp emission of the
+    workload's program, oracle/ref_programs/) on all host threads."""
     lib = ref_lib()
     if lib is None:
         return None
     vp, ci = ctypes.c_void_p, ctypes.c_int
     out = np.zeros(8192, np.float32)
-    if workload == "asum":
+    base = workload
+    note = ""
+    if workload.startswith("scaleout"):
+        # the reference's emitted C indexes with 32-bit int and keeps the
+        # partials in a stack VLA: 2^31 elements overflow both, so a
+        # bounded sample of the same per-element work is timed
+        base = "dot" if workload.endswith("dot") else "asum"
+        note = ("; a 2^24 (dot) / 2^26 (asum) sample of the 2^31 workload: the reference's emitted C "
+                "indexes with 32-bit int and cannot address 2^31 elements")
+    if base in ("asum",):
         n = (1 << 26) // 1024
         xs = _seeded(1 << 26, 2, -1.0, 1.0)
         fn = lib.asum_proxy
         fn.argtypes = [vp, vp, ci]
         call = lambda: fn(out.ctypes.data, xs.ctypes.data, n)  # noqa: E731
-        nbytes, sample = 4 << 26, "asum proxy (sum; the reference has no abs) over 2^26 fp32, full size"
-    elif workload == "dot":
+        nbytes, sample = 4 << 26, "asum_proxy over 2^26 fp32, full size"
+    elif base in ("dot", "dot_literal"):
         n = (1 << 24) // 1024
         xs, ys = _seeded(1 << 24, 0, 0.0, 1.0), _seeded(1 << 24, 1, 0.0, 1.0)
         fn = lib.dot
         fn.argtypes = [vp, vp, vp, ci]
         call = lambda: fn(out.ctypes.data, xs.ctypes.data, ys.ctypes.data, n)  # noqa: E731
         nbytes, sample = 8 << 24, "dot over 2^24 fp32 pairs, full size"
-    elif workload == "gemv":
+    elif base in ("gemv", "gemv_xprivate"):
         A, x = _seeded((8192, 8192), 3, -1.0, 1.0), _seeded(8192, 4, -1.0, 1.0)
         fn = lib.gemv
         fn.argtypes = [vp, vp, vp]
         call = lambda: fn(out.ctypes.data, A.ctypes.data, x.ctypes.data)  # noqa: E731
         nbytes, sample = 4 * (8192 * 8192 + 2 * 8192), "gemv 8192x8192 fp32, full size"
-    elif workload == "scal":
+    elif base == "scal":
         n = (1 << 26) // 1024
         xs = _seeded(1 << 26, 7, -1.0, 1.0)
         ys = np.zeros(1 << 26, np.float32)
@@ -416,7 +463,7 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         fn.argtypes = [vp, ctypes.c_float, vp, ci]
         call = lambda: fn(ys.ctypes.data, 1.5, xs.ctypes.data, n)  # noqa: E731
         nbytes, sample = 8 << 26, "scal (y = alpha x) over 2^26 fp32, full size (read + write)"
-    elif workload == "mm":
+    elif base == "mm":
         A, B = _seeded((4096, 4096), 5, -1.0, 1.0), _seeded((4096, 4096), 6, -1.0, 1.0)
         Bt = np.ascontiguousarray(B.T)
         big = np.zeros(4096 * 4096, np.float32)
@@ -424,13 +471,13 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         fn.argtypes = [vp, vp, vp]
         call = lambda: fn(big.ctypes.data, A.ctypes.data, Bt.ctypes.data)  # noqa: E731
         flops = 2 * 4096 ** 3
-        sample = ("mm 4096^3 fp32, full size, B passed pre-transposed (the reference language has "
-                  "no transpose)")
+        sample = "mm 4096^3 fp32, full size, B passed pre-transposed"
         min_seconds, max_reps = 0.0, 2
         steps = None if steps is None else min(steps, 2)  # ~5 s per call on 16 threads
         nbytes = None
     else:
         return None
+    prog = REF_STRATEGY.get(base, ("", ""))[1]
     for _ in range(max(1, warmup if nbytes is not None else min(warmup, 1))):
         call()
     times = []
@@ -444,17 +491,40 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         if steps is None and (time.perf_counter() - t_start > min_seconds or len(times) >= max_reps):
             break
     best = min(times)
+    how = (f"reference c-openmp emission of {prog} (gcc -O3 -march={lib.march} -fopenmp, "
+           f"OMP threads = {int(lib.ref_threads())})")
+    common = {"cores": int(lib.ref_threads()), "cpu_model": _cpu_model(), "kind": "reference",
+              "march": lib.march, "ms_per_call": round(1e3 * statistics.median(times), 4)}
     if nbytes is None:  # mm: flop rate
-        return {"value": round(flops / statistics.median(times) / 1e9, 3), "unit": "GFLOP/s",
-                "cores": int(lib.ref_threads()), "cpu_model": _cpu_model(), "kind": "reference",
-                "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
-                          f"median of {len(times)} calls",
-                "ms_per_call": round(1e3 * statistics.median(times), 4)}
-    return {"value": round(nbytes / statistics.median(times) / 1e9, 3), "unit": "GB/s",
-            "cores": int(lib.ref_threads()), "cpu_model": _cpu_model(), "kind": "reference",
-            "sample": f"{sample}; reference c-openmp emission (gcc -O3 -fopenmp), "
-                      f"median of {len(times)} calls, best {nbytes / best / 1e9:.1f} GB/s",
-            "ms_per_call": round(1e3 * statistics.median(times), 4)}
+        return dict(common, value=round(flops / statistics.median(times) / 1e9, 3), unit="GFLOP/s",
+                    sample=f"{sample}{note}; {how}, median of {len(times)} calls")
+    return dict(common, value=round(nbytes / statistics.median(times) / 1e9, 3), unit="GB/s",
+                sample=f"{sample}{note}; {how}, median of {len(times)} calls, "
+                       f"best {nbytes / best / 1e9:.1f} GB/s")
+
+
+def reference_arm(args):
+    """`--impl reference`: the reference's own CPU implementation of the
+    workload (oracle/_ref, its c-openmp emission, all host threads), on the
+    same metric, unit and workload as our arm; each step one call."""
+    r = cpu_reference(args.workload, steps=args.steps, warmup=args.warmup)
+    unit = "GFLOP/s" if args.workload == "mm" else "GB/s"
+    wl, strat = REF_STRATEGY.get(args.workload, (args.workload, "none"))
+    line = {"impl": "reference", "metric": METRIC, "unit": unit, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl, "strategy": strat,
+                       "reference_path": "the reference's c-openmp emission of the program on the "
+                                         "host cores (oracle/_ref, built by oracle/build_ref.py)"}}
+    if r is None:
+        line["unavailable"] = _cpu_unavailable(args.workload, 1)
+    else:
+        line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
+                     "cpu_baseline": _cpu_fields(r),
+                     "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0}})
+    print(json.dumps(line), flush=True)
+    return 0
 
 
 # ------------------------------------------------------------ main
@@ -474,9 +544,21 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # `python bench.py --gpus N` without a launcher: one process per GPU
+        # under torchrun, this same command line in every rank
+        return _spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        # the reference's CPU path: rank 0 alone, on the host cores; other
+        # ranks of a torchrun launch exit without work
+        return reference_arm(args) if rank == 0 else 0
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              f"(torchrun --nproc-per-node {args.gpus}) or drop the launcher", file=sys.stderr)
+        return 2
     # plumbing check on a one-GPU box: every rank on GPU 0, gloo for the host
     # side (the fused peer combine still runs GPU to GPU through CUDA IPC);
     # the timings of ranks sharing a GPU are not scaling numbers
@@ -488,8 +570,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("gloo" if share else "nccl")
+        if args.impl == "ours" and not share and torch.cuda.device_count() < world:
+            print(f"bench.py: {world} ranks need {world} GPUs, {torch.cuda.device_count()} visible "
+                  "(DPIA_BENCH_SHARE_GPU=1 runs every rank on GPU 0 as a plumbing check)",
+                  file=sys.stderr)
+            return 3
+        if args.impl == "ours":
+            torch.cuda.set_device(local)
+        dist.init_process_group("gloo" if (share or args.impl == "reference") else "nccl")
         if args.impl == "ours" and args.combine == "peer":
             # collective capability probe: every rank maps every peer's
             # mailbox (CUDA IPC + NVLink P2P); if any rank cannot, all ranks
@@ -504,42 +592,11 @@ def main():
                 ok = 0
             if not int(_allreduce(dist, ok, dist.ReduceOp.MIN, local, share)):
                 args.combine = "nccl"
-        if args.impl == "ours" and args.combine == "nccl":
-            import ctypes
-            uid = ctypes.create_string_buffer(128)
-            if rank == 0:
-                RT.lib().dpia_nccl_unique_id(uid)
-            obj = [bytes(uid.raw)]
-            dist.broadcast_object_list(obj, src=0)
-            RT.init(local)
-            RT.lib().dpia_nccl_init(local, world, rank, obj[0])
-
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        r = cpu_reference(args.workload, steps=args.steps, warmup=args.warmup)
-        unit = "GFLOP/s" if args.workload == "mm" else "GB/s"
-        from paper_1710_08332_b200.bench_programs import CONFIGS
-        cfg_line = (dict({k: v for k, v in _cfg_desc(CONFIGS[args.workload]()).items() if k != "l2"},
-                         reference_path="the reference's c-openmp emission of the same workload on the "
-                                        "host cores (oracle/_ref)")
-                    if args.workload in CONFIGS else
-                    {"workload": f"{args.workload} (reference c-openmp path on host cores)"})
-        line = {"impl": "reference", "metric": METRIC, "unit": unit, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": cfg_line}
-        if r is None:
-            why = ("oracle/_ref/libref_cpu.so not built (needs /root/reference at build)" if ref_lib() is None
-                   else f"the reference's c-openmp path has no program for workload {args.workload!r}")
-            line.update({"unavailable": why})
-        else:
-            line.update({"value": r["value"], "ms_per_step": r["ms_per_call"],
-                         "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")},
-                         "e2e": {"value": r["value"], "unit": r["unit"], "h2d_bytes_per_step": 0,
-                                 "d2h_bytes_per_step": 0}})
-        print(json.dumps(line), flush=True)
-        return
+        if args.impl == "ours" and not share:
+            # NCCL is always set up at N > 1: it is the combine of
+            # --combine nccl, the fallback of the peer combine and the
+            # cross-check of its totals
+            _nccl_init(dist, local, world, rank)
 
     device = local
     RT.init(device)
@@ -547,9 +604,25 @@ def main():
     peak, peak_src = peaks()
 
     def measure(workload, steps, warmup, with_e2e):
-        cfg, exe, inputs, prepare = make_workload(workload, device, rank, world, args.combine)
+        cfg, exe, inputs, prepare, prog = make_workload(workload, device, rank, world, args.combine)
         prepare(stream)
         stream.sync()
+        check = None
+        if exe.peer is not None and world > 1:
+            # the fused combine's total against the partials it combines
+            # (bit-exact rank-order sum) and against NCCL; on any
+            # disagreement or peer timeout every rank falls back to NCCL
+            check = _combine_check(exe, prog, stream, dist, share, rank, local)
+            if not check["agree_all_ranks"]:
+                if share:
+                    raise SystemExit(f"peer combine disagrees: {check}")
+                exe.peer.close()
+                cfg, exe, inputs, prepare, prog = make_workload(workload, device, rank, world, "nccl")
+                prepare(stream)
+                stream.sync()
+                check["combine_used"] = "nccl (fallback)"
+            else:
+                check["combine_used"] = "peer"
         allreduce = None
         reduces = workload in ("asum", "dot") or workload.startswith("scaleout")
         if world > 1 and exe.peer is None and reduces:
@@ -586,7 +659,7 @@ def main():
             ms = run_timed(exe, stream, steps, allreduce=allreduce)
             wall = time.perf_counter() - t0
         RT.lib().dpia_device_sync(device)
-        mean_ms = statistics.mean(ms)
+        mean_ms = mean_ms_local = statistics.mean(ms)
         if dist is not None:
             import torch
             mean_ms = float(_allreduce(dist, mean_ms, dist.ReduceOp.MAX, local, share))
@@ -625,6 +698,10 @@ def main():
         res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
                "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
                "value": value, "roofline": roof}
+        if check is not None:
+            res["combine_check"] = check
+        if world > 1:
+            res["ranks"] = _rank_info(dist, rank, device, mean_ms_local, share)
         if with_e2e and inputs is not None:
             e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
             if dist is not None:   # whole job: every rank's bytes over the slowest rank's time
@@ -675,26 +752,38 @@ def main():
 
     head = measure(args.workload, args.steps, args.warmup, with_e2e=True)
     suite = {}
-    if not args.no_suite and world == 1:
-        for w in ("dot", "asum", "gemv", "mm", "scal", "scaleout_asum", "scaleout_dot"):
+    # N = 1: every benchmark program; N > 1: the sharded reductions of
+    # BASELINE config 5 (2^31 in total, strong scaling) beside the weak-scaled
+    # headline -- gemv / mm / scal would only replicate (no exchange step)
+    names = (("dot", "dot_literal", "asum", "gemv", "gemv_xprivate", "mm", "scal",
+              "scaleout_asum", "scaleout_dot") if world == 1 else ("scaleout_asum", "scaleout_dot"))
+    if not args.no_suite:
+        for w in names:
             if w == args.workload:
                 continue
             r = measure(w, min(args.steps, 20), 3, with_e2e=True)
             suite[w] = {"value": round(r["value"], 1), "unit": "GFLOP/s" if w == "mm" else "GB/s",
                         "ms_per_step": round(r["mean_ms"], 5), "roofline": r["roofline"],
-                        "e2e": r.get("e2e"), "clocks": r["clocks"], "config": _cfg_desc(r["cfg"])}
-            for extra in ("e2e_unpipelined", "e2e_row_pipeline"):
+                        "scaling": "strong" if w.startswith("scaleout") else "weak",
+                        "e2e": r.get("e2e"), "clocks": r["clocks"],
+                        "config": _cfg_desc(r["cfg"], world, args.combine),
+                        "kernels": r["exe"].kernel_names()}
+            if r.get("e2e") is None and w.startswith("scaleout"):
+                suite[w]["e2e_note"] = ("config 5 generates its inputs on device by a counter hash "
+                                        "(BASELINE.json configs[4]); no host data moves")
+            for extra in ("e2e_unpipelined", "e2e_row_pipeline", "combine_check", "ranks"):
                 if r.get(extra):
                     suite[w][extra] = r[extra]
-            if not args.no_cpu:
-                c = cpu_reference(w)
-                suite[w]["cpu_baseline"] = ({k: c[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
-                                            if c else None)
+            if not args.no_cpu and rank == 0:
+                c = cpu_reference(w) if world == 1 else None
+                suite[w]["cpu_baseline"] = (_cpu_fields(c) if c else
+                                            {"unavailable": _cpu_unavailable(w, world)})
+            r["exe"] = None
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_reference(args.workload)
     if rank != 0:
-        return
+        return 0
     cfg, exe = head["cfg"], head["exe"]
     strong = args.workload.startswith("scaleout")
     line = {"metric": METRIC, "value": round(head["value"], 2),
@@ -715,10 +804,100 @@ def main():
                                        "dpia_l2_scrub (libdpia_rt, between steps, outside the events)":
                                        args.steps},
             "kernels": exe.kernel_names(),
-            "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample")}
-                             if cpu else None),
+            "cpu_baseline": (_cpu_fields(cpu) if cpu else
+                             {"unavailable": _cpu_unavailable(args.workload, world)}),
             "suite": suite}
+    for extra in ("combine_check", "ranks"):
+        if head.get(extra):
+            line[extra] = head[extra]
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cpu_fields(c):
+    return {k: c[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample", "march") if k in c}
+
+
+def _cpu_unavailable(workload, world):
+    if world > 1:
+        return "the CPU baseline is timed at N = 1 only (rank 0, host cores); see the N = 1 line"
+    if ref_lib() is None:
+        return "oracle/_ref/libref_cpu.so not built (needs /root/reference at build time)"
+    return f"the reference's c-openmp path has no program for workload {workload!r}"
+
+
+def _spawn_ranks(n):
+    """Re-run this command line as n ranks under torchrun (one process per
+    GPU, rendezvous on 127.0.0.1); returns torchrun's exit code.  Rank 0
+    prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def _nccl_init(dist, local, world, rank):
+    uid = ctypes.create_string_buffer(128)
+    if rank == 0:
+        RT.lib().dpia_nccl_unique_id(uid)
+    obj = [bytes(uid.raw)]
+    dist.broadcast_object_list(obj, src=0)
+    RT.init(local)
+    RT.lib().dpia_nccl_init(local, world, rank, obj[0])
+
+
+def _combine_check(exe, prog, stream, dist, share, rank, local):
+    """peer.cross_check on every rank, plus the NCCL sum of the same
+    partials when NCCL is up; agreement is decided over all ranks."""
+    from paper_1710_08332_b200.peer import PeerError, cross_check, local_twin, torch_allgather
+    try:
+        ev = cross_check(exe, local_twin(exe, prog), stream, torch_allgather)
+        ok = ev["bit_exact"]
+    except (PeerError, RT.DpiaRuntimeError) as e:
+        ev, ok = {"error": str(e)}, False
+    if ok and not share:
+        buf = RT.DeviceBuffer(16, exe.device)
+        buf.upload(np.array([ev["partials"][rank], 0, 0, 0], np.float32))
+        RT.lib().dpia_nccl_allreduce(buf.ptr, 1, 0, stream.handle)
+        stream.sync()
+        v = np.zeros(4, np.float32)
+        buf.download(v)
+        buf.free()
+        ev["nccl_allreduce"] = float(v[0])
+        ev["nccl_rel_diff"] = abs(float(v[0]) - ev["peer_total"][0]) / max(ev["abs_sum"], 1e-30)
+        ok = ev["nccl_rel_diff"] <= 1e-6
+    ev["agree_all_ranks"] = bool(int(_allreduce(dist, int(ok), dist.ReduceOp.MIN, local, share)))
+    return ev
+
+
+def _rank_info(dist, rank, device, ms, share):
+    """Per-rank evidence: device, PCI bus, the runtime library this process
+    loaded, and its own mean step time (the line reports the max)."""
+    import torch
+    props = torch.cuda.get_device_properties(device)
+    info = {"rank": rank, "device": device, "ms_per_step": round(ms, 5), "gpu": props.name,
+            "pci_bus_id": getattr(props, "pci_bus_id", None), "shared_gpu": bool(share),
+            "lib": _loaded_lib()}
+    out = [None] * dist.get_world_size()
+    dist.all_gather_object(out, info)
+    return out
+
+
+def _loaded_lib():
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                if "libdpia_rt" in ln:
+                    return os.path.relpath(ln.split()[-1], ROOT)
+    except OSError:
+        pass
+    return None
 
 
 def _allreduce(dist, value, op, local, share):
@@ -729,24 +908,38 @@ def _allreduce(dist, value, op, local, share):
     return t.item()
 
 
+WORKLOADS = {
+    "asum": ("asum N=2^26 fp32", "asVector4 + mapWorkgroup/mapLocal + reduceSeq(abs) + reduceLocal, "
+             "grid combine fused as a last-block tail"),
+    "dot": ("dot N=2^24 fp32", "asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal, grid "
+            "combine fused as a last-block tail"),
+    "dot_literal": ("dot N=2^24 fp32", "BASELINE config 1 as the reference states it "
+                    "(oracle/ref_programs/dot.dpia): mapGlobal over 1024-element chunks, reduceSeq "
+                    "per chunk, top-level sequential reduce of the 16384 partials"),
+    "gemv": ("gemv 8192x8192 fp32", "BASELINE config 3: row per work-group, x staged with toLocal "
+             "(shared memory), reduceSeq over vec4 column slices, reduceLocal per row"),
+    "gemv_xprivate": ("gemv 8192x8192 fp32", "row per work-group, x staged toPrivate in the "
+                      "work-items' column layout (registers), reduceSeq + reduceLocal per row"),
+    "scal": ("scal N=2^26 fp32 (read + write)", "grid-stride mapGlobal over vec4"),
+    "mm": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "128x128 tiles, 8x8 register tiles, toLocal "
+           "k-tiles of 16, FFMA2"),
+}
+
+
 def _cfg_desc(cfg, world=1, combine="nccl"):
     if cfg.name.startswith("scaleout"):
         kind = "dot" if cfg.name.endswith("dot") else "asum"
-        return {"workload": f"{kind} scale-out N=2^31 fp32 total, {world} shard(s), partials combined "
+        return {"workload": f"{kind} scale-out N=2^31 fp32 total",
+                "strategy": f"{world} shard(s) of 2^31/{world}, partials combined "
                             + ("inside the kernel over NVLink (peer)" if combine == "peer" and world > 1
                                else "by a 4-byte NCCL all-reduce" if world > 1 else "(one shard)"),
                 "sigma_per_rank": cfg.sigma,
                 "launch": list(cfg.launch), "l2": "inputs (>= 1 GiB per GPU) exceed L2; L2 also "
                 "scrubbed between steps"}
-    return {"workload": {"asum": "asum N=2^26 fp32, asVector4 + mapWorkgroup/mapLocal + reduceLocal",
-                         "dot": "dot N=2^24 fp32, asVector4 + mapWorkgroup/mapLocal/reduceSeq + reduceLocal",
-                         "gemv": "gemv 8192x8192 fp32, row per work-group, x staged toPrivate in the work-items column layout (registers)",
-                         "scal": "scal N=2^26 fp32 (read + write), grid-stride mapGlobal over vec4",
-                         "mm": "mm 4096^3 fp32 (FFMA, no tensor cores), 128x128 tiles, 8x8 register "
-                               "tiles, toLocal k-tiles of 16, FFMA2"}[cfg.name],
-            "sigma": cfg.sigma, "launch": list(cfg.launch),
+    wl, strat = WORKLOADS[cfg.name]
+    return {"workload": wl, "strategy": strat, "sigma": cfg.sigma, "launch": list(cfg.launch),
             "l2": "scrubbed between steps (a read of 2x L2 by dpia_l2_scrub, outside the timed events)"}
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -56,5 +56,49 @@ def build(verbose: bool = False) -> bool:
     return True
 
 
+def _host_tag() -> str:
+    """Short hash of this host's CPU model and feature flags: a -march=native
+    build is only reused on a host that reports the same CPU."""
+    import hashlib
+    h = hashlib.sha1()
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith(("model name", "flags")):
+                    h.update(ln.encode())
+                    if ln.startswith("flags"):
+                        break
+    except OSError:
+        pass
+    return h.hexdigest()[:12]
+
+
+def native_lib():
+    """(path, march) of the reference CPU library to time on this host.
+
+    The emitted .c files (the reference compiler's output, git-ignored but
+    shipped with the snapshot) are recompiled here once with -march=native,
+    as BASELINE.md section 4 prescribes; the portable x86-64-v3 build is the
+    fallback when gcc is missing or fails.  (None, None) if neither exists."""
+    NATIVE = os.path.join(OUT, f"libref_cpu_native_{_host_tag()}.so")
+    srcs = [os.path.join(OUT, n + ".c") for n in PROGRAMS] + [os.path.join(OUT, "harness.c")]
+    if os.path.exists(NATIVE) and all(os.path.getmtime(NATIVE) >= os.path.getmtime(c)
+                                      for c in srcs if os.path.exists(c)):
+        return NATIVE, "native"
+    if all(os.path.exists(c) for c in srcs):
+        tmp = f"{NATIVE}.{os.getpid()}.tmp"
+        try:
+            subprocess.run(["gcc", "-O3", "-march=native", "-fopenmp", "-shared", "-fPIC", "-o", tmp]
+                           + srcs, check=True, capture_output=True)
+            os.replace(tmp, NATIVE)
+            return NATIVE, "native"
+        except (OSError, subprocess.CalledProcessError):
+            if os.path.exists(tmp):
+                os.remove(tmp)
+    if os.path.exists(LIB):
+        return LIB, "x86-64-v3"
+    return None, None
+
+
 if __name__ == "__main__":
     build(verbose=True)

@@ -174,6 +174,78 @@ def _prim(name, targs, args, env, sigma):
     return NotImplemented
 
 
+# ------------------------------------------------- error bounds (float mode)
+
+class Bounded:
+    """A float-mode number carried with a first-order bound on its rounding
+    sensitivity: t = sum of |terms| for + - *, propagated through / as
+    t_a/|b| + |a| t_b/b^2.  Evaluating a program on Bounded inputs gives,
+    per output, the normwise scale of the tolerance |got - want| <= tol * t
+    that the fp32 parity tests state."""
+    __slots__ = ("v", "t")
+
+    def __init__(self, v, t=None):
+        self.v = v
+        self.t = abs(v) if t is None else t
+
+    @staticmethod
+    def _w(o):
+        return o if isinstance(o, Bounded) else Bounded(o)
+
+    def __add__(self, o):
+        o = self._w(o)
+        return Bounded(self.v + o.v, self.t + o.t)
+
+    __radd__ = __add__
+
+    def __sub__(self, o):
+        o = self._w(o)
+        return Bounded(self.v - o.v, self.t + o.t)
+
+    def __rsub__(self, o):
+        return self._w(o) - self
+
+    def __mul__(self, o):
+        o = self._w(o)
+        return Bounded(self.v * o.v, self.t * o.t)
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, o):
+        o = self._w(o)
+        return Bounded(self.v / o.v, self.t / abs(o.v) + abs(self.v) * o.t / (o.v * o.v))
+
+    def __rtruediv__(self, o):
+        return self._w(o) / self
+
+    def __neg__(self):
+        return Bounded(-self.v, self.t)
+
+    def __abs__(self):
+        return Bounded(abs(self.v), self.t)
+
+
+def bounded(value):
+    """Wrap every float leaf of an input value in Bounded."""
+    if isinstance(value, float):
+        return Bounded(value)
+    if isinstance(value, Vec):
+        return Vec(tuple(bounded(x) for x in value.items))
+    if isinstance(value, tuple):
+        return tuple(bounded(x) for x in value)
+    if isinstance(value, list):
+        return [bounded(x) for x in value]
+    return value
+
+
+def eval_with_bounds(p: Phrase, env: Dict[str, object], sigma: Dict[str, int] = None):
+    """(values, bounds): the float64 result leaves and their sum|terms|."""
+    out = flatten_value(eval_phrase(p, {k: bounded(v) for k, v in env.items()}, sigma))
+    vals = [x.v if isinstance(x, Bounded) else x for x in out]
+    bnds = [x.t if isinstance(x, Bounded) else abs(x) for x in out]
+    return vals, bnds
+
+
 # ------------------------------------------------------ value marshalling
 
 def flatten_value(v) -> List[Number]:

@@ -391,6 +391,32 @@ def dot_config(N: int = 1 << 24, L: int = 1024, K: int = 16, blocks=None) -> Con
     return Config("dot", dot_program(L, K), {"n": n}, (blocks or n, L), bytes=8 * N, flops=2 * N)
 
 
+def dot_literal_program(chunk: int = 1024) -> str:
+    """BASELINE config 1 exactly as the reference can state and run it
+    (oracle/ref_programs/dot.dpia): mapGlobal over
+    `chunk`-element pieces of (zip xs ys), a sequential reduce per piece
+    (reduceSeq: one work-item walks its own contiguous piece), then the
+    top-level sequential reduce of the partial sums -- the fused
+    single-thread tail of the emitted kernel.  Only the reference's own
+    primitives; no transpose, no vectors, no reduceLocal."""
+    return f"""
+(nat n)
+(param xs (exp (array (* n {chunk}) num)))
+(param ys (exp (array (* n {chunk}) num)))
+(reduce (+) 0
+ (mapGlobal (lam (c (exp (array {chunk} (pair num num))))
+   (reduce (lam (x (exp (pair num num))) (lam (a (exp num)) (+ (* (fst x) (snd x)) a))) 0 c))
+  (split {chunk} (zip xs ys))))
+"""
+
+
+def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 128) -> Config:
+    """One work-item per chunk: N / chunk work-items in groups of L."""
+    n = N // chunk
+    return Config("dot_literal", dot_literal_program(chunk), {"n": n}, (n // L, L),
+                  bytes=8 * N, flops=2 * N)
+
+
 def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -399,13 +425,22 @@ def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Co
 
 
 def gemv_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int = 148 * 8,
-                x_private: bool = True) -> Config:
+                x_private: bool = False) -> Config:
+    """BASELINE config 3: row per work-group, x staged with toLocal
+    (x_private=True: the toPrivate register-staged variant, `gemv_xprivate`)."""
     return Config("gemv", gemv_program(M, N, L, x_private), {}, (min(blocks, M), L),
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
 
+def gemv_xprivate_config(**kw) -> Config:
+    cfg = gemv_config(x_private=True, **kw)
+    cfg.name = "gemv_xprivate"
+    return cfg
+
+
 CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
-           "scal": scal_config}
+           "scal": scal_config, "dot_literal": dot_literal_config,
+           "gemv_xprivate": gemv_xprivate_config}
 
 
 def aot_sources():

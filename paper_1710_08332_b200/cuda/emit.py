@@ -1089,7 +1089,11 @@ class KernelEmitter:
         trip = self.nat_int(n)
         start, stride, S = self._geometry(level, dim)
         v = self.fresh(binder)
-        wide = trip is None or trip > IX.INT32_MAX
+        # `v += stride` must not overflow either: the last increment reaches
+        # up to trip - 1 + stride (the stride's bound when it is a runtime
+        # quantity: blockDim <= 1024, gridDim-based up to 2^31)
+        step = S if S is not None else (1024 if level in ("local", "lin", "fold") else 1 << 31)
+        wide = trip is None or trip - 1 + step > IX.INT32_MAX
         ctype = "long long" if wide else "int"
         self.R[v] = trip
         single = trip is not None and S is not None and trip <= S
@@ -1721,6 +1725,12 @@ class ProgramEmitter:
         for key, recs in ke.records.items():
             best = None
             keys_at: List = []
+            # a buffer that only the single-thread (dpia_tid == 0) regions
+            # touch -- e.g. the accumulator of a sequential top-level reduce
+            # in a fused tail -- lives in thread 0's registers: every access
+            # is by the same thread, so no other work-item needs to see it
+            if recs and all(st for _, _, st, _ in recs):
+                continue
             distributed = any(st or any(lp.level in ("local", "lin", "fold", "global")
                                         for lp in loops[depth:])
                               for _, loops, st, depth in recs)

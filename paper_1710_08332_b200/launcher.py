@@ -19,7 +19,7 @@ import numpy as np
 
 from . import layout as LY
 from . import runtime as RT
-from .cuda.emit import CudaSignature, emit_cuda, normalize_launch
+from .cuda.emit import CudaError, CudaSignature, emit_cuda, normalize_launch
 from .cuda.hierarchy import check_work_item_races
 from .dtypes import DataType
 from .terms import Phrase
@@ -179,6 +179,13 @@ def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None
     src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name,
                          sigma=sigma if specialize else None, launch=geom if specialize else None,
                          peer=peer is not None)
+    if peer is not None:
+        # dpia::peer_sum writes one mailbox slot per output scalar into every
+        # peer: the group's mailboxes must have been sized for exactly that
+        nsc = LY.nbytes(outs[0][1], sigma, float_mode) // (4 if float_mode else 8)
+        if nsc != peer.n:
+            raise CudaError(f"the program's result has {nsc} scalars; the peer group's mailboxes "
+                            f"hold {peer.n}")
     exe = Executable(src, sig, device, float_mode, sigma, geometry=geom, peer=peer)
     return exe.compile().allocate()
 

@@ -85,6 +85,7 @@ class PeerGroup:
     def check(self):
         """Raise if a peer_sum on this rank timed out waiting for a peer."""
         err = np.zeros(1, np.uint32)
+        RT.lib().dpia_device_sync(self.device)   # after every launch queued on any stream
         RT.lib().dpia_memcpy_dtoh(self.device, err.ctypes.data_as(ctypes.c_void_p),
                                   self.local + self.nbytes - SLOT_BYTES, 4, None)
         if err[0]:
@@ -99,6 +100,52 @@ class PeerGroup:
             RT.lib().dpia_free(self.device, self.local)
             self.local = 0
         self.boxes.free()
+
+
+def local_twin(exe, prog):
+    """The program of `exe` built without the fused cross-GPU combine, with
+    the same geometry and sizes, reading `exe`'s input buffers: one launch
+    leaves this rank's own partial in its `out`."""
+    from .api import executable
+    twin = executable(prog, exe.geometry, exe.sigma, float_mode=exe.float_mode, device=exe.device)
+    for n, _d in exe.sig.inputs:
+        twin.bind(n, exe.buffers[n])
+    return twin
+
+
+def rank_order_sum(parts: List[np.ndarray]) -> np.ndarray:
+    """parts[0] + parts[1] + ... in rank order, in the partials' own dtype --
+    the association dpia::peer_sum uses, so the kernel's total must equal it
+    bit for bit."""
+    acc = parts[0].copy()
+    for p in parts[1:]:
+        acc = (acc + p).astype(parts[0].dtype)
+    return acc
+
+
+def cross_check(exe, twin, stream, allgather: Callable[[bytes], List[bytes]]) -> dict:
+    """Check the fused combine against the partials it combines.
+
+    Every rank launches `twin` (no combine) to get its own partial, the
+    partials are gathered over the host process group and summed in rank
+    order; then `exe` (the fused combine) runs once and its total must equal
+    that sum bit for bit on every rank.  Returns the evidence; raises
+    PeerError if a peer never published (the kernel's error word)."""
+    twin.launch(stream)
+    stream.sync()
+    part = twin.download("out", stream)
+    stream.sync()
+    parts = [np.frombuffer(b, part.dtype).copy() for b in allgather(part.tobytes())]
+    want = rank_order_sum(parts)
+    exe.launch(stream)
+    stream.sync()
+    exe.peer.check()
+    got = exe.download("out", stream)
+    stream.sync()
+    exact = bool(np.array_equal(got.view(np.uint8), want.view(np.uint8)))
+    return {"peer_total": [float(v) for v in got], "rank_order_sum": [float(v) for v in want],
+            "partials": [float(p[0]) for p in parts], "bit_exact": exact,
+            "abs_sum": float(sum(np.abs(p.astype(np.float64)).sum() for p in parts))}
 
 
 def mailbox_bytes(world: int, n_scalars: int) -> int:

@@ -282,13 +282,24 @@ class DeviceBuffer:
                                _sh(stream))
 
     def download(self, out, stream=None):
+        """Copy to host.  Without a stream the copy is ordered after ALL work
+        queued on the device (the launch streams are non-blocking and do not
+        synchronise with the legacy stream), and complete on return."""
         assert out.flags["C_CONTIGUOUS"] and out.nbytes <= self.nbytes
+        if stream is None:
+            lib().dpia_device_sync(self.device)
         lib().dpia_memcpy_dtoh(self.device, out.ctypes.data_as(ctypes.c_void_p), self.ptr, out.nbytes,
                                _sh(stream))
+        if stream is None:
+            lib().dpia_device_sync(self.device)
         return out
 
     def zero(self, stream=None):
+        """Zero the buffer: asynchronously on `stream`, or -- without one --
+        complete before returning, so launches on any stream see the zeros."""
         lib().dpia_memset(self.device, self.ptr, 0, self.nbytes, _sh(stream))
+        if stream is None:
+            lib().dpia_device_sync(self.device)
 
 
 class DeviceView:

@@ -71,6 +71,7 @@ class ShardedReduction:
         self.shard = shard_plan(total_elems, chunk, world, rank)
         text = asum_program(L, K) if kind == "asum" else dot_program(L, K)
         prog = compile_program(text, name=f"{kind}_shard")
+        self.prog = prog
         n = self.shard.chunks
         self.peer = None
         if combine == "peer":
@@ -94,5 +95,9 @@ class ShardedReduction:
         if allreduce and self.combine == "nccl":
             RT.lib().dpia_nccl_allreduce(self.exe.buffers["out"].ptr, 1, 0, stream.handle)
 
-    def result(self) -> float:
-        return float(self.exe.download("out")[0])
+    def result(self, stream=None) -> float:
+        """The (combined) result; ordered after the launches on `stream`, or
+        after all device work when no stream is given."""
+        if stream is not None:
+            stream.sync()
+        return float(self.exe.download("out", stream)[0])

@@ -36,7 +36,8 @@ import numpy as np
 from . import layout as LY
 from . import runtime as RT
 from .dtypes import Array, ExpT, Num
-from .terms import Lam, Lit, Var, free_vars, unapply
+from .sizes import nat as nat_of
+from .terms import Lam, Lit, Var, free_vars, substitute, unapply
 
 MAPS = {"map", "mapGlobal", "mapWorkgroup", "mapLocal", "mapSeq", "mapWorkgroup1", "mapLocal1"}
 WRAPS = {"join", "toGlobal", "toLocal", "toPrivate"}
@@ -85,16 +86,32 @@ def _is_view(p, params) -> bool:
     return False
 
 
-def _chunk_local(p, params) -> bool:
+def _mentions_size(p, nat: str) -> bool:
+    """Whether the size variable occurs anywhere in p (binder annotations,
+    type arguments, literal types): substituting it must leave p unchanged."""
+    return substitute(p, nat, _PROBE) != p
+
+
+_PROBE = nat_of(1 << 40)
+
+
+def _chunk_local(p, params, nat: str) -> bool:
+    """The body maps a closed F over constant-size chunks of a view of the
+    inputs.  F and the split factor must not depend on the size parameter:
+    a shard specialises it to n / K, which would otherwise change the
+    chunks themselves (and so every per-chunk result), not just their
+    number."""
     body = _strip(p, WRAPS)
     u = unapply(body)
     if u is None or u[0] not in MAPS:
         return False
     f, e = u[2][-2], u[2][-1]
-    if free_vars(f) & set(params):
+    if free_vars(f) & set(params) or _mentions_size(f, nat):
         return False
     s = unapply(e)
     if s is not None and s[0] == "split":
+        if s[1] and nat in getattr(s[1][0], "free", frozenset()):
+            return False
         e = s[2][-1]
     return _is_view(e, params)
 
@@ -119,12 +136,12 @@ def shard_spec(prog) -> ShardSpec:
     out = prog.out_type
     body = src.body
     if isinstance(out, Array) and _linear(out.size, nat):
-        if _chunk_local(body, params):
+        if _chunk_local(body, params, nat):
             return ShardSpec(nat, "map")
         raise ShardError("the body is not a map over contiguous chunks of its inputs")
     u = unapply(body)
     if (isinstance(out, Num) and u is not None and u[0] in ("reduce", "reduceLocal", "reduceSeq") and _is_plus(u[2][0])
-            and isinstance(u[2][1], Lit) and u[2][1].value == 0 and _chunk_local(u[2][2], params)):
+            and isinstance(u[2][1], Lit) and u[2][1].value == 0 and _chunk_local(u[2][2], params, nat)):
         return ShardSpec(nat, "sum")
     raise ShardError("only chunk-local maps and (+)/0 reductions of them are sharded")
 

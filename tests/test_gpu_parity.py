@@ -336,13 +336,19 @@ FUZZ_FLOAT = load_golden("fuzz_float.json")
 @pytest.mark.parametrize("case", FUZZ_FLOAT, ids=lambda c: f"fseed{c['seed']}")
 def test_reference_fuzz_programs_fp32(case):
     """Kernel-legal reference fuzz programs in float mode: the fp32 kernel
-    against the reference's float64 result (short expressions of values in
-    [-2, 2]: |got - want| <= 1e-3 + 1e-4 |want|)."""
+    against the reference's float64 result with the normwise bound
+    |got - want| <= 1e-5 * sum|terms| per output (sum|terms| propagated by
+    oracle.dpia_eval.eval_with_bounds, whose values equal the reference's
+    result; input rounding to fp32 alone reaches 6e-8 of the bound)."""
+    from oracle.dpia_eval import eval_with_bounds
     prog = compile_program(case["text"])
     inputs = {k: from_json(v) for k, v in case["inputs"].items()}
-    got = run_program_cuda(prog, inputs, launch=(2, 4), float_mode=True, flat=True)
-    want = flatten_value(from_json(case["expected"]))
-    assert np.allclose(np.asarray(got, np.float64), np.asarray(want, np.float64), rtol=1e-4, atol=1e-3)
+    got = np.asarray(run_program_cuda(prog, inputs, launch=(2, 4), float_mode=True, flat=True),
+                     np.float64)
+    want = np.asarray(flatten_value(from_json(case["expected"])), np.float64)
+    vals, bounds = eval_with_bounds(prog.source.body, inputs, {})
+    assert np.allclose(vals, want, rtol=1e-12, atol=1e-12)
+    assert np.all(np.abs(got - want) <= 1e-5 * np.asarray(bounds, np.float64)), (got, want, bounds)
 
 
 def test_executable_run_pinned_repeated():

@@ -41,6 +41,21 @@ TRANSPOSED = """
   (transpose (split n xs))))
 """
 
+# the chunk is n elements: a shard at n / K would multiply half-chunks
+NAT_CHUNK = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(reduceLocal (+) 0 (mapGlobal (lam (c (exp (array n num))) (reduceSeq (lam x (lam a (* x a))) 1 c))
+  (split n xs)))
+"""
+# constant chunks, but the per-chunk function's types mention n
+NAT_BODY = """
+(nat n)
+(param xs (exp (array (* n 8) num)))
+(join (mapGlobal (lam (c (exp (array 8 num)))
+  (mapSeq (lam (x (exp num)) (+ x (reduce (+) 0 (as (array n num) 1))))  c)) (split 8 xs)))
+"""
+
 
 @pytest.mark.parametrize("text,kind", [
     (dot_program(32, 2), "sum"), (asum_program(32, 2), "sum"), (SQUARE_MAP, "map"), (CHUNK_MAP, "map")])
@@ -49,11 +64,14 @@ def test_shard_spec_accepts(text, kind):
 
 
 @pytest.mark.parametrize("text", [gemv_config(1024, 1024).text, mm_config(128, 128, 128).text,
-                                  scal_config().text, PRODUCT, OFFSET_SUM, TRANSPOSED])
+                                  scal_config().text, PRODUCT, OFFSET_SUM, TRANSPOSED,
+                                  NAT_CHUNK, NAT_BODY])
 def test_shard_spec_rejects(text):
     """No size parameter (gemv, mm), an unsplittable input (scal's alpha
-    splat), a combine that is not (+)/0, and a map over a transposed view
-    (its chunks interleave the input) are refused, never split."""
+    splat), a combine that is not (+)/0, a map over a transposed view
+    (its chunks interleave the input), and chunks or per-chunk functions
+    that depend on the size parameter (a shard's n / K would change them)
+    are refused, never split."""
     with pytest.raises(ShardError):
         shard_spec(compile_program(text))
 
