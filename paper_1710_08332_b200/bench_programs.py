@@ -424,10 +424,16 @@ def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Co
     return Config("asum", asum_program(L, K), {"n": n}, (blocks or n, L), bytes=4 * N, flops=2 * N)
 
 
-def gemv_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int = 148 * 8,
+def gemv_config(M: int = 8192, N: int = 8192, L: int = None, blocks: int = None,
                 x_private: bool = False) -> Config:
     """BASELINE config 3: row per work-group, x staged with toLocal
-    (x_private=True: the toPrivate register-staged variant, `gemv_xprivate`)."""
+    (x_private=True: the toPrivate register-staged variant, `gemv_xprivate`).
+    Geometry: one wave of resident work-groups on the 148 SMs -- toLocal
+    holds x (32 KiB) in shared memory, so 4 groups of 512 fit per SM (592);
+    the register-staged variant runs 8 groups of 256 per SM (1184)
+    (profiles/r01e_gemv_sweep.txt)."""
+    L = L or min(256 if x_private else 512, N // 4)
+    blocks = blocks or (148 * 8 if x_private else 148 * 4)
     return Config("gemv", gemv_program(M, N, L, x_private), {}, (min(blocks, M), L),
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 

@@ -7,6 +7,7 @@ Accepts the reference's `.dpia` language unchanged (`SRC/parser.py:57-259`):
 """
 from __future__ import annotations
 
+import re
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Tuple, Union
 
@@ -37,82 +38,85 @@ class Token:
 
 
 SExp = Union[Token, list]
-_DELIMS = set(" \t\r\n();")
+
+# one alternation, tried in order at every position: layout, a `;;` line
+# comment, a parenthesis, or an atom (anything up to the next delimiter)
+_LEXEME = re.compile(r"(?P<nl>\n)|(?P<ws>[ \t\r]+)|(?P<comment>;;[^\n]*)|(?P<paren>[()])"
+                     r"|(?P<atom>[^ \t\r\n();]+)")
 
 
 def tokenize(text: str) -> List[Token]:
+    """Atoms and parentheses with 1-based line / column positions."""
     out: List[Token] = []
-    line, col, i, n = 1, 1, 0, len(text)
-    while i < n:
-        ch = text[i]
-        if ch == "\n":
-            line, col, i = line + 1, 1, i + 1
-        elif ch in " \t\r":
-            col, i = col + 1, i + 1
-        elif ch == ";" and text.startswith(";;", i):
-            while i < n and text[i] != "\n":
-                i += 1
-        elif ch in "()":
-            out.append(Token(ch, line, col))
-            col, i = col + 1, i + 1
-        else:
-            j = i
-            while j < n and text[j] not in _DELIMS:
-                j += 1
-            if j == i:
-                raise ParseError(f"stray character {ch!r}", line, col)
-            out.append(Token(text[i:j], line, col))
-            col, i = col + (j - i), j
+    line, line_start, pos = 1, 0, 0
+    while pos < len(text):
+        m = _LEXEME.match(text, pos)
+        if m is None:      # a lone ';' -- the only character no lexeme accepts
+            raise ParseError(f"unexpected character {text[pos]!r}", line, pos - line_start + 1)
+        kind = m.lastgroup
+        if kind == "nl":
+            line, line_start = line + 1, m.end()
+        elif kind in ("paren", "atom"):
+            out.append(Token(m.group(), line, pos - line_start + 1))
+        pos = m.end()
     return out
 
 
 def read_all(text: str) -> List[SExp]:
-    top: List[SExp] = []
-    stack: List[list] = [top]
-    for tok in tokenize(text):
-        if tok.text == "(":
-            stack.append([])
-        elif tok.text == ")":
-            if len(stack) == 1:
-                raise ParseError("unbalanced ')'", tok.line, tok.col)
-            done = stack.pop()
-            stack[-1].append(done)
-        else:
-            stack[-1].append(tok)
-    if len(stack) != 1:
-        raise ParseError("unbalanced '(' at end of input")
-    return top
+    """The top-level forms: nested lists of tokens."""
+    toks = tokenize(text)
+
+    def form(k: int):
+        """The form starting at toks[k] and the index after it."""
+        if toks[k].text != "(":
+            return toks[k], k + 1
+        opener, items, k = toks[k], [], k + 1
+        while k < len(toks) and toks[k].text != ")":
+            item, k = form(k)
+            items.append(item)
+        if k == len(toks):
+            raise ParseError(f"input ends inside the form opened at {opener.line}:{opener.col}")
+        return items, k + 1
+
+    forms, k = [], 0
+    while k < len(toks):
+        if toks[k].text == ")":
+            raise ParseError("')' closes nothing", toks[k].line, toks[k].col)
+        f, k = form(k)
+        forms.append(f)
+    return forms
 
 
 def position(sx: SExp) -> Tuple[int, int]:
-    while isinstance(sx, list):
-        if not sx:
-            return (0, 0)
-        sx = sx[0]
-    return (sx.line, sx.col)
+    """(line, column) of the first token inside sx; (0, 0) for ()."""
+    first = sx
+    while isinstance(first, list) and first:
+        first = first[0]
+    return (first.line, first.col) if isinstance(first, Token) else (0, 0)
 
 
 def error_at(sx: SExp, msg: str, cls=ParseError) -> ParseError:
-    line, col = position(sx)
-    return cls(msg, line, col)
+    return cls(msg, *position(sx))
 
 
 def head_of(sx: SExp) -> Optional[str]:
-    if isinstance(sx, list) and sx and isinstance(sx[0], Token):
-        return sx[0].text
-    return None
+    """The operator atom of a form, if it has one."""
+    return sx[0].text if isinstance(sx, list) and sx and isinstance(sx[0], Token) else None
+
+
+_INT = re.compile(r"[+-]?\d+")
 
 
 def number_of(sx: SExp):
-    """int or float literal value of a token, else None."""
+    """The int or float a token spells, else None."""
     if not isinstance(sx, Token):
         return None
-    for conv in (int, float):
-        try:
-            return conv(sx.text)
-        except ValueError:
-            pass
-    return None
+    if _INT.fullmatch(sx.text):
+        return int(sx.text)
+    try:
+        return float(sx.text)
+    except ValueError:
+        return None
 
 
 # ---------------------------------------------------------------- types

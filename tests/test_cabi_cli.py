@@ -234,3 +234,15 @@ def test_reference_cpu_path_computes_the_workloads():
     lib.gemv(out.ctypes.data, A.ctypes.data, x.ctypes.data)
     want = A.astype(np.float64) @ x
     assert np.all(np.abs(out - want) <= 1e-4 * (np.abs(A) @ np.abs(x)))
+
+
+def test_cli_fuzz_arguments_and_report(tmp_path):
+    """CPU: a missing corpus is a parse-class failure (exit 2); the JUnit
+    writer emits one testcase per program with its failure message."""
+    import xml.etree.ElementTree as ET
+    from paper_1710_08332_b200.cli import Status, _junit, main
+    assert main(["fuzz", "--corpus", str(tmp_path / "nope.json")]) == Status.PARSE
+    _junit(tmp_path / "r.xml", [("seed-0", None), ("seed-1", "GPU [1] != reference [2]")])
+    root = ET.parse(tmp_path / "r.xml").getroot()
+    assert root.get("tests") == "2" and root.get("failures") == "1"
+    assert root.findall("testcase")[1].find("failure").get("message").startswith("GPU")

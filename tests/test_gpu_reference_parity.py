@@ -34,7 +34,10 @@ TOL = 1e-4   # normwise fp32 bound, SURVEY.md 8c
 
 
 def golden(case):
-    with open(os.path.join(HERE, "golden", "fullsize", case + ".json")) as f:
+    path = os.path.join(HERE, "golden", "fullsize", case + ".json")
+    if not os.path.exists(path):
+        pytest.fail(f"{path} missing: run tests/golden/make_fullsize.py {case} where the reference is")
+    with open(path) as f:
         return json.load(f)
 
 
