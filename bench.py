@@ -127,12 +127,56 @@ def ffma_peak(device, stream):
 
 
 def ncu_traffic(workload):
-    """Per-launch DRAM bytes of the dominant kernel from a committed ncu capture."""
+    """Per-launch DRAM bytes of the dominant kernel from a committed ncu
+    capture (the fallback of live_traffic)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             return json.load(f).get(workload)
     except (OSError, ValueError):
         return None
+
+
+def live_traffic(workload, kernel, timeout=240):
+    """DRAM bytes (read + write) of one launch of `kernel`, measured in this
+    run: ncu profiles a child process that builds the same workload and
+    launches it after an L2 scrub (`--traffic-child`), outside every timed
+    region.  Returns (bytes or None, source)."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--csv",
+           "--print-units", "base", "-k", f"regex:^{kernel}$", "--launch-skip", "2",
+           "--launch-count", "1", sys.executable, os.path.abspath(__file__), "--traffic-child",
+           "--workload", workload]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+    except (OSError, subprocess.TimeoutExpired) as e:
+        return ncu_traffic(workload), f"committed ncu capture (live ncu failed: {type(e).__name__})"
+    vals = {}
+    for ln in r.stdout.splitlines():
+        cells = [c.strip('"') for c in ln.split('","')]
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            if name in cells:
+                try:
+                    vals[name] = float(cells[-1].strip('"').replace(",", ""))
+                except ValueError:
+                    pass
+    if len(vals) == 2:
+        return int(sum(vals.values())), "live: ncu dram__bytes_read.sum + dram__bytes_write.sum, one launch"
+    return ncu_traffic(workload), f"committed ncu capture (live ncu rc={r.returncode}, no metrics parsed)"
+
+
+def traffic_child(workload):
+    """The process live_traffic profiles: the workload's program, inputs and
+    launch exactly as measured, three launches each after an L2 scrub."""
+    RT.init(0)
+    stream = RT.Stream(0)
+    cfg, exe, inputs, prepare, prog = make_workload(workload, 0)
+    prepare(stream)
+    for _ in range(3):
+        RT.lib().dpia_l2_flush(0, stream.handle)
+        exe.launch(stream)
+    stream.sync()
+    return 0
 
 
 class Clocks:
@@ -538,11 +582,17 @@ def main():
     ap.add_argument("--workload", default="asum")
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--traffic", choices=["live", "committed"], default="live",
+                    help="roofline.traffic from an ncu run of the same workload made now "
+                         "(after the timed regions), or from profiles/ncu_traffic.json")
+    ap.add_argument("--traffic-child", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--combine", choices=["peer", "nccl"], default="peer",
                     help="cross-GPU combine of the partial sums (N > 1): inside the kernel over "
                          "NVLink (peer) or a 4-byte ncclAllReduce after it")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.traffic_child:
+        return traffic_child(args.workload)
 
     if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
         # `python bench.py --gpus N` without a launcher: one process per GPU
@@ -674,7 +724,7 @@ def main():
             value = world * cfg.flops / (mean_ms * 1e-3) / 1e9
             roof = {"bound": "fp32", "achieved": round(achieved, 2), "peak": round(fp32[0], 2),
                     "unit": "TFLOP/s", "frac": round(achieved / fp32[0], 4),
-                    "traffic": ncu_traffic(workload), "peak_source": fp32[1],
+                    "traffic": None, "peak_source": fp32[1],
                     "algorithmic_flops_per_launch": cfg.flops, "kernel_ms": round(kmean, 5)}
             meas, inner = ffma_peak(device, stream)
             roof["measured_ffma2_peak"] = meas
@@ -688,13 +738,23 @@ def main():
             value = world * cfg.bytes / (mean_ms * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                     "unit": "GB/s", "frac": round(achieved / peak, 4),
-                    "traffic": ncu_traffic(workload),
+                    "traffic": None,
                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                     "algorithmic_bytes_per_launch": cfg.bytes, "kernel_ms": round(kmean, 5)}
             if workload in ("asum", "dot", "gemv"):
                 sol = read_sol(device, cfg.bytes, stream)
                 roof["size_matched_read_sol_gbs"] = sol
                 roof["frac_of_size_matched_sol"] = round(achieved / sol, 4)
+        if world == 1:
+            # DRAM traffic of the same kernel, measured after the timed region
+            if args.traffic == "live":
+                t, tsrc = live_traffic(workload, exe.kernel_names()[0])
+            else:
+                t, tsrc = ncu_traffic(workload), "committed ncu capture (profiles/ncu_traffic.json)"
+            roof["traffic"] = t
+            roof["traffic_source"] = tsrc
+            if t:
+                roof["traffic_over_algorithmic"] = round(t / cfg.bytes, 4)
         res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
                "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
                "value": value, "roofline": roof}

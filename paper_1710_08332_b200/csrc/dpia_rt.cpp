@@ -531,6 +531,18 @@ static int load_helper(int device, const char* src, const char* name, CUmodule* 
   return 0;
 }
 
+// grid of the runtime's own streaming helpers (L2 scrub, hash fill): 8
+// resident blocks per SM over the device's SM count (148 on a B200)
+static int helper_blocks(int device) {
+  CUdevice d;
+  int sms = 0;
+  if (drv::cuDeviceGet(&d, device) != CUDA_SUCCESS ||
+      drv::cuDeviceGetAttribute(&sms, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, d) != CUDA_SUCCESS ||
+      sms <= 0)
+    sms = 148;
+  return sms * 8;
+}
+
 int dpia_l2_flush(int device, void* stream) {
   if (int e = bind(device)) return e;
   if (!g_flush_buf[device]) {
@@ -548,7 +560,7 @@ int dpia_l2_flush(int device, void* stream) {
   CUdeviceptr sink = g_flush_buf[device] + g_flush_bytes[device];
   unsigned long long n = g_flush_bytes[device] / 16;
   void* args[] = {&g_flush_buf[device], &n, &sink};
-  CU(drv::cuLaunchKernel(g_scrub_fn[device], 148 * 8, 1, 1, 512, 1, 1, 0,
+  CU(drv::cuLaunchKernel(g_scrub_fn[device], helper_blocks(device), 1, 1, 512, 1, 1, 0,
                          static_cast<CUstream>(stream), args, nullptr));
   return 0;
 }
@@ -575,7 +587,7 @@ int dpia_fill_hash_f32(int device, uint64_t dptr, uint64_t count, uint64_t offse
   }
   unsigned long long n = count, off = offset;
   void* args[] = {&dptr, &n, &off, &seed, &lo, &hi};
-  CU(drv::cuLaunchKernel(g_fill_fn[device], 148 * 8, 1, 1, 256, 1, 1, 0,
+  CU(drv::cuLaunchKernel(g_fill_fn[device], helper_blocks(device), 1, 1, 256, 1, 1, 0,
                     static_cast<CUstream>(stream), args, nullptr));
   return 0;
 }
