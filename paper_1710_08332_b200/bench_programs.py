@@ -410,8 +410,10 @@ def dot_literal_program(chunk: int = 1024) -> str:
 """
 
 
-def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 128) -> Config:
-    """One work-item per chunk: N / chunk work-items in groups of L."""
+def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 32) -> Config:
+    """One work-item per chunk: N / chunk work-items in groups of L (one
+    warp per group spreads the 16384 work-items over every SM;
+    profiles/r02_litgeo.txt)."""
     n = N // chunk
     return Config("dot_literal", dot_literal_program(chunk), {"n": n}, (n // L, L),
                   bytes=8 * N, flops=2 * N)

@@ -51,6 +51,8 @@ from .index import Ix, div, ix, mod, render
 
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "dpia_device.cuh")
 UNROLL_LIMIT = 64
+# partial unroll factor of longer per-work-item sequential loops
+SEQ_UNROLL = 8
 # work-item loops of a pipelined staging may take up to this many iterations
 # per thread (unrolled into guarded copies, one prefetch register set each)
 PF_MAX_COPIES = 4
@@ -1142,6 +1144,12 @@ class KernelEmitter:
         else:
             if level == "seq" and trip is not None and trip <= UNROLL_LIMIT:
                 self.line("#pragma unroll")
+            elif level == "seq" and trip is not None and self.per_thread:
+                # a long sequential fold inside one work-item (reduceSeq over
+                # a large chunk, or a single-thread tail): partial unrolling
+                # keeps several independent loads in flight; the fold's order
+                # is unchanged
+                self.line(f"#pragma unroll {SEQ_UNROLL}")
             self.open(f"for ({ctype} {v} = {start}; {v} < {bound}; {v} += {stride})")
         enter(single)
 
