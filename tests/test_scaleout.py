@@ -244,3 +244,123 @@ def test_tile_schedule(rows, cols):
     ready = [max(pos[("A", i)], pos[("B", j)]) for i, j in tiles]
     assert ready == sorted(ready)
     assert order[0] == ("A", 0) and ("B", 0) in order[:2 + rows // cols]
+
+
+def _two_gpu_worker(rank, world, port, kind, q):
+    """One rank per DISTINCT GPU: the fused combine over real NVLink P2P,
+    checked against the rank-order sum of the gathered partials (bit-exact)
+    and against NCCL's all-reduce of the same partials."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import ctypes
+
+    import torch
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world)
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.peer import cross_check, local_twin, torch_allgather
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    try:
+        RT.init(rank)
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            RT.lib().dpia_nccl_unique_id(uid)
+        obj = [bytes(uid.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        RT.lib().dpia_nccl_init(rank, world, rank, obj[0])
+        run = ShardedReduction(kind, 1 << 28, world, rank, device=rank, combine="peer",
+                               allgather=torch_allgather)
+        st = RT.Stream(rank)
+        run.fill_inputs(st)
+        st.sync()
+        ev = cross_check(run.exe, local_twin(run.exe, run.prog), st, torch_allgather)
+        buf = RT.DeviceBuffer(16, rank)
+        buf.upload(np.array([ev["partials"][rank], 0, 0, 0], np.float32))
+        RT.lib().dpia_nccl_allreduce(buf.ptr, 1, 0, st.handle)
+        st.sync()
+        v = np.zeros(4, np.float32)
+        buf.download(v)
+        q.put((rank, ev["bit_exact"], ev["peer_total"][0], float(v[0]), ev["abs_sum"]))
+        dist.barrier()
+        run.peer.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), None, None, None))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["asum", "dot"])
+def test_peer_combine_two_distinct_gpus(kind):
+    """The fused cross-GPU combine across two physical GPUs (skipped on a
+    one-GPU box; the shared-GPU test above covers the protocol there)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_two_gpu_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+    for r in (0, 1):
+        exact, peer, nccl, absum = res[r]
+        assert exact is True, res
+        assert abs(peer - nccl) <= 1e-6 * absum
+    assert res[0][1] == res[1][1]
+    want = (blas_np.hashed_asum(1 << 28, SEEDS["x"]) if kind == "asum"
+            else blas_np.hashed_dot(1 << 28, SEEDS["x"], SEEDS["y"]))
+    assert blas_np.within(res[0][1], want[0], want[1])
+
+
+def test_rank_order_sum_is_the_kernels_association():
+    """CPU: peer.rank_order_sum adds in rank order in the partials' dtype
+    (what dpia::peer_sum does), which differs from a float64 sum."""
+    from paper_1710_08332_b200.peer import rank_order_sum
+    parts = [np.array([1e8], np.float32), np.array([1.0], np.float32), np.array([-1e8], np.float32)]
+    got = rank_order_sum(parts)
+    assert got.dtype == np.float32 and got[0] == np.float32(np.float32(1e8 + 1.0) - 1e8)
+    assert rank_order_sum([np.array([3], np.int64), np.array([4], np.int64)])[0] == 7
+
+
+def _cross_worker(rank, world, port, kind, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1710_08332_b200 import runtime as RT
+    from paper_1710_08332_b200.peer import cross_check, local_twin, torch_allgather
+    from paper_1710_08332_b200.scaleout import ShardedReduction
+    try:
+        run = ShardedReduction(kind, 1 << 24, world, rank, device=0, combine="peer",
+                               allgather=torch_allgather)
+        st = RT.Stream(0)
+        run.fill_inputs(st)
+        st.sync()
+        ev = cross_check(run.exe, local_twin(run.exe, run.prog), st, torch_allgather)
+        q.put((rank, ev["bit_exact"], ev["peer_total"][0], ev["rank_order_sum"][0]))
+        dist.barrier()
+        run.peer.close()
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e), None, None))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["asum", "dot"])
+def test_cross_check_two_ranks_sharing_one_gpu(kind):
+    """peer.cross_check (bench.py's agreement gate at N > 1): each rank's
+    combine-free twin gives its partial, and the fused combine's total is
+    bit-identical to the rank-order sum of the gathered partials."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_cross_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r[0], r[1:]) for r in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+    for r in (0, 1):
+        assert res[r][0] is True, res
+        assert res[r][1] == res[r][2]
+    assert res[0][1] == res[1][1]
