@@ -17,6 +17,8 @@
 //                          order (replaces ncclAllReduce of the partials)
 // * dpia::grid_arrive   -- last-block-done detection used to fuse a single
 //                          work-group tail phase into the preceding grid phase
+// * dpia::bulk_stage    -- toLocal staging of a whole input as one TMA bulk
+//                          copy (cp.async.bulk + mbarrier complete_tx)
 //
 // Self-contained: NVRTC compiles it without any system header.
 #pragma once
@@ -258,6 +260,39 @@ __device__ void peer_sum(T* out, int n, const unsigned long long* boxes, int ran
       }
     }
     if (lane == 0) out[k] = acc;
+  }
+}
+
+// Bulk (TMA) staging of `bytes` contiguous bytes global -> shared, issued by
+// thread 0 and completed on an mbarrier in shared memory (used once per
+// block, phase 0): the emitter's lowering of a block-invariant toLocal copy
+// of a whole input.  Every thread returns once the data has landed.  Both
+// addresses are 16-byte aligned and bytes is a multiple of 16, < 2^20.
+__device__ __forceinline__ void bulk_stage(void* smem_dst, const void* gsrc, unsigned bytes,
+                                           unsigned long long* mbar, int tid) {
+  const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(mbar));
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(gsrc), "r"(bytes), "r"(bar)
+        : "memory");
+  }
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar)
+        : "memory");
   }
 }
 

@@ -53,6 +53,10 @@ HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "
 UNROLL_LIMIT = 64
 # partial unroll factor of longer per-work-item sequential loops
 SEQ_UNROLL = 8
+# block-invariant identity stagings of an input into shared memory as one
+# bulk (TMA) copy: KernelEmitter.bulk_stage; DPIA_BULK_STAGE=0 emits the
+# work-item copy loop instead
+BULK_STAGE = os.environ.get("DPIA_BULK_STAGE", "1") != "0"
 # work-item loops of a pipelined staging may take up to this many iterations
 # per thread (unrolled into guarded copies, one prefetch register set each)
 PF_MAX_COPIES = 4
@@ -1167,10 +1171,11 @@ class KernelEmitter:
             for node, d0, fl, c1 in self.invariant_stagings(body, binders):
                 buf = self._declare_local(fl.binder, d0)
                 self.env[fl.binder] = buf
-                # block-uniform context (every thread of the work-group)
-                self.loops.append(Loop("workgroup", dim, "", 1, nat(1), True))
-                self.comm(c1)
-                self.loops.pop()
+                if not self.bulk_stage(c1, buf):
+                    # block-uniform context (every thread of the work-group)
+                    self.loops.append(Loop("workgroup", dim, "", 1, nat(1), True))
+                    self.comm(c1)
+                    self.loops.pop()
                 self.line("__syncthreads();")
                 del self.env[fl.binder]
                 self.hoisted[id(node)] = buf
@@ -1183,6 +1188,50 @@ class KernelEmitter:
             self.comm(body)
 
         self.loop(level, dim, n, ivar, emit_body, bind=(ovar, lambda i: Alias(a, i)))
+
+    def bulk_stage(self, c1: Phrase, buf: Buffer) -> bool:
+        """toLocal staging of a whole input array into a shared buffer of the
+        same layout -- `parforLocal (proj1 t) (lam i o. o := idx x i)` -- as
+        one Blackwell bulk copy (TMA: cp.async.bulk global -> shared,
+        completion counted on an mbarrier) issued by one thread, instead of
+        a copy loop over the work-items.  Used for the block-invariant
+        stagings (hoisted out of the work-group loop).  False when the
+        pattern, the sizes or the alignment do not fit (the loop is emitted)."""
+        if not BULK_STAGE or buf.swz is not None or buf.pad or buf.prefix:
+            return False
+        u = unapply(c1)
+        if u is None or u[0] not in ("parforLocal", "parfor") or len(u[2]) != 2:
+            return False
+        (n, d), (acc, f) = u[1], u[2]
+        if not (isinstance(acc, Proj) and acc.index == 1 and isinstance(acc.target, Var)
+                and acc.target.name == buf.key and isinstance(f, Lam) and isinstance(f.body, Lam)):
+            return False
+        asg = unapply(f.body.body)
+        if asg is None or asg[0] != ":=" or len(asg[2]) != 1 or not isinstance(asg[2][0], PairP):
+            return False
+        dst, src = asg[2][0].fst, asg[2][0].snd
+        rd = unapply(src)
+        if not (isinstance(dst, Var) and dst.name == f.body.binder and rd is not None
+                and rd[0] == "idx" and len(rd[2]) == 2 and isinstance(rd[2][0], Var)
+                and isinstance(rd[2][1], Var) and rd[2][1].name == f.binder):
+            return False
+        x = rd[2][0].name
+        xb = self.env.get(x)
+        if not (isinstance(xb, Buffer) and xb.space == "in" and not xb.prefix):
+            return False
+        dims, elem = split_array(xb.dtype)
+        bdims, belem = split_array(buf.dtype)
+        count = self.nat_int(n)
+        if len(dims) != 1 or len(bdims) != 1 or not isinstance(elem, (Num, Vector)) or elem != belem \
+                or count is None or self.nat_int(dims[0]) != count or self.nat_int(bdims[0]) != count:
+            return False
+        nbytes = count * self._elem_bytes(elem)
+        if nbytes == 0 or nbytes % 16 or nbytes >= (1 << 20):
+            return False
+        off = self.alloc_smem(8)
+        self.line(f"dpia::bulk_stage({buf.cname}, {xb.cname}, {nbytes}u, "
+                  f"reinterpret_cast<unsigned long long*>(dpia_smem + {off}), dpia_tid);")
+        return True
 
     def lint(self, prim, level, dim):
         enclosing = [(lp.level, lp.dim) for lp in self.loops if lp.level not in ("seq",)]
