@@ -142,6 +142,10 @@ def live_traffic(workload, kernel, timeout=240):
     launches it after an L2 scrub (`--traffic-child`), outside every timed
     region.  Returns (bytes or None, source)."""
     import shutil
+    if _under_profiler():
+        # a profiler already wraps this process (e.g. the driver's ncu launch
+        # list): no nested ncu
+        return ncu_traffic(workload), "committed ncu capture (bench.py itself runs under a profiler)"
     ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--csv",
            "--print-units", "base", "-k", f"regex:^{kernel}$", "--launch-skip", "2",
@@ -163,6 +167,13 @@ def live_traffic(workload, kernel, timeout=240):
     if len(vals) == 2:
         return int(sum(vals.values())), "live: ncu dram__bytes_read.sum + dram__bytes_write.sum, one launch"
     return ncu_traffic(workload), f"committed ncu capture (live ncu rc={r.returncode}, no metrics parsed)"
+
+
+def _under_profiler() -> bool:
+    """ncu / compute-sanitizer inject themselves through CUDA_INJECTION64_PATH
+    and an LD_PRELOAD of their process-tree launcher."""
+    pre = os.environ.get("LD_PRELOAD", "")
+    return bool(os.environ.get("CUDA_INJECTION64_PATH")) or "TreeLauncher" in pre or "nsight" in pre
 
 
 def traffic_child(workload):

@@ -54,7 +54,10 @@ def main():
     ys = rng.uniform(0, 1, n * 1024).astype(np.float32)
     for tag, text in (("literal", dot_literal_program()), ("partials-only", PARTIALS)):
         prog = compile_program(text, name="lit")
-        for launch in ((64, 256), (128, 128), (256, 64), (512, 32), (148, 128), (296, 32), (32, 512)):
+        launches = ((64, 256), (128, 128), (256, 64), (512, 32), (148, 128), (296, 32), (32, 512))
+        if "--quick" in sys.argv:
+            launches = ((128, 128), (512, 32))
+        for launch in launches:
             exe = executable(prog, launch, {"n": n}, float_mode=True)
             exe.upload("xs", xs, st)
             exe.upload("ys", ys, st)
