@@ -51,12 +51,6 @@ from .index import Ix, div, ix, mod, render
 
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "dpia_device.cuh")
 UNROLL_LIMIT = 64
-# partial unroll factor of long sequential loops run by a single thread
-# (scope "tail"), or by every work-item (scope "item"; per-item loops that
-# walk a contiguous chunk rely on L1 reuse across iterations, which deeper
-# unrolling defeats -- profiles/r02_litgeo_unroll.txt)
-SEQ_UNROLL = int(os.environ.get("DPIA_SEQ_UNROLL", "8"))
-SEQ_UNROLL_SCOPE = os.environ.get("DPIA_SEQ_UNROLL_SCOPE", "tail")
 # block-invariant identity stagings of an input into shared memory as one
 # bulk (TMA) copy: KernelEmitter.bulk_stage; DPIA_BULK_STAGE=0 emits the
 # work-item copy loop instead
@@ -1152,12 +1146,7 @@ class KernelEmitter:
         else:
             if level == "seq" and trip is not None and trip <= UNROLL_LIMIT:
                 self.line("#pragma unroll")
-            elif level == "seq" and trip is not None and SEQ_UNROLL > 1 and \
-                    (self.single_thread if SEQ_UNROLL_SCOPE == "tail" else self.per_thread):
-                # a long sequential fold in one thread (the top-level reduce
-                # of a fused tail): partial unrolling keeps several
-                # independent loads in flight; the fold's order is unchanged
-                self.line(f"#pragma unroll {SEQ_UNROLL}")
+
             self.open(f"for ({ctype} {v} = {start}; {v} < {bound}; {v} += {stride})")
         enter(single)
 
