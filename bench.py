@@ -685,11 +685,12 @@ def main():
             else:
                 check["combine_used"] = "peer"
         allreduce = None
-        reduces = workload in ("asum", "dot") or workload.startswith("scaleout")
+        reduces = workload in ("asum", "dot", "dot_literal") or workload.startswith("scaleout")
         if world > 1 and exe.peer is None and reduces:
-            # gemv / mm / scal shard with no collective (independent rows)
-            if args.combine != "nccl":
-                raise SystemExit("internal: a reduction without the peer combine needs --combine nccl")
+            # the NCCL combine (--combine nccl, or the fallback of the peer
+            # combine); gemv / mm / scal shard with no collective at all
+            if share:
+                raise SystemExit("internal: ranks sharing one GPU have no NCCL combine")
             outbuf = exe.buffers["out"]
 
             def allreduce(s):  # NCCL sum of the per-rank partial, on our stream
