@@ -178,8 +178,10 @@ def _vector_class(values):
     stack = list(values)
     while stack:
         v = stack.pop()
-        if isinstance(v, (list, tuple)):
-            stack.extend(v)
+        if isinstance(v, list):
+            stack.extend(v[:1])        # arrays are homogeneous: one element says it
+        elif isinstance(v, tuple):
+            stack.extend(v)            # pairs are not
         elif hasattr(v, "items") and not isinstance(v, dict):
             return type(v)
     return None
