@@ -51,6 +51,10 @@ from .index import Ix, div, ix, mod, render
 
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(__file__)), "csrc", "dpia_device.cuh")
 UNROLL_LIMIT = 64
+# sequential folds inside a work-item read unit-stride global data as
+# VEC_WIDTH-wide vectors (KernelEmitter._vec_loop); DPIA_VEC_LOADS=0 disables
+VEC_LOADS = os.environ.get("DPIA_VEC_LOADS", "1") != "0"
+VEC_WIDTH = 4
 # block-invariant identity stagings of an input into shared memory as one
 # bulk (TMA) copy: KernelEmitter.bulk_stage; DPIA_BULK_STAGE=0 emits the
 # work-item copy loop instead
@@ -469,6 +473,8 @@ class KernelEmitter:
         self.for_plans: Dict[int, list] = {}
         self.rotated: Dict[str, str] = {}
         self.hoisted_writes: Set[int] = set()
+        self.vec_vars: Set[str] = set()      # loop counters of VEC_WIDTH-unrolled folds
+        self.vec_hits = 0
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -710,7 +716,30 @@ class KernelEmitter:
 
     def exp(self, p: Phrase, steps: List[Step]) -> str:
         r = self.resolve(p, steps)
-        return r.text if isinstance(r, Ref) else r
+        if isinstance(r, Ref):
+            return self._lane_read(r) or r.text
+        return r
+
+    def _lane_read(self, r: Ref) -> Optional[str]:
+        """Inside a VEC_WIDTH-unrolled sequential fold (`_vec_loop`): a scalar
+        read of a global buffer at flat index W*j + A + c (j the unrolled
+        counter, every other term a multiple of W, 0 <= c < W) becomes lane
+        c of the W-vector at W*j + A.  The W unrolled iterations read the
+        same vector, which the compiler loads once (LDG.128)."""
+        if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global") \
+                or r.buf.swz or r.buf.pad or not isinstance(r.buf.elem, Num):
+            return None
+        W = VEC_WIDTH
+        coef = dict((m, c) for m, c in r.flat.terms)
+        js = [v for v in self.vec_vars if coef.get((v,)) == W]
+        if len(js) != 1:
+            return None
+        lane = coef.get((), 0) % W
+        if lane < 0 or any(c % W for m, c in r.flat.terms if m != ()):
+            return None
+        base = r.flat + ix(-lane) if lane else r.flat
+        self.vec_hits += 1
+        return f"dpia::vload<{self.scalar}, {W}>({r.buf.cname}, {self.r(base)}).v[{lane}]"
 
     def acc(self, p: Phrase, steps: List[Step]) -> Union[Ref, VStore]:
         if isinstance(p, Proj) and p.index == 1 and isinstance(p.target, Var):
@@ -846,6 +875,8 @@ class KernelEmitter:
                                 "not supported")
             if self._fma2_loop(p, targs[0], f):
                 return
+            if self._vec_loop(targs[0], f):
+                return
             cands, rotate = [], False
             if id(p) in self.for_plans:
                 cands, rotate = self.for_plans[id(p)], True
@@ -862,6 +893,48 @@ class KernelEmitter:
             self.combine(targs, args)
             return
         raise CudaError(f"no command clause for {name!r}")
+
+    # ------------------------------------- vector loads in sequential folds
+    def _vec_loop(self, n: Nat, f: Lam) -> bool:
+        """A long sequential loop inside one work-item (a reduceSeq over a
+        contiguous chunk, or the single-thread top-level reduce of a fused
+        tail) that reads global buffers at unit stride: emitted unrolled by
+        VEC_WIDTH, iteration W*j + k reading lane k of one W-wide vector load
+        (`_lane_read`), instead of W scalar loads.  The iterations run in
+        the original order, so the fold's association is unchanged.  Tried
+        on a scratch copy of the output; False (nothing emitted) when no
+        read qualifies."""
+        W = VEC_WIDTH
+        trip = self.nat_int(n)
+        if not VEC_LOADS or not self.per_thread or self.pf is not None or trip is None \
+                or trip % W or trip <= UNROLL_LIMIT:
+            return False
+        mark, ind, hits = len(self.lines), self.ind, self.vec_hits
+        j = self.fresh("j")
+        self.R[j] = trip // W
+        self.open(f"for (int {j} = 0; {j} < {trip // W}; {j} += 1)")
+        self.vec_vars.add(j)
+        self.loops.append(Loop("seq", 0, j, trip // W, nat(trip // W), False))
+        old = self.env.get(f.binder)
+        try:
+            for k in range(W):
+                self.open("")
+                self.env[f.binder] = Val(Idx(n), ixv=ix(j) * W + k)
+                self.comm(f.body)
+                self.close()
+        finally:
+            self.loops.pop()
+            self.vec_vars.discard(j)
+            if old is None:
+                self.env.pop(f.binder, None)
+            else:
+                self.env[f.binder] = old
+        self.close()
+        if self.vec_hits == hits:
+            del self.lines[mark:]
+            self.ind = ind
+            return False
+        return True
 
     # ------------------------------------------------- packed FP32 FMA
     def _fma2_loop(self, p: Phrase, n: Nat, f: Lam) -> bool:

@@ -119,7 +119,12 @@ class Executable:
 
     def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int]):
         """Launch with some parameters re-pointed (device addresses), e.g. at
-        windows of larger buffers -- the row chunks of pipeline.RowPipeline."""
+        windows of larger buffers -- the row chunks of pipeline.RowPipeline.
+        Windows must be 16-byte aligned: the emitted kernels read their
+        buffers with whole-vector loads (asVector, vectorised folds)."""
+        bad = [n for n, q in ptrs.items() if q % 16]
+        if bad:
+            raise ValueError(f"launch_with: windows {bad} are not 16-byte aligned")
         if self.peer is not None:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry

@@ -273,3 +273,27 @@ def test_golden_fixtures_regenerate_identically(tmp_path):
     for name in ("programs.json", "fuzz.json", "fuzz_float.json", "index.json"):
         with open(os.path.join(here, name), "rb") as a, open(tmp_path / name, "rb") as b:
             assert a.read() == b.read(), name
+
+
+def test_vectorised_fold_emission(monkeypatch):
+    """CPU: config 1's literal program reads its chunks and the tail's
+    partials as 4-wide vectors; DPIA_VEC_LOADS=0 restores scalar loads; a
+    transposed (strided) chunk is never vectorised."""
+    from paper_1710_08332_b200 import compile_program
+    from paper_1710_08332_b200.bench_programs import dot_literal_config
+    from paper_1710_08332_b200.cuda import emit as E
+    cfg = dot_literal_config()
+    prog = compile_program(cfg.text)
+    outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    src, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    assert "dpia::vload<float, 4>(xs, 1024 * " in src and "dpia::vload<float, 4>(g_tmp4, 4 * " in src
+    monkeypatch.setattr(E, "VEC_LOADS", False)
+    src0, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    assert "vload" not in src0.split('extern "C"')[1]
+    monkeypatch.setattr(E, "VEC_LOADS", True)
+    strided = compile_program("(nat n)\n(param xs (exp (array (* n 128) num)))\n"
+                              "(mapGlobal (lam (c (exp (array 128 num))) (reduce (+) 0 c))"
+                              " (transpose (split n xs)))")
+    s2, _ = E.emit_cuda(strided.imperative, [("out", strided.out_type)],
+                        [(n, t.data) for n, t in strided.source.params], sigma={"n": 16}, launch=(1, 32))
+    assert "vload" not in s2.split('extern "C"')[1]

@@ -503,3 +503,43 @@ def test_mm_row_pipeline_matches_unchunked(chunks):
     finally:
         for p in pins:
             p.free()
+
+
+VEC_FOLDS = [
+    # per-item chunks read at unit stride: vectorised (chunk a multiple of 4, > 64)
+    ("(nat n)\n(param xs (exp (array (* n 256) num)))\n"
+     "(mapGlobal (lam (c (exp (array 256 num))) (reduce (lam (x (exp num)) (lam (a (exp num)) "
+     "(+ a (* x x)))) 0 c)) (split 256 xs))", {"n": 12}, 256),
+    # the same with a chunk that is not a multiple of 4: scalar loads
+    ("(nat n)\n(param xs (exp (array (* n 130) num)))\n"
+     "(mapGlobal (lam (c (exp (array 130 num))) (reduce (lam (x (exp num)) (lam (a (exp num)) "
+     "(- a x))) 0 c)) (split 130 xs))", {"n": 9}, 130),
+    # a strided (transposed) chunk: no vector loads
+    ("(nat n)\n(param xs (exp (array (* n 128) num)))\n"
+     "(mapGlobal (lam (c (exp (array 128 num))) (reduce (lam (x (exp num)) (lam (a (exp num)) "
+     "(+ (* a 3) x))) 0 c)) (transpose (split n xs)))", {"n": 16}, 128),
+]
+
+
+@pytest.mark.parametrize("text,sigma,chunk", VEC_FOLDS)
+@pytest.mark.parametrize("launch", [(1, 32), (3, 8)])
+def test_vectorised_sequential_folds(text, sigma, chunk, launch):
+    """KernelEmitter._vec_loop: long per-item folds read their chunk as
+    4-wide vectors, in the original order -- int mode bit-exact against the
+    oracle for vectorised, non-multiple-of-4 and strided chunks, and the
+    literal config-1 program with its vectorised single-thread tail."""
+    prog = compile_program(text)
+    n = sigma["n"]
+    xs = _ints(n * chunk, 21)
+    want = flatten_value(eval_phrase(prog.source.body, {"xs": xs}, sigma))
+    got = run_program_cuda(prog, {"xs": xs}, sigma=sigma, launch=launch, float_mode=False, flat=True)
+    assert [int(v) for v in got] == want
+
+
+def test_literal_dot_vectorised_int_exact():
+    from paper_1710_08332_b200.bench_programs import dot_literal_program
+    prog = compile_program(dot_literal_program(256))
+    xs, ys = _ints(64 * 256, 5), _ints(64 * 256, 6)
+    for launch in ((2, 32), (64, 1), (1, 1)):
+        got = run_program_cuda(prog, {"xs": xs, "ys": ys}, sigma={"n": 64}, launch=launch, float_mode=False)
+        assert got == eval_phrase(prog.source.body, {"xs": xs, "ys": ys}, {"n": 64})
