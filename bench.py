@@ -877,7 +877,7 @@ def main():
                                        args.steps},
             "kernels": exe.kernel_names(),
             "cpu_baseline": (_cpu_fields(cpu) if cpu else
-                             {"unavailable": _cpu_unavailable(args.workload, world)}),
+                             {"unavailable": _cpu_unavailable(args.workload, world, args.no_cpu)}),
             "suite": suite}
     for extra in ("combine_check", "ranks"):
         if head.get(extra):
@@ -890,7 +890,9 @@ def _cpu_fields(c):
     return {k: c[k] for k in ("value", "unit", "cores", "cpu_model", "kind", "sample", "march") if k in c}
 
 
-def _cpu_unavailable(workload, world):
+def _cpu_unavailable(workload, world, skipped=False):
+    if skipped:
+        return "not timed in this run (--no-cpu)"
     if world > 1:
         return "the CPU baseline is timed at N = 1 only (rank 0, host cores); see the N = 1 line"
     if ref_lib() is None:

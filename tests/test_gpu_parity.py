@@ -517,7 +517,7 @@ VEC_FOLDS = [
     # a strided (transposed) chunk: no vector loads
     ("(nat n)\n(param xs (exp (array (* n 128) num)))\n"
      "(mapGlobal (lam (c (exp (array 128 num))) (reduce (lam (x (exp num)) (lam (a (exp num)) "
-     "(+ (* a 3) x))) 0 c)) (transpose (split n xs)))", {"n": 16}, 128),
+     "(- x a))) 0 c)) (transpose (split n xs)))", {"n": 16}, 128),
 ]
 
 
