@@ -37,6 +37,7 @@ Additions over the reference backend (SURVEY.md sections 0 and 7):
 from __future__ import annotations
 
 import os
+import re
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Set, Tuple, Union
 
@@ -55,6 +56,11 @@ UNROLL_LIMIT = 64
 # VEC_WIDTH-wide vectors (KernelEmitter._vec_loop); DPIA_VEC_LOADS=0 disables
 VEC_LOADS = os.environ.get("DPIA_VEC_LOADS", "1") != "0"
 VEC_WIDTH = 4
+# ... and keep VEC_PREFETCH vectors per read stream in flight (a rotating
+# register queue refilled VEC_PREFETCH vectors ahead); 0 disables.  A single
+# thread (a fused tail's top-level fold) keeps VEC_PREFETCH_SINGLE.
+VEC_PREFETCH = int(os.environ.get("DPIA_VEC_PREFETCH", "8"))
+VEC_PREFETCH_SINGLE = int(os.environ.get("DPIA_VEC_PREFETCH_SINGLE", "32"))
 # block-invariant identity stagings of an input into shared memory as one
 # bulk (TMA) copy: KernelEmitter.bulk_stage; DPIA_BULK_STAGE=0 emits the
 # work-item copy loop instead
@@ -475,6 +481,7 @@ class KernelEmitter:
         self.hoisted_writes: Set[int] = set()
         self.vec_vars: Set[str] = set()      # loop counters of VEC_WIDTH-unrolled folds
         self.vec_hits = 0
+        self.vec_pf: Optional[dict] = None   # the innermost prefetching fold (`_vec_loop`)
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -725,7 +732,9 @@ class KernelEmitter:
         read of a global buffer at flat index W*j + A + c (j the unrolled
         counter, every other term a multiple of W, 0 <= c < W) becomes lane
         c of the W-vector at W*j + A.  The W unrolled iterations read the
-        same vector, which the compiler loads once (LDG.128)."""
+        same vector, which the compiler loads once (LDG.128).  In a
+        prefetching fold the vector comes from the stream's register queue
+        when A mentions no loop variable bound inside the fold."""
         if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global") \
                 or r.buf.swz or r.buf.pad or not isinstance(r.buf.elem, Num):
             return None
@@ -739,7 +748,16 @@ class KernelEmitter:
             return None
         base = r.flat + ix(-lane) if lane else r.flat
         self.vec_hits += 1
-        return f"dpia::vload<{self.scalar}, {W}>({r.buf.cname}, {self.r(base)}).v[{lane}]"
+        text = self.r(base)
+        pf = self.vec_pf
+        if pf is not None and js[0] == pf["j"]:
+            inner = {lp.var for lp in self.loops[pf["depth"]:]} - {pf["j"]}
+            if not any(re.search(rf"\b{re.escape(v)}\b", text) for v in inner):
+                key = (r.buf.cname, text)
+                if key not in pf["streams"]:
+                    pf["streams"][key] = (f"pfv_{pf['tag']}_{len(pf['streams'])}", r.buf, base)
+                return f"{pf['streams'][key][0]}.v[{lane}]"
+        return f"dpia::vload<{self.scalar}, {W}>({r.buf.cname}, {text}).v[{lane}]"
 
     def acc(self, p: Phrase, steps: List[Step]) -> Union[Ref, VStore]:
         if isinstance(p, Proj) and p.index == 1 and isinstance(p.target, Var):
@@ -831,6 +849,8 @@ class KernelEmitter:
                 return
             rhs = name                       # commit: registers -> shared memory
         buf = target.ref.buf if isinstance(target, VStore) else target.buf
+        if self.vec_pf is not None:
+            self.vec_pf["written"].add(buf.cname)
         if isinstance(target, VStore):
             stmt = (f"dpia::vstore<{self.scalar}, {target.width}>({buf.cname}, "
                     f"{self.r(target.ref.at)}, {rhs});")
@@ -901,20 +921,61 @@ class KernelEmitter:
         tail) that reads global buffers at unit stride: emitted unrolled by
         VEC_WIDTH, iteration W*j + k reading lane k of one W-wide vector load
         (`_lane_read`), instead of W scalar loads.  The iterations run in
-        the original order, so the fold's association is unchanged.  Tried
-        on a scratch copy of the output; False (nothing emitted) when no
-        read qualifies."""
+        the original order, so the fold's association is unchanged.  Each
+        read stream is software-pipelined through a rotating register queue
+        of D vectors (`_emit_vec_loop`) unless the fold writes the buffer.
+        Tried on a scratch copy of the output; False (nothing emitted) when
+        no read qualifies."""
         W = VEC_WIDTH
         trip = self.nat_int(n)
         if not VEC_LOADS or not self.per_thread or self.pf is not None or trip is None \
                 or trip % W or trip <= UNROLL_LIMIT:
             return False
-        mark, ind, hits = len(self.lines), self.ind, self.vec_hits
+        T = trip // W
+        D = VEC_PREFETCH_SINGLE if self.single_thread and not self.loops else VEC_PREFETCH
+        D = 1 << (D.bit_length() - 1) if D > 0 else 0     # a power of two ...
+        while D > 1 and (T % D or T < 2 * D):            # ... dividing T, at most T / 2
+            D //= 2
+        for depth in ([D] if D > 1 else []) + [0]:
+            mark, ind, hits = len(self.lines), self.ind, self.vec_hits
+            ok = self._emit_vec_loop(n, f, T, depth)
+            if ok and self.vec_hits > hits:
+                return True
+            del self.lines[mark:]
+            self.ind = ind
+        return False
+
+    def _emit_vec_loop(self, n: Nat, f: Lam, T: int, D: int) -> bool:
+        """One attempt of `_vec_loop`.  D > 1: the loop is
+            queue_s[d] = V_s(d), d < D                  (prologue)
+            for jo in 0, D, ..: for jd < D (unrolled): j = jo + jd
+                v_s = queue_s[jd]; queue_s[jd] = V_s(j + D) if j + D < T
+                body(j) reading lanes of v_s
+        for every stream s (a buffer and a base offset; V_s(j) its vector at
+        iteration j), so D vectors per stream are in flight while the body
+        folds in order.  False when D > 1 and the body writes a queued
+        buffer or nothing was queued."""
+        W = VEC_WIDTH
         j = self.fresh("j")
-        self.R[j] = trip // W
-        self.open(f"for (int {j} = 0; {j} < {trip // W}; {j} += 1)")
+        self.R[j] = T
+        outer_pf = self.vec_pf
+        pf = None
+        top = len(self.lines)
+        if D > 1:
+            self._k += 1
+            pf = {"j": j, "depth": len(self.loops), "streams": {}, "written": set(), "tag": self._k}
+            self.vec_pf = pf
+            jo, jd = self.fresh("jo"), self.fresh("jd")
+            self.open(f"for (int {jo} = 0; {jo} < {T}; {jo} += {D})")
+            self.line("#pragma unroll")
+            self.open(f"for (int {jd} = 0; {jd} < {D}; {jd} += 1)")
+            self.line(f"const int {j} = {jo} + {jd};")
+            take = len(self.lines)
+        else:
+            self.vec_pf = None
+            self.open(f"for (int {j} = 0; {j} < {T}; {j} += 1)")
         self.vec_vars.add(j)
-        self.loops.append(Loop("seq", 0, j, trip // W, nat(trip // W), False))
+        self.loops.append(Loop("seq", 0, j, T, nat(T), False))
         old = self.env.get(f.binder)
         try:
             for k in range(W):
@@ -925,15 +986,38 @@ class KernelEmitter:
         finally:
             self.loops.pop()
             self.vec_vars.discard(j)
+            self.vec_pf = outer_pf
             if old is None:
                 self.env.pop(f.binder, None)
             else:
                 self.env[f.binder] = old
         self.close()
-        if self.vec_hits == hits:
-            del self.lines[mark:]
-            self.ind = ind
+        if pf is None:
+            return True
+        self.close()
+        streams = list(pf["streams"].values())
+        if not streams or any(b.cname in pf["written"] for _, b, _ in streams):
             return False
+        vt = f"dpia::vec<{self.scalar}, {W}>"
+        pad_in = "  " * (self.ind + 2)
+        body = []
+        for name, b, base in streams:
+            q = name.replace("pfv_", "pfq_")
+            body.append(f"{pad_in}const {vt} {name} = {q}[{jd}];")
+            body.append(f"{pad_in}if ({j} + {D} < {T}) {q}[{jd}] = dpia::vload<{self.scalar}, {W}>"
+                        f"({b.cname}, {self.r(base + ix(W * D))});")
+        self.lines[take:take] = body
+        pad = "  " * self.ind
+        pro = []
+        for name, b, base in streams:
+            pro.append(f"{pad}{vt} {name.replace('pfv_', 'pfq_')}[{D}];")
+        pro.append(f"{pad}#pragma unroll")
+        pro.append(f"{pad}for (int {j} = 0; {j} < {D}; {j} += 1) {{")
+        for name, b, base in streams:
+            pro.append(f"{pad}  {name.replace('pfv_', 'pfq_')}[{j}] = dpia::vload<{self.scalar}, {W}>"
+                       f"({b.cname}, {self.r(base)});")
+        pro.append(f"{pad}}}")
+        self.lines[top:top] = pro
         return True
 
     # ------------------------------------------------- packed FP32 FMA

@@ -297,3 +297,33 @@ def test_vectorised_fold_emission(monkeypatch):
     s2, _ = E.emit_cuda(strided.imperative, [("out", strided.out_type)],
                         [(n, t.data) for n, t in strided.source.params], sigma={"n": 16}, launch=(1, 32))
     assert "vload" not in s2.split('extern "C"')[1]
+
+
+def test_vectorised_fold_prefetch_queue(monkeypatch):
+    """CPU: each read stream of a long sequential fold is software-pipelined
+    through a rotating register queue (VEC_PREFETCH vectors per work-item
+    stream, VEC_PREFETCH_SINGLE for the single-thread tail), refilled D
+    vectors ahead under a bound guard; depth 0 restores the plain
+    vectorised fold, and a depth that does not divide the trip shrinks."""
+    from paper_1710_08332_b200 import compile_program
+    from paper_1710_08332_b200.bench_programs import dot_literal_config
+    from paper_1710_08332_b200.cuda import emit as E
+    cfg = dot_literal_config()
+    prog = compile_program(cfg.text)
+    outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    monkeypatch.setattr(E, "VEC_PREFETCH", 8)
+    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 32)
+    src, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    body = src.split('extern "C"')[1]
+    # two chunk streams (xs, ys) of depth 8, one tail stream of depth 32
+    assert body.count("[8];") == 2 and body.count("[32];") == 1
+    assert "+ 8 < 256) pfq_" in body and "+ 32 < 4096) pfq_" in body
+    assert "4 * j_" in body and "+ 32);" in body and "+ 128);" in body   # 4 * D scalars ahead
+    monkeypatch.setattr(E, "VEC_PREFETCH", 0)
+    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 0)
+    src0, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    assert "pfq_" not in src0 and "dpia::vload<float, 4>(xs, 1024 * " in src0
+    monkeypatch.setattr(E, "VEC_PREFETCH", 24)     # 256 % 24 != 0 -> 16 (a divisor, <= T/2)
+    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 32)
+    src3, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    assert "+ 12 < 256)" not in src3 and "+ 16 < 256) pfq_" in src3
