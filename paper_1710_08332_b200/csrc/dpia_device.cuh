@@ -19,6 +19,10 @@
 //                          work-group tail phase into the preceding grid phase
 // * dpia::bulk_stage    -- toLocal staging of a whole input as one TMA bulk
 //                          copy (cp.async.bulk + mbarrier complete_tx)
+// * dpia::vload32       -- one 32-byte (sm_100 LDG.E.256) vector load: the
+//                          register queues of a work-item's sequential fold
+// * dpia::ring_*        -- a single thread's shared-memory ring of TMA bulk
+//                          copies (the top-level sequential fold of a tail)
 //
 // Self-contained: NVRTC compiles it without any system header.
 #pragma once
@@ -292,6 +296,78 @@ __device__ __forceinline__ void bulk_stage(void* smem_dst, const void* gsrc, uns
         " selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(bar)
+        : "memory");
+  }
+}
+
+// ------------------------------------------------------ 32-byte loads
+// One 256-bit global load (sm_100: LDG.E.ENL2.256) of W = 32 / sizeof(T)
+// consecutive scalars at p + i, 32-byte aligned.  NC: the buffer is read-only
+// for the whole kernel (a const __restrict__ input): the non-coherent path.
+template <bool NC>
+__device__ __forceinline__ vec<float, 8> vload32(const float* p, long long i) {
+  vec<float, 8> r;
+  if (NC)
+    asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7]) : "l"(p + i));
+  else
+    asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]),
+                   "=f"(r.v[5]), "=f"(r.v[6]), "=f"(r.v[7]) : "l"(p + i) : "memory");
+  return r;
+}
+template <bool NC>
+__device__ __forceinline__ vec<long long, 4> vload32(const long long* p, long long i) {
+  vec<long long, 4> r;
+  if (NC)
+    asm volatile("ld.global.nc.v4.s64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.v[0]), "=l"(r.v[1]), "=l"(r.v[2]), "=l"(r.v[3]) : "l"(p + i));
+  else
+    asm volatile("ld.global.v4.s64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(r.v[0]), "=l"(r.v[1]), "=l"(r.v[2]), "=l"(r.v[3]) : "l"(p + i) : "memory");
+  return r;
+}
+
+// --------------------------------------------- single-thread bulk ring
+// One thread streams a contiguous global range through S shared-memory
+// slots with TMA bulk copies; slot s completes on mbarrier mb[s] (one
+// expect_tx per fill, covering every stream that shares the slot index).
+// ring_init: after data other threads wrote through the generic proxy was
+// made visible to this thread (the fused tail's grid_arrive), order it
+// before the async-proxy reads.
+__device__ __forceinline__ void ring_init(unsigned long long* mb, int slots) {
+  for (int s = 0; s < slots; ++s) {
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb + s));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void ring_expect(unsigned long long* mb, unsigned bytes) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  // the slot's previous contents were read through the generic proxy
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void ring_copy(void* dst, const void* src, unsigned bytes,
+                                          unsigned long long* mb) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void ring_wait(unsigned long long* mb, unsigned parity) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
         : "memory");
   }
 }

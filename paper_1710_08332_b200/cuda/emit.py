@@ -56,11 +56,21 @@ UNROLL_LIMIT = 64
 # VEC_WIDTH-wide vectors (KernelEmitter._vec_loop); DPIA_VEC_LOADS=0 disables
 VEC_LOADS = os.environ.get("DPIA_VEC_LOADS", "1") != "0"
 VEC_WIDTH = 4
-# ... and keep VEC_PREFETCH vectors per read stream in flight (a rotating
-# register queue refilled VEC_PREFETCH vectors ahead); 0 disables.  A single
-# thread (a fused tail's top-level fold) keeps VEC_PREFETCH_SINGLE.
+# ... and each read stream of a work-item's fold keeps VEC_PREFETCH queue
+# slots in flight (a rotating register queue refilled VEC_PREFETCH slots
+# ahead; 0 disables).  A slot is one VEC_LOAD_BYTES vector: 32 = one sm_100
+# 256-bit load (LDG.E.256: half the L1 wavefronts per byte of a work-item's
+# own -- uncoalesced -- chunk, tools/chunkread.py), 16 = LDG.128.
 VEC_PREFETCH = int(os.environ.get("DPIA_VEC_PREFETCH", "8"))
-VEC_PREFETCH_SINGLE = int(os.environ.get("DPIA_VEC_PREFETCH_SINGLE", "32"))
+VEC_LOAD_BYTES = int(os.environ.get("DPIA_VEC_LOAD_BYTES", "32"))
+# A single thread's fold (the top-level sequential reduce of a fused tail)
+# streams its data through a shared-memory ring of TAIL_RING_STAGES TMA bulk
+# copies of TAIL_RING_BYTES per stream; DPIA_TAIL_RING=0 uses the register
+# queue instead.
+TAIL_RING = os.environ.get("DPIA_TAIL_RING", "1") != "0"
+TAIL_RING_STAGES = int(os.environ.get("DPIA_TAIL_RING_STAGES", "4"))
+TAIL_RING_BYTES = int(os.environ.get("DPIA_TAIL_RING_BYTES", "2048"))
+TAIL_RING_UNROLL = int(os.environ.get("DPIA_TAIL_RING_UNROLL", "16"))
 # block-invariant identity stagings of an input into shared memory as one
 # bulk (TMA) copy: KernelEmitter.bulk_stage; DPIA_BULK_STAGE=0 emits the
 # work-item copy loop instead
@@ -174,6 +184,7 @@ class CudaSignature:
     launch: Optional[Tuple[Tuple[int, int], Tuple[int, int]]]
     sigma: Optional[Dict[str, int]]
     spaces: Dict[str, str] = field(default_factory=dict, repr=False)   # buffer binder -> space
+    align: Dict[str, int] = field(default_factory=dict, repr=False)    # buffer -> bytes (> 16) its loads need
 
     def params(self) -> List[str]:
         out = [f"{self.scalar} *{n}" for n, _ in self.outputs]
@@ -479,7 +490,7 @@ class KernelEmitter:
         self.for_plans: Dict[int, list] = {}
         self.rotated: Dict[str, str] = {}
         self.hoisted_writes: Set[int] = set()
-        self.vec_vars: Set[str] = set()      # loop counters of VEC_WIDTH-unrolled folds
+        self.vec_vars: Dict[str, int] = {}   # loop counter -> lane width of an unrolled fold
         self.vec_hits = 0
         self.vec_pf: Optional[dict] = None   # the innermost prefetching fold (`_vec_loop`)
 
@@ -728,21 +739,21 @@ class KernelEmitter:
         return r
 
     def _lane_read(self, r: Ref) -> Optional[str]:
-        """Inside a VEC_WIDTH-unrolled sequential fold (`_vec_loop`): a scalar
-        read of a global buffer at flat index W*j + A + c (j the unrolled
-        counter, every other term a multiple of W, 0 <= c < W) becomes lane
-        c of the W-vector at W*j + A.  The W unrolled iterations read the
-        same vector, which the compiler loads once (LDG.128).  In a
-        prefetching fold the vector comes from the stream's register queue
-        when A mentions no loop variable bound inside the fold."""
+        """Inside a W-unrolled sequential fold (`_vec_loop`): a scalar read
+        of a global buffer at flat index W*j + A + c (j the unrolled counter,
+        every other term a multiple of W, 0 <= c < W) becomes lane c of the
+        W-vector at W*j + A.  The W unrolled iterations read the same
+        vector, which the compiler loads once.  In a prefetching fold the
+        vector comes from the stream's queue or ring when A mentions no loop
+        variable bound inside the fold."""
         if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global") \
                 or r.buf.swz or r.buf.pad or not isinstance(r.buf.elem, Num):
             return None
-        W = VEC_WIDTH
         coef = dict((m, c) for m, c in r.flat.terms)
-        js = [v for v in self.vec_vars if coef.get((v,)) == W]
+        js = [v for v, w in self.vec_vars.items() if coef.get((v,)) == w]
         if len(js) != 1:
             return None
+        W = self.vec_vars[js[0]]
         lane = coef.get((), 0) % W
         if lane < 0 or any(c % W for m, c in r.flat.terms if m != ()):
             return None
@@ -918,63 +929,109 @@ class KernelEmitter:
     def _vec_loop(self, n: Nat, f: Lam) -> bool:
         """A long sequential loop inside one work-item (a reduceSeq over a
         contiguous chunk, or the single-thread top-level reduce of a fused
-        tail) that reads global buffers at unit stride: emitted unrolled by
-        VEC_WIDTH, iteration W*j + k reading lane k of one W-wide vector load
+        tail) that reads global buffers at unit stride: emitted unrolled by a
+        lane width W, iteration W*j + k reading lane k of one W-wide vector
         (`_lane_read`), instead of W scalar loads.  The iterations run in
-        the original order, so the fold's association is unchanged.  Each
-        read stream is software-pipelined through a rotating register queue
-        of D vectors (`_emit_vec_loop`) unless the fold writes the buffer.
-        Tried on a scratch copy of the output; False (nothing emitted) when
-        no read qualifies."""
-        W = VEC_WIDTH
+        the original order, so the fold's association is unchanged.  The
+        read streams are software-pipelined (`_emit_vec_loop`): through a
+        shared-memory ring of TMA bulk copies in a single thread's fold,
+        through a rotating register queue of 32-byte (then 16-byte) loads in
+        a work-item's fold, unless the fold writes a streamed buffer.  Each
+        variant is tried on a scratch copy of the output; False (nothing
+        emitted) when no read qualifies."""
         trip = self.nat_int(n)
         if not VEC_LOADS or not self.per_thread or self.pf is not None or trip is None \
-                or trip % W or trip <= UNROLL_LIMIT:
+                or trip <= UNROLL_LIMIT:
             return False
-        T = trip // W
-        D = VEC_PREFETCH_SINGLE if self.single_thread and not self.loops else VEC_PREFETCH
-        D = 1 << (D.bit_length() - 1) if D > 0 else 0     # a power of two ...
-        while D > 1 and (T % D or T < 2 * D):            # ... dividing T, at most T / 2
-            D //= 2
-        for depth in ([D] if D > 1 else []) + [0]:
-            mark, ind, hits = len(self.lines), self.ind, self.vec_hits
-            ok = self._emit_vec_loop(n, f, T, depth)
-            if ok and self.vec_hits > hits:
+        sb = 4 if self.scalar == "float" else 8
+        modes = []
+        if TAIL_RING and self.single_thread and not self.loops and TAIL_RING_STAGES > 0:
+            modes.append(("ring", VEC_WIDTH))
+        if VEC_PREFETCH > 1:
+            if VEC_LOAD_BYTES == 32:
+                modes.append(("queue32", 32 // sb))
+            modes.append(("queue", VEC_WIDTH))
+        modes.append(("plain", VEC_WIDTH))
+        for mode, W in modes:
+            if trip % W:
+                continue
+            mark, ind, hits, smem = len(self.lines), self.ind, self.vec_hits, self.smem
+            if self._emit_vec_loop(n, f, trip // W, W, mode) and self.vec_hits > hits:
                 return True
             del self.lines[mark:]
-            self.ind = ind
+            self.ind, self.smem = ind, smem
         return False
 
-    def _emit_vec_loop(self, n: Nat, f: Lam, T: int, D: int) -> bool:
-        """One attempt of `_vec_loop`.  D > 1: the loop is
-            queue_s[d] = V_s(d), d < D                  (prologue)
+    @staticmethod
+    def _pow2_divisor(want: int, T: int, cap: int) -> int:
+        """The largest power of two <= min(want, cap) dividing T (0 if < 2)."""
+        d = 1 << (max(1, min(want, cap)).bit_length() - 1)
+        while d > 1 and T % d:
+            d //= 2
+        return d if d > 1 else 0
+
+    def _emit_vec_loop(self, n: Nat, f: Lam, T: int, W: int, mode: str) -> bool:
+        """One attempt of `_vec_loop`, T iterations of W lanes.
+
+        queue / queue32 (a work-item's fold): D slots per stream s (a buffer
+        and a base offset; V_s(j) its W-vector at iteration j)
+            q_s[d] = V_s(d), d < D                        (prologue)
             for jo in 0, D, ..: for jd < D (unrolled): j = jo + jd
-                v_s = queue_s[jd]; queue_s[jd] = V_s(j + D) if j + D < T
+                v_s = q_s[jd]; q_s[jd] = V_s(j + D) if j + D < T
                 body(j) reading lanes of v_s
-        for every stream s (a buffer and a base offset; V_s(j) its vector at
-        iteration j), so D vectors per stream are in flight while the body
-        folds in order.  False when D > 1 and the body writes a queued
-        buffer or nothing was queued."""
-        W = VEC_WIDTH
+        so D vectors per stream are in flight while the body folds in
+        order; queue32 loads each slot with one 32-byte load.
+
+        ring (a single thread's fold): C-vector pieces of every stream go
+        through S shared-memory slots filled by TMA bulk copies
+            fill slot k of every stream, k < S           (prologue)
+            for jo in 0, C, ..: wait slot k = jo / C (mbarrier parity)
+                for jd < C: j = jo + jd; v_s = slot[jd]; body(j)
+                refill the slot with piece k + S
+        False when the body writes a streamed buffer or nothing streams."""
         j = self.fresh("j")
         self.R[j] = T
         outer_pf = self.vec_pf
         pf = None
         top = len(self.lines)
-        if D > 1:
+        sb = 4 if self.scalar == "float" else 8
+        vt = f"dpia::vec<{self.scalar}, {W}>"
+        D = C = S = 0
+        if mode in ("queue", "queue32"):
+            D = self._pow2_divisor(VEC_PREFETCH * 32 // (W * sb), T, T // 2)
+            if not D:
+                return False
+        elif mode == "ring":
+            C = self._pow2_divisor(TAIL_RING_BYTES // (W * sb), T, T)
+            if not C:
+                return False
+            S = min(TAIL_RING_STAGES, T // C)
+        if mode != "plain":
             self._k += 1
             pf = {"j": j, "depth": len(self.loops), "streams": {}, "written": set(), "tag": self._k}
             self.vec_pf = pf
+        else:
+            self.vec_pf = None
+        if mode in ("queue", "queue32"):
             jo, jd = self.fresh("jo"), self.fresh("jd")
             self.open(f"for (int {jo} = 0; {jo} < {T}; {jo} += {D})")
             self.line("#pragma unroll")
             self.open(f"for (int {jd} = 0; {jd} < {D}; {jd} += 1)")
             self.line(f"const int {j} = {jo} + {jd};")
             take = len(self.lines)
+        elif mode == "ring":
+            jo, jd, rk, rs, mb = (self.fresh(x) for x in ("jo", "jd", "rk", "rs", "rmb"))
+            self.open(f"for (int {jo} = 0; {jo} < {T}; {jo} += {C})")
+            self.line(f"const int {rk} = {jo} / {C}, {rs} = {rk} % {S};")
+            self.line(f"dpia::ring_wait({mb} + {rs}, (unsigned)(({rk} / {S}) & 1));")
+            slot_at = len(self.lines)
+            self.line(f"#pragma unroll {TAIL_RING_UNROLL}")
+            self.open(f"for (int {jd} = 0; {jd} < {C}; {jd} += 1)")
+            self.line(f"const int {j} = {jo} + {jd};")
+            take = len(self.lines)
         else:
-            self.vec_pf = None
             self.open(f"for (int {j} = 0; {j} < {T}; {j} += 1)")
-        self.vec_vars.add(j)
+        self.vec_vars[j] = W
         self.loops.append(Loop("seq", 0, j, T, nat(T), False))
         old = self.env.get(f.binder)
         try:
@@ -985,7 +1042,7 @@ class KernelEmitter:
                 self.close()
         finally:
             self.loops.pop()
-            self.vec_vars.discard(j)
+            self.vec_vars.pop(j, None)
             self.vec_pf = outer_pf
             if old is None:
                 self.env.pop(f.binder, None)
@@ -994,29 +1051,73 @@ class KernelEmitter:
         self.close()
         if pf is None:
             return True
-        self.close()
         streams = list(pf["streams"].values())
         if not streams or any(b.cname in pf["written"] for _, b, _ in streams):
             return False
-        vt = f"dpia::vec<{self.scalar}, {W}>"
-        pad_in = "  " * (self.ind + 2)
+        if mode == "ring":
+            return self._finish_ring(streams, top, slot_at, take, T, W, C, S, j, jo, jd, rs, mb)
+        self.close()
+        pad = "  " * self.ind
+        pad_in = pad + "    "
         body = []
         for name, b, base in streams:
             q = name.replace("pfv_", "pfq_")
             body.append(f"{pad_in}const {vt} {name} = {q}[{jd}];")
-            body.append(f"{pad_in}if ({j} + {D} < {T}) {q}[{jd}] = dpia::vload<{self.scalar}, {W}>"
-                        f"({b.cname}, {self.r(base + ix(W * D))});")
+            body.append(f"{pad_in}if ({j} + {D} < {T}) {q}[{jd}] = {self._vload(mode, b, W, base + ix(W * D))};")
         self.lines[take:take] = body
-        pad = "  " * self.ind
-        pro = []
-        for name, b, base in streams:
-            pro.append(f"{pad}{vt} {name.replace('pfv_', 'pfq_')}[{D}];")
+        pro = [f"{pad}{vt} {name.replace('pfv_', 'pfq_')}[{D}];" for name, _b, _base in streams]
         pro.append(f"{pad}#pragma unroll")
         pro.append(f"{pad}for (int {j} = 0; {j} < {D}; {j} += 1) {{")
         for name, b, base in streams:
-            pro.append(f"{pad}  {name.replace('pfv_', 'pfq_')}[{j}] = dpia::vload<{self.scalar}, {W}>"
-                       f"({b.cname}, {self.r(base)});")
+            pro.append(f"{pad}  {name.replace('pfv_', 'pfq_')}[{j}] = {self._vload(mode, b, W, base)};")
         pro.append(f"{pad}}}")
+        self.lines[top:top] = pro
+        return True
+
+    def _vload(self, mode: str, b: Buffer, W: int, at: Ix) -> str:
+        if mode == "queue32":
+            self.prog.align[b.cname] = max(self.prog.align.get(b.cname, 16), 32)
+            return f"dpia::vload32<{'true' if b.space == 'in' else 'false'}>({b.cname}, {self.r(at)})"
+        return f"dpia::vload<{self.scalar}, {W}>({b.cname}, {self.r(at)})"
+
+    def _finish_ring(self, streams, top, slot_at, take, T, W, C, S, j, jo, jd, rs, mb) -> bool:
+        """Complete a ring-mode fold (see `_emit_vec_loop`): slot pointers,
+        shared-memory reads, the refill after each piece and the prologue."""
+        sb = 4 if self.scalar == "float" else 8
+        piece = C * W * sb
+        if piece % 16 or piece >= (1 << 20):
+            return False
+        moff = self.alloc_smem(8 * S)
+        offs = [self.alloc_smem(S * piece) for _ in streams]
+        pad1 = "  " * self.ind            # the piece loop's body
+        pad2 = pad1 + "  "                # the lane loop's body
+        vt = f"dpia::vec<{self.scalar}, {W}>"
+        # this piece's slot of every stream, and the lanes the body reads
+        self.lines[take:take] = [
+            f"{pad2}const {vt} {name} = dpia::vload<{self.scalar}, {W}>({name}_s, {W} * {jd});"
+            for name, _b, _base in streams]
+        self.lines[slot_at:slot_at] = [
+            f"{pad1}const {self.scalar}* {name}_s = reinterpret_cast<const {self.scalar}*>"
+            f"(dpia_smem + {off}) + {rs} * {C * W};" for (name, _b, _base), off in zip(streams, offs)]
+
+        def fill(p, slot, at_j):
+            out = [f"{p}{{", f"{p}  const int {j} = {at_j};",
+                   f"{p}  dpia::ring_expect({mb} + {slot}, {piece * len(streams)}u);"]
+            for (name, b, base), off in zip(streams, offs):
+                out.append(f"{p}  dpia::ring_copy(dpia_smem + {off} + {slot} * {piece}, "
+                           f"{b.cname} + ({self.r(base)}), {piece}u, {mb} + {slot});")
+            out.append(f"{p}}}")
+            return out
+
+        self.line(f"if ({jo} + {S * C} < {T})")
+        self.lines += fill(pad1, rs, f"{jo} + {S * C}")
+        self.close()
+        rq = self.fresh("rq")
+        pad = "  " * self.ind
+        pro = [f"{pad}unsigned long long* {mb} = reinterpret_cast<unsigned long long*>(dpia_smem + {moff});",
+               f"{pad}dpia::ring_init({mb}, {S});",
+               f"{pad}for (int {rq} = 0; {rq} < {S}; {rq} += 1)"]
+        pro += fill(pad, rq, f"{rq} * {C}")
         self.lines[top:top] = pro
         return True
 
@@ -1633,6 +1734,7 @@ class ProgramEmitter:
         self.scratch_names: Set[str] = set()
         self.in_tail = False
         self.size_names: Set[str] = set()
+        self.align: Dict[str, int] = {}      # buffer -> byte alignment its loads need (> 16)
 
     def is_shared(self, name: str) -> bool:
         return self.spaces.get(name, "private") != "private"
@@ -1756,7 +1858,8 @@ class ProgramEmitter:
         size_names = sorted(self.size_names) if self.sigma is None else []
         sig = CudaSignature(self.outputs, self.inputs,
                             [(b.cname, b.dtype) for b in self.scratch], size_names, infos,
-                            self.scalar, self.launch, self.sigma, dict(self.spaces))
+                            self.scalar, self.launch, self.sigma, dict(self.spaces),
+                            dict(self.align))
         src = ["// generated by the DPIA CUDA backend (paper_1710_08332_b200) for sm_100a",
                header, self.types.struct_text()] + bodies
         return "\n".join(s for s in src if s) + "\n", sig

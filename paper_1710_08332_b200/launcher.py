@@ -120,11 +120,15 @@ class Executable:
     def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int]):
         """Launch with some parameters re-pointed (device addresses), e.g. at
         windows of larger buffers -- the row chunks of pipeline.RowPipeline.
-        Windows must be 16-byte aligned: the emitted kernels read their
-        buffers with whole-vector loads (asVector, vectorised folds)."""
-        bad = [n for n, q in ptrs.items() if q % 16]
+        Windows must be 16-byte aligned -- the emitted kernels read their
+        buffers with whole-vector loads (asVector, vectorised folds) -- and
+        32-byte aligned where a fold's register queue loads 32 bytes at a
+        time (`sig.align`)."""
+        need = {n: max(16, self.sig.align.get(n, 16)) for n in ptrs}
+        bad = [n for n, q in ptrs.items() if q % need[n]]
         if bad:
-            raise ValueError(f"launch_with: windows {bad} are not 16-byte aligned")
+            raise ValueError(f"launch_with: windows {bad} are not aligned to "
+                             f"{[need[n] for n in bad]} bytes")
         if self.peer is not None:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry

@@ -276,21 +276,27 @@ def test_golden_fixtures_regenerate_identically(tmp_path):
 
 
 def test_vectorised_fold_emission(monkeypatch):
-    """CPU: config 1's literal program reads its chunks and the tail's
-    partials as 4-wide vectors; DPIA_VEC_LOADS=0 restores scalar loads; a
-    transposed (strided) chunk is never vectorised."""
+    """CPU: with the software pipelining off, config 1's literal program
+    reads its chunks and the tail's partials as 4-wide vectors;
+    DPIA_VEC_LOADS=0 restores scalar loads; a transposed (strided) chunk is
+    never vectorised."""
     from paper_1710_08332_b200 import compile_program
     from paper_1710_08332_b200.bench_programs import dot_literal_config
     from paper_1710_08332_b200.cuda import emit as E
     cfg = dot_literal_config()
     prog = compile_program(cfg.text)
     outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    monkeypatch.setattr(E, "VEC_PREFETCH", 0)
+    monkeypatch.setattr(E, "TAIL_RING", False)
     src, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
     assert "dpia::vload<float, 4>(xs, 1024 * " in src and "dpia::vload<float, 4>(g_tmp4, 4 * " in src
+    assert "pfq_" not in src and "ring_" not in src.split('extern "C"')[1]
     monkeypatch.setattr(E, "VEC_LOADS", False)
     src0, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
     assert "vload" not in src0.split('extern "C"')[1]
     monkeypatch.setattr(E, "VEC_LOADS", True)
+    monkeypatch.setattr(E, "VEC_PREFETCH", 8)
+    monkeypatch.setattr(E, "TAIL_RING", True)
     strided = compile_program("(nat n)\n(param xs (exp (array (* n 128) num)))\n"
                               "(mapGlobal (lam (c (exp (array 128 num))) (reduce (+) 0 c))"
                               " (transpose (split n xs)))")
@@ -299,31 +305,45 @@ def test_vectorised_fold_emission(monkeypatch):
     assert "vload" not in s2.split('extern "C"')[1]
 
 
-def test_vectorised_fold_prefetch_queue(monkeypatch):
-    """CPU: each read stream of a long sequential fold is software-pipelined
-    through a rotating register queue (VEC_PREFETCH vectors per work-item
-    stream, VEC_PREFETCH_SINGLE for the single-thread tail), refilled D
-    vectors ahead under a bound guard; depth 0 restores the plain
-    vectorised fold, and a depth that does not divide the trip shrinks."""
+def test_vectorised_fold_pipelining(monkeypatch):
+    """CPU: a work-item's fold streams each input through a rotating queue
+    of 32-byte loads (VEC_PREFETCH slots, refilled D slots ahead under a
+    bound guard; the signature asks 32-byte alignment of those buffers);
+    16-byte slots with DPIA_VEC_LOAD_BYTES=16; the single-thread top-level
+    fold of the fused tail streams the partials through a shared-memory
+    ring of TMA bulk copies (TAIL_RING_STAGES x TAIL_RING_BYTES), or a
+    register queue with the ring off; depths that do not divide the trip
+    shrink to a power of two that does."""
     from paper_1710_08332_b200 import compile_program
     from paper_1710_08332_b200.bench_programs import dot_literal_config
     from paper_1710_08332_b200.cuda import emit as E
     cfg = dot_literal_config()
     prog = compile_program(cfg.text)
     outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
-    monkeypatch.setattr(E, "VEC_PREFETCH", 8)
-    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 32)
-    src, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
-    body = src.split('extern "C"')[1]
-    # two chunk streams (xs, ys) of depth 8, one tail stream of depth 32
-    assert body.count("[8];") == 2 and body.count("[32];") == 1
-    assert "+ 8 < 256) pfq_" in body and "+ 32 < 4096) pfq_" in body
-    assert "4 * j_" in body and "+ 32);" in body and "+ 128);" in body   # 4 * D scalars ahead
-    monkeypatch.setattr(E, "VEC_PREFETCH", 0)
-    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 0)
-    src0, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
-    assert "pfq_" not in src0 and "dpia::vload<float, 4>(xs, 1024 * " in src0
-    monkeypatch.setattr(E, "VEC_PREFETCH", 24)     # 256 % 24 != 0 -> 16 (a divisor, <= T/2)
-    monkeypatch.setattr(E, "VEC_PREFETCH_SINGLE", 32)
-    src3, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
-    assert "+ 12 < 256)" not in src3 and "+ 16 < 256) pfq_" in src3
+
+    def emit(**kw):
+        for k, v in kw.items():
+            monkeypatch.setattr(E, k, v)
+        src, sig = E.emit_cuda(prog.imperative, outs, ins, float_mode=True, sigma=cfg.sigma,
+                               launch=cfg.launch)
+        return src.split('extern "C"')[1], sig
+
+    body, sig = emit(VEC_PREFETCH=8, VEC_LOAD_BYTES=32, TAIL_RING=True, TAIL_RING_STAGES=4,
+                     TAIL_RING_BYTES=2048)
+    # chunks: 1024 floats = 128 32-byte vectors per stream, 8 in flight
+    assert body.count("dpia::vec<float, 8> pfq_") == 2 and "[8];" in body
+    assert "dpia::vload32<true>(xs, 1024 * i_" in body and "+ 8 < 128) pfq_" in body
+    assert sig.align == {"xs": 32, "ys": 32}
+    # tail: 4096 vec4 of partials in pieces of 128 (2 KiB), 4 slots, bulk copies
+    assert "dpia::ring_init(" in body and body.count("dpia::ring_copy(") == 2
+    assert "jo_" in body and "< 4096; jo_" in body and "+= 128)" in body and "+ 512 < 4096)" in body
+    assert sig.kernels[0].smem >= 4 * 2048 + 4 * 8
+    body16, sig16 = emit(VEC_LOAD_BYTES=16)
+    assert "vload32" not in body16 and "+ 16 < 256) pfq_" in body16 and not sig16.align
+    body_q, sig_q = emit(VEC_LOAD_BYTES=32, TAIL_RING=False)
+    assert "ring_init" not in body_q and "dpia::vload32<false>(g_tmp4, 8 * j_" in body_q
+    assert sig_q.kernels[0].smem < 64
+    body_s, _ = emit(TAIL_RING=True, TAIL_RING_BYTES=3000, VEC_PREFETCH=6)   # -> 128-vector pieces, 4 slots
+    assert "+= 128)" in body_s and "+ 4 < 128) pfq_" in body_s
+    body0, _ = emit(VEC_PREFETCH=0, TAIL_RING=False)
+    assert "pfq_" not in body0 and "ring_" not in body0
