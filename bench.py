@@ -63,32 +63,65 @@ def fp32_peak(device):
 _SOL_CACHE = {}
 
 
+def l2_bytes(device):
+    return RT.device_attribute(device, 38) or (126 << 20)     # CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE
+
+
+def rotation(device, step_bytes):
+    """How many input sets the steady-state timing rotates through: enough
+    that R x the step's bytes >= 3 x L2, so the set a step reads was evicted
+    by the reads of the steps since its last use (the contract's "inputs
+    larger than L2")."""
+    return max(1, -(-3 * l2_bytes(device) // step_bytes))
+
+
 def read_sol(device, nbytes, stream):
     """Size-matched speed of light: a hand-written minimal CUDA streaming-read
     kernel (tools/readsol.py; measurement infrastructure, not product) timed
-    exactly like the benchmark steps on `nbytes` of HBM."""
+    exactly like the benchmark steps on `nbytes` of HBM: {"steady": GB/s over
+    back-to-back reads of rotating buffers, "isolated": GB/s of one launch
+    after an L2 scrub}."""
     if nbytes in _SOL_CACHE:
         return _SOL_CACHE[nbytes]
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     from readsol import SRC
     mod = RT.Module(RT.get_cubin(SRC), device)
     fn = mod.function("readsum")
-    buf, out = RT.DeviceBuffer(nbytes, device), RT.DeviceBuffer(16, device)
-    buf.zero(stream)
-    args = [RT.C.c_uint64(buf.ptr), RT.C.c_longlong(nbytes // 16), RT.C.c_uint64(out.ptr)]
+    R = rotation(device, nbytes)
+    bufs, out = [RT.DeviceBuffer(nbytes, device) for _ in range(R)], RT.DeviceBuffer(16, device)
+    for b in bufs:
+        b.zero(stream)
+    args = [[RT.C.c_uint64(b.ptr), RT.C.c_longlong(nbytes // 16), RT.C.c_uint64(out.ptr)] for b in bufs]
+
+    def launch(i):
+        RT.launch(fn, device, (296, 1), (1024, 1), 0, args[i % R], stream)
     ts = []
     for it in range(13):
         RT.lib().dpia_l2_flush(device, stream.handle)
         e0, e1 = RT.Event(device), RT.Event(device)
         e0.record(stream)
-        RT.launch(fn, device, (296, 1), (1024, 1), 0, args, stream)
+        launch(0)
         e1.record(stream)
         stream.sync()
         if it >= 3:
             ts.append(e0.elapsed_ms(e1))
-    buf.free()
+    K = 30
+    for i in range(6):
+        launch(i)
+    runs = []
+    for rep in range(3):
+        e0, e1 = RT.Event(device), RT.Event(device)
+        e0.record(stream)
+        for i in range(K):
+            launch(i)
+        e1.record(stream)
+        stream.sync()
+        runs.append(e0.elapsed_ms(e1) / K)
+    for b in bufs:
+        b.free()
     out.free()
-    _SOL_CACHE[nbytes] = round(nbytes / statistics.median(ts) / 1e6, 1)
+    _SOL_CACHE[nbytes] = {"steady": round(nbytes / statistics.median(runs) / 1e6, 1),
+                          "isolated": round(nbytes / statistics.median(ts) / 1e6, 1)}
     return _SOL_CACHE[nbytes]
 
 
@@ -293,25 +326,62 @@ def _seeded(shape, seed, lo, hi):
     return np.random.default_rng(seed).uniform(lo, hi, size=shape).astype(np.float32)
 
 
-def time_steps(exe, stream, steps, warmup, flush=True, allreduce=None):
-    dev = exe.device
-    ev = [(RT.Event(dev), RT.Event(dev)) for _ in range(steps)]
-    for _ in range(warmup):
-        if flush:
-            RT.lib().dpia_l2_flush(dev, stream.handle)
-        exe.launch(stream)
-        if allreduce:
-            allreduce(stream)
-    stream.sync()
-    return ev
+class Rotation:
+    """The steady-state step: K steps back to back on one stream, step i
+    reading input set i % R (`rotation`), between ONE event pair.  Set 0 is
+    the executable's own buffers; the other sets are device copies of its
+    inputs (and of outputs larger than 1 MiB, so written lines rotate too)."""
+
+    def __init__(self, exe, step_bytes, stream):
+        self.exe = exe
+        self.R = rotation(exe.device, step_bytes)
+        self.extra = []
+        self.ptrs = [None]
+        names = [n for n, _ in exe.sig.inputs] + [n for n, _ in exe.sig.outputs
+                                                  if exe.buffers[n].nbytes > (1 << 20)]
+        for _ in range(self.R - 1):
+            ptrs = {}
+            for n in names:
+                src = exe.buffers[n]
+                b = RT.DeviceBuffer(src.nbytes, exe.device)
+                RT.lib().dpia_memcpy_dtod(exe.device, b.ptr, src.ptr, src.nbytes, stream.handle)
+                self.extra.append(b)
+                ptrs[n] = b.ptr
+            self.ptrs.append(ptrs)
+        stream.sync()
+
+    def launch(self, i, stream):
+        p = self.ptrs[i % self.R]
+        if p is None:
+            self.exe.launch(stream)
+        else:
+            self.exe.launch_with(stream, p)
+
+    def run(self, stream, steps, allreduce=None, start=0):
+        """ms per step of `steps` back-to-back steps (events on `stream`)."""
+        e0, e1 = RT.Event(self.exe.device), RT.Event(self.exe.device)
+        e0.record(stream)
+        for i in range(start, start + steps):
+            self.launch(i, stream)
+            if allreduce:
+                allreduce(stream)
+        e1.record(stream)
+        stream.sync()
+        return e0.elapsed_ms(e1) / steps
+
+    def free(self):
+        for b in self.extra:
+            b.free()
+        self.extra, self.ptrs, self.R = [], [None], 1
 
 
-def run_timed(exe, stream, steps, flush=True, allreduce=None):
+def run_isolated(exe, stream, steps, allreduce=None):
+    """Per-launch event pairs, each launch after an L2 scrub (the round-1
+    method; reported beside the steady-state number)."""
     dev = exe.device
     ev = [(RT.Event(dev), RT.Event(dev)) for _ in range(steps)]
     for e0, e1 in ev:
-        if flush:
-            RT.lib().dpia_l2_flush(dev, stream.handle)
+        RT.lib().dpia_l2_flush(dev, stream.handle)
         e0.record(stream)
         exe.launch(stream)
         if allreduce:
@@ -695,7 +765,12 @@ def main():
 
             def allreduce(s):  # NCCL sum of the per-rank partial, on our stream
                 RT.lib().dpia_nccl_allreduce(outbuf.ptr, 1, 0, s.handle)
-        time_steps(exe, stream, steps, warmup, allreduce=allreduce)
+        rot = Rotation(exe, cfg.bytes, stream)
+        for i in range(warmup):
+            rot.launch(i, stream)
+            if allreduce:
+                allreduce(stream)
+        stream.sync()
         if dist is not None:
             dist.barrier()
         RT.lib().dpia_device_sync(device)
@@ -703,33 +778,35 @@ def main():
         # sampler sees the clocks of the timed region; every rank does the
         # same number of launches (the fused peer combine pairs them up)
         t_b = time.perf_counter()
-        for _ in range(20):
-            RT.lib().dpia_l2_flush(device, stream.handle)
-            exe.launch(stream)
-        stream.sync()
+        rot.run(stream, 20, allreduce)
         batches = max(1, int(0.6 / max(time.perf_counter() - t_b, 1e-4)))
         if dist is not None:
             import torch
             batches = int(_allreduce(dist, batches, dist.ReduceOp.MAX, local, share))
         with Clocks(device) as clk:
             for _ in range(batches):
-                for _ in range(20):
-                    RT.lib().dpia_l2_flush(device, stream.handle)
-                    exe.launch(stream)
-                stream.sync()
+                rot.run(stream, 20, allreduce)
+            if dist is not None:
+                dist.barrier()
             t0 = time.perf_counter()
-            ms = run_timed(exe, stream, steps, allreduce=allreduce)
+            # the timed region: `steps` steps back to back, one event pair
+            mean_ms = mean_ms_local = rot.run(stream, steps, allreduce)
             wall = time.perf_counter() - t0
         RT.lib().dpia_device_sync(device)
-        mean_ms = mean_ms_local = statistics.mean(ms)
         if dist is not None:
             import torch
             mean_ms = float(_allreduce(dist, mean_ms, dist.ReduceOp.MAX, local, share))
             dist.barrier()
-        if allreduce is None and exe.peer is None:
-            kmean = statistics.mean(ms)       # a step is exactly the program's kernel(s)
+        if allreduce is None:
+            kmean = mean_ms_local             # a step is exactly the program's kernel(s)
         else:                                 # the dominant kernel alone, without the combine
-            kmean = statistics.mean(run_timed(exe, stream, steps))
+            kmean = rot.run(stream, steps)
+        # the round-1 method beside it: each launch alone after an L2 scrub
+        iso = run_isolated(exe, stream, steps, allreduce)
+        iso_ms = statistics.mean(iso)
+        rot_desc = {"input_sets": rot.R, "l2_bytes": l2_bytes(device),
+                    "bytes_per_step": cfg.bytes}
+        rot.free()
         if workload == "mm":
             fp32 = fp32_peak(device)
             achieved = cfg.flops / (kmean * 1e-3) / 1e12
@@ -755,8 +832,8 @@ def main():
                     "algorithmic_bytes_per_launch": cfg.bytes, "kernel_ms": round(kmean, 5)}
             if workload in ("asum", "dot", "gemv"):
                 sol = read_sol(device, cfg.bytes, stream)
-                roof["size_matched_read_sol_gbs"] = sol
-                roof["frac_of_size_matched_sol"] = round(achieved / sol, 4)
+                roof["size_matched_read_sol_gbs"] = sol["steady"]
+                roof["frac_of_size_matched_sol"] = round(achieved / sol["steady"], 4)
         if world == 1:
             # DRAM traffic of the same kernel, measured after the timed region
             if args.traffic == "live":
@@ -767,9 +844,19 @@ def main():
             roof["traffic_source"] = tsrc
             if t:
                 roof["traffic_over_algorithmic"] = round(t / cfg.bytes, 4)
-        res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "median_ms": statistics.median(ms),
-               "min_ms": min(ms), "wall_s": wall, "clocks": clk.summary(),
-               "value": value, "roofline": roof}
+        work = cfg.flops if workload == "mm" else cfg.bytes
+        roof["isolated"] = {
+            "ms_per_launch": round(iso_ms, 5),
+            "achieved": round(work / (iso_ms * 1e-3) / (1e12 if workload == "mm" else 1e9),
+                              2 if workload == "mm" else 1),
+            "frac": round(work / (iso_ms * 1e-3) / (1e12 if workload == "mm" else 1e9) / roof["peak"], 4),
+            "method": "each launch alone between its own event pair, after an L2 scrub (round-1 "
+                      "timing): adds the event pair and an unhidden launch, ~6 us "
+                      "(profiles/r01f_tailexp4.txt)"}
+        if workload in ("asum", "dot", "gemv"):
+            roof["isolated"]["size_matched_read_sol_gbs"] = read_sol(device, cfg.bytes, stream)["isolated"]
+        res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "wall_s": wall, "clocks": clk.summary(),
+               "value": value, "roofline": roof, "rotation": rot_desc}
         if check is not None:
             res["combine_check"] = check
         if world > 1:
@@ -838,7 +925,8 @@ def main():
                         "ms_per_step": round(r["mean_ms"], 5), "roofline": r["roofline"],
                         "scaling": "strong" if w.startswith("scaleout") else "weak",
                         "e2e": r.get("e2e"), "clocks": r["clocks"],
-                        "config": _cfg_desc(r["cfg"], world, args.combine),
+                        "config": dict(_cfg_desc(r["cfg"], world, args.combine),
+                                       input_sets=r["rotation"]["input_sets"]),
                         "kernels": r["exe"].kernel_names()}
             if r.get("e2e") is None and w.startswith("scaleout"):
                 suite[w]["e2e_note"] = ("config 5 generates its inputs on device by a counter hash "
@@ -865,16 +953,14 @@ def main():
             "dtype": "f32",
             "data": ("synthetic (device-side counter hash, per-shard global offsets)" if strong
                      else "synthetic (numpy default_rng uniform, resident in HBM)"),
-            "config": dict(_cfg_desc(cfg, world, args.combine),
+            "config": dict(_cfg_desc(cfg, world, args.combine), input_sets=head["rotation"]["input_sets"],
                            **({"combine": args.combine} if world > 1 else {}),
                            **({"shared_gpu": "plumbing check: all ranks on GPU 0 (not a scaling number)"}
                               if share and world > 1 else {})),
             "roofline": head["roofline"], "e2e": head.get("e2e"), "clocks": head["clocks"],
             "gpu_launches": args.steps * len(exe.sig.kernels),
             "gpu_launches_breakdown": {"emitted program kernels (inside the timed events)":
-                                       args.steps * len(exe.sig.kernels),
-                                       "dpia_l2_scrub (libdpia_rt, between steps, outside the events)":
-                                       args.steps},
+                                       args.steps * len(exe.sig.kernels)},
             "kernels": exe.kernel_names(),
             "cpu_baseline": (_cpu_fields(cpu) if cpu else
                              {"unavailable": _cpu_unavailable(args.workload, world, args.no_cpu)}),
@@ -1008,11 +1094,16 @@ def _cfg_desc(cfg, world=1, combine="nccl"):
                             + ("inside the kernel over NVLink (peer)" if combine == "peer" and world > 1
                                else "by a 4-byte NCCL all-reduce" if world > 1 else "(one shard)"),
                 "sigma_per_rank": cfg.sigma,
-                "launch": list(cfg.launch), "l2": "inputs (>= 1 GiB per GPU) exceed L2; L2 also "
-                "scrubbed between steps"}
+                "launch": list(cfg.launch), "l2": L2_NOTE}
     wl, strat = WORKLOADS[cfg.name]
     return {"workload": wl, "strategy": strat, "sigma": cfg.sigma, "launch": list(cfg.launch),
-            "l2": "scrubbed between steps (a read of 2x L2 by dpia_l2_scrub, outside the timed events)"}
+            "l2": L2_NOTE}
+
+
+L2_NOTE = ("inputs larger than L2: the steps rotate through R device copies of the inputs (and of "
+           "outputs > 1 MiB) with R x step bytes >= 3 x L2, so each step's data was evicted by the "
+           "steps since its last use; the steps run back to back between one event pair (no scrub); "
+           "roofline.isolated is the per-launch scrubbed timing")
 
 
 if __name__ == "__main__":
