@@ -93,8 +93,8 @@ def read_sol(device, nbytes, stream):
         b.zero(stream)
     args = [[RT.C.c_uint64(b.ptr), RT.C.c_longlong(nbytes // 16), RT.C.c_uint64(out.ptr)] for b in bufs]
 
-    def launch(i):
-        RT.launch(fn, device, (296, 1), (1024, 1), 0, args[i % R], stream)
+    def launch(i, chain=False):
+        RT.launch(fn, device, (296, 1), (1024, 1), 0, args[i % R], stream, pdl=chain)
     ts = []
     for it in range(13):
         RT.lib().dpia_l2_flush(device, stream.handle)
@@ -107,13 +107,13 @@ def read_sol(device, nbytes, stream):
             ts.append(e0.elapsed_ms(e1))
     K = 30
     for i in range(6):
-        launch(i)
+        launch(i, True)
     runs = []
     for rep in range(3):
         e0, e1 = RT.Event(device), RT.Event(device)
         e0.record(stream)
         for i in range(K):
-            launch(i)
+            launch(i, True)        # chained like the benchmark steps
         e1.record(stream)
         stream.sync()
         runs.append(e0.elapsed_ms(e1) / K)
@@ -332,8 +332,9 @@ class Rotation:
     the executable's own buffers; the other sets are device copies of its
     inputs (and of outputs larger than 1 MiB, so written lines rotate too)."""
 
-    def __init__(self, exe, step_bytes, stream):
+    def __init__(self, exe, step_bytes, stream, chain=True):
         self.exe = exe
+        self.chain = chain          # each step chained behind the previous (PDL)
         self.R = rotation(exe.device, step_bytes)
         self.extra = []
         self.ptrs = [None]
@@ -353,9 +354,9 @@ class Rotation:
     def launch(self, i, stream):
         p = self.ptrs[i % self.R]
         if p is None:
-            self.exe.launch(stream)
+            self.exe.launch(stream, chain=self.chain)
         else:
-            self.exe.launch_with(stream, p)
+            self.exe.launch_with(stream, p, chain=self.chain)
 
     def run(self, stream, steps, allreduce=None, start=0):
         """ms per step of `steps` back-to-back steps (events on `stream`)."""
@@ -663,6 +664,8 @@ def main():
     ap.add_argument("--workload", default="asum")
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="launch the steps without chaining them (programmatic dependent launch)")
     ap.add_argument("--traffic", choices=["live", "committed"], default="live",
                     help="roofline.traffic from an ncu run of the same workload made now "
                          "(after the timed regions), or from profiles/ncu_traffic.json")
@@ -765,7 +768,7 @@ def main():
 
             def allreduce(s):  # NCCL sum of the per-rank partial, on our stream
                 RT.lib().dpia_nccl_allreduce(outbuf.ptr, 1, 0, s.handle)
-        rot = Rotation(exe, cfg.bytes, stream)
+        rot = Rotation(exe, cfg.bytes, stream, chain=not args.no_chain)
         for i in range(warmup):
             rot.launch(i, stream)
             if allreduce:
@@ -805,7 +808,7 @@ def main():
         iso = run_isolated(exe, stream, steps, allreduce)
         iso_ms = statistics.mean(iso)
         rot_desc = {"input_sets": rot.R, "l2_bytes": l2_bytes(device),
-                    "bytes_per_step": cfg.bytes}
+                    "bytes_per_step": cfg.bytes, "chained": rot.chain}
         rot.free()
         if workload == "mm":
             fp32 = fp32_peak(device)
@@ -1102,8 +1105,11 @@ def _cfg_desc(cfg, world=1, combine="nccl"):
 
 L2_NOTE = ("inputs larger than L2: the steps rotate through R device copies of the inputs (and of "
            "outputs > 1 MiB) with R x step bytes >= 3 x L2, so each step's data was evicted by the "
-           "steps since its last use; the steps run back to back between one event pair (no scrub); "
-           "roofline.isolated is the per-launch scrubbed timing")
+           "steps since its last use; the steps run back to back between one event pair (no scrub), "
+           "each chained behind the previous one (Executable.launch(chain=True): programmatic "
+           "dependent launch; the step streams its inputs while the previous step drains and waits "
+           "for it before touching shared memory); roofline.isolated is the per-launch scrubbed "
+           "timing")
 
 
 if __name__ == "__main__":

@@ -35,6 +35,9 @@ int dpia_device_name(int device, char* buf, int len);
 
 /* ---- compilation (replaces emit_kernel's text-only OpenCL output,
  *      SRC/opencl.py:265-314, with a real sm_100a binary) --------------- */
+/* NVRTC version the runtime compiles with (the toolkit's libnvrtc, loaded by
+   absolute path so an older libnvrtc already in the process is not used). */
+int dpia_nvrtc_version(int* major, int* minor);
 /* NVRTC: CUDA C source -> cubin for `arch` (e.g. "sm_100a").  `options` is a
  * '\n'-separated list of extra NVRTC flags.  On success *image points to a
  * malloc'ed cubin of *size bytes (release with dpia_free_host).  The compile

@@ -372,6 +372,21 @@ __device__ __forceinline__ void ring_wait(unsigned long long* mb, unsigned parit
   }
 }
 
+// --------------------------------------- chained launches (PDL, sm_90+)
+// pdl_trigger: this grid's dependent (the next launch on the stream, when it
+// was launched chained) may be scheduled now.  pdl_wait_once: wait, once per
+// thread, until the grid this one is chained behind has completed and its
+// memory is visible.  Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait_once(bool& pending) {
+  if (pending) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    pending = false;
+  }
+}
+
 __device__ __forceinline__ void grid_reset(unsigned int* counter, int tid) {
   if (tid == 0) *counter = 0u;
 }

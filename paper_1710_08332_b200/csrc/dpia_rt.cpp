@@ -41,10 +41,32 @@ decltype(&::cuLaunchKernelEx) cuLaunchKernelEx = nullptr;
 decltype(&::cuTensorMapEncodeTiled) cuTensorMapEncodeTiled = nullptr;
 }  // namespace drv
 
+// NVRTC is loaded the same way, by the absolute path of the toolkit the
+// runtime was built against (DPIA_NVRTC_PATH, set by runtime.build_lib;
+// $DPIA_NVRTC overrides), with RTLD_LOCAL: a process that already loaded an
+// older libnvrtc.so.12 (PyTorch ships one) would otherwise bind these calls
+// to it by SONAME, and an older NVRTC rejects sm_100 PTX such as the 256-bit
+// ld.global.v8.f32 the emitter uses.
+#define DPIA_NVRTC_FUNCS(X)                                                              \
+  X(nvrtcCreateProgram) X(nvrtcCompileProgram) X(nvrtcGetProgramLogSize)                  \
+  X(nvrtcGetProgramLog) X(nvrtcDestroyProgram) X(nvrtcGetCUBINSize) X(nvrtcGetCUBIN)      \
+  X(nvrtcGetErrorString) X(nvrtcVersion)
+
+#ifndef DPIA_NVRTC_PATH
+#define DPIA_NVRTC_PATH "libnvrtc.so.12"
+#endif
+
+namespace rtc {
+#define DPIA_DECL(f) decltype(&::f) f = nullptr;
+DPIA_NVRTC_FUNCS(DPIA_DECL)
+#undef DPIA_DECL
+}  // namespace rtc
+
 namespace {
 
 thread_local std::string g_err;
 void* g_libcuda = nullptr;
+void* g_libnvrtc = nullptr;
 
 int fail(int code, const char* fmt, ...) {
   char buf[1024];
@@ -70,6 +92,24 @@ int load_driver() {
       reinterpret_cast<decltype(drv::cuLaunchKernelEx)>(dlsym(g_libcuda, DPIA_STR(cuLaunchKernelEx)));
   drv::cuTensorMapEncodeTiled = reinterpret_cast<decltype(drv::cuTensorMapEncodeTiled)>(
       dlsym(g_libcuda, DPIA_STR(cuTensorMapEncodeTiled)));
+  return 0;
+}
+
+int load_nvrtc() {
+  if (g_libnvrtc) return 0;
+  static std::mutex m;
+  std::lock_guard<std::mutex> lock(m);
+  if (g_libnvrtc) return 0;
+  const char* env = getenv("DPIA_NVRTC");
+  void* h = dlopen(env && *env ? env : DPIA_NVRTC_PATH, RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return fail(-1, "cannot load NVRTC (%s): %s", DPIA_NVRTC_PATH, dlerror());
+#define DPIA_LOAD(f)                                                    \
+  rtc::f = reinterpret_cast<decltype(rtc::f)>(dlsym(h, DPIA_STR(f)));   \
+  if (!rtc::f) return fail(-1, "NVRTC lacks %s", DPIA_STR(f));
+  DPIA_NVRTC_FUNCS(DPIA_LOAD)
+#undef DPIA_LOAD
+  g_libnvrtc = h;
   return 0;
 }
 
@@ -220,12 +260,19 @@ int dpia_device_name(int device, char* buf, int len) {
   return 0;
 }
 
+int dpia_nvrtc_version(int* major, int* minor) {
+  if (int e = load_nvrtc()) return e;
+  nvrtcResult r = rtc::nvrtcVersion(major, minor);
+  return r == NVRTC_SUCCESS ? 0 : fail(r, "nvrtcVersion: %s", rtc::nvrtcGetErrorString(r));
+}
+
 int dpia_compile(const char* source, const char* program_name, const char* arch,
                  const char* options, void** image, size_t* size, char* log, size_t logcap) {
   if (log && logcap) log[0] = 0;
+  if (int e = load_nvrtc()) return e;
   nvrtcProgram prog;
-  nvrtcResult r = nvrtcCreateProgram(&prog, source, program_name, 0, nullptr, nullptr);
-  if (r != NVRTC_SUCCESS) return fail(r, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  nvrtcResult r = rtc::nvrtcCreateProgram(&prog, source, program_name, 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return fail(r, "nvrtcCreateProgram: %s", rtc::nvrtcGetErrorString(r));
   std::vector<std::string> opts;
   opts.push_back(std::string("--gpu-architecture=") + (arch && *arch ? arch : "sm_100a"));
   opts.push_back("--std=c++17");
@@ -242,32 +289,32 @@ int dpia_compile(const char* source, const char* program_name, const char* arch,
   }
   std::vector<const char*> cops;
   for (auto& o : opts) cops.push_back(o.c_str());
-  r = nvrtcCompileProgram(prog, static_cast<int>(cops.size()), cops.data());
+  r = rtc::nvrtcCompileProgram(prog, static_cast<int>(cops.size()), cops.data());
   size_t lsz = 0;
-  nvrtcGetProgramLogSize(prog, &lsz);
+  rtc::nvrtcGetProgramLogSize(prog, &lsz);
   if (log && logcap && lsz > 1) {
     std::string l(lsz, '\0');
-    nvrtcGetProgramLog(prog, &l[0]);
+    rtc::nvrtcGetProgramLog(prog, &l[0]);
     size_t n = lsz < logcap ? lsz : logcap - 1;
     memcpy(log, l.data(), n);
     log[n] = 0;
   }
   if (r != NVRTC_SUCCESS) {
-    nvrtcDestroyProgram(&prog);
-    return fail(r, "nvrtcCompileProgram: %s (see log)", nvrtcGetErrorString(r));
+    rtc::nvrtcDestroyProgram(&prog);
+    return fail(r, "nvrtcCompileProgram: %s (see log)", rtc::nvrtcGetErrorString(r));
   }
   size_t n = 0;
-  r = nvrtcGetCUBINSize(prog, &n);
+  r = rtc::nvrtcGetCUBINSize(prog, &n);
   if (r != NVRTC_SUCCESS) {
-    nvrtcDestroyProgram(&prog);
-    return fail(r, "nvrtcGetCUBINSize: %s", nvrtcGetErrorString(r));
+    rtc::nvrtcDestroyProgram(&prog);
+    return fail(r, "nvrtcGetCUBINSize: %s", rtc::nvrtcGetErrorString(r));
   }
   void* buf = malloc(n);
-  r = nvrtcGetCUBIN(prog, static_cast<char*>(buf));
-  nvrtcDestroyProgram(&prog);
+  r = rtc::nvrtcGetCUBIN(prog, static_cast<char*>(buf));
+  rtc::nvrtcDestroyProgram(&prog);
   if (r != NVRTC_SUCCESS) {
     free(buf);
-    return fail(r, "nvrtcGetCUBIN: %s", nvrtcGetErrorString(r));
+    return fail(r, "nvrtcGetCUBIN: %s", rtc::nvrtcGetErrorString(r));
   }
   *image = buf;
   *size = n;

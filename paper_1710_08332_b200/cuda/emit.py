@@ -68,6 +68,11 @@ VEC_LOAD_BYTES = int(os.environ.get("DPIA_VEC_LOAD_BYTES", "32"))
 # copies of TAIL_RING_BYTES per stream; DPIA_TAIL_RING=0 uses the register
 # queue instead.
 TAIL_RING = os.environ.get("DPIA_TAIL_RING", "1") != "0"
+# A program's first kernel can be chained behind the previous launch on its
+# stream with programmatic dependent launch (Executable.launch(chain=True)):
+# it waits for that grid only before touching non-input global memory
+# (ProgramEmitter._chain_waits); DPIA_CHAIN=0 emits no chaining code.
+CHAIN = os.environ.get("DPIA_CHAIN", "1") != "0"
 TAIL_RING_STAGES = int(os.environ.get("DPIA_TAIL_RING_STAGES", "4"))
 TAIL_RING_BYTES = int(os.environ.get("DPIA_TAIL_RING_BYTES", "2048"))
 TAIL_RING_UNROLL = int(os.environ.get("DPIA_TAIL_RING_UNROLL", "16"))
@@ -1928,6 +1933,15 @@ class ProgramEmitter:
             # runs and waits here until that grid has completed and its memory
             # is visible (a no-op under an ordinary launch)
             head.append('  asm volatile("griddepcontrol.wait;" ::: "memory");')
+        elif CHAIN:
+            # the first phase may itself be chained behind the previous launch
+            # of a program on the stream (Executable.launch(chain=True)): it
+            # lets its own dependent launch early, streams its inputs at once
+            # and waits for that grid only before it first touches memory the
+            # grid may still use (`_chain_waits`); all no-ops when not chained
+            head.append("  dpia::pdl_trigger();")
+            head.append("  bool dpia_chained = true;")
+            body_lines = self._chain_waits(body_lines, args)
         if ke.uses_gid:
             wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
             it = "long long" if wide else "int"
@@ -1940,6 +1954,31 @@ class ProgramEmitter:
                           barriers=frozenset(ke.barriers), hoisted=frozenset(ke.hoisted),
                           rotated=dict(ke.rotated), decls=list(decls))
         return text, info
+
+    @staticmethod
+    def _chain_waits(lines: List[str], args) -> List[str]:
+        """Insert `dpia::pdl_wait_once` before every line of a first-phase
+        kernel that names a non-input global buffer (an output, a scratch
+        buffer, the fused tail's counter, the peer mailboxes): the inputs are
+        read-only for both chained grids, everything else may still be read
+        or written by the grid this one is chained behind.  The wait runs
+        once per thread (a flag), so sites inside loops cost a predicate
+        test; a site right after a #pragma is fenced before the pragma."""
+        names = [n for kind, n in args if kind != "in" and kind != "size"]
+        names = [n for n in names] + [n + "_raw" for n in names]
+        if not names:
+            return lines
+        pat = re.compile(r"\b(" + "|".join(re.escape(n) for n in names) + r")\b")
+        out: List[str] = []
+        for ln in lines:
+            if pat.search(ln):
+                ind = ln[:len(ln) - len(ln.lstrip())]
+                at = len(out)
+                if at and out[-1].lstrip().startswith("#pragma"):
+                    at -= 1
+                out.insert(at, f"{ind}dpia::pdl_wait_once(dpia_chained);")
+            out.append(ln)
+        return out
 
     def _kernel_names(self, grid, tail):
         names = set()

@@ -105,7 +105,15 @@ class Executable:
         return LY.from_bytes(raw, d, self.sigma, self.float_mode)
 
     # ------------------------------------------------------------ launch
-    def launch(self, stream: Optional[RT.Stream] = None):
+    def launch(self, stream: Optional[RT.Stream] = None, chain: bool = False):
+        """Launch the program's kernels on `stream`.  chain=True: the first
+        kernel is launched with programmatic dependent launch behind the
+        previous kernel on the stream -- it starts streaming its inputs while
+        that grid drains and waits for it only before touching any other
+        global memory (cuda/emit.py ProgramEmitter._chain_waits).  The caller
+        asserts that the previous kernel writes none of this program's
+        inputs (true for back-to-back launches of programs over their own
+        inputs, e.g. repeated steps); results are identical either way."""
         if self.peer is not None:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
@@ -115,9 +123,9 @@ class Executable:
             # later phases: programmatic dependent launch (their first
             # statement is griddepcontrol.wait), which hides their launch
             # latency behind the previous phase
-            RT.launch(fn, self.device, grid, l, k.smem, vals, stream, pdl=i > 0)
+            RT.launch(fn, self.device, grid, l, k.smem, vals, stream, pdl=i > 0 or chain)
 
-    def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int]):
+    def launch_with(self, stream: Optional[RT.Stream], ptrs: Dict[str, int], chain: bool = False):
         """Launch with some parameters re-pointed (device addresses), e.g. at
         windows of larger buffers -- the row chunks of pipeline.RowPipeline.
         Windows must be 16-byte aligned -- the emitted kernels read their
@@ -137,7 +145,7 @@ class Executable:
                     for (kind, n), v in zip(k.args, vals)]
             grid = g if k.grid == "launch" else (1, 1)
             RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream,
-                      pdl=i > 0)
+                      pdl=i > 0 or chain)
 
     def run(self, inputs: Dict[str, object], stream: Optional[RT.Stream] = None,
             out: Optional[Dict[str, np.ndarray]] = None) -> Dict[str, np.ndarray]:

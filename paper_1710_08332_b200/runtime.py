@@ -29,6 +29,7 @@ _PROTOS = {
     "dpia_device_count": (_i, [C.POINTER(_i)]),
     "dpia_device_attribute": (_i, [_i, _i, C.POINTER(_i)]),
     "dpia_device_name": (_i, [_i, C.c_char_p, _i]),
+    "dpia_nvrtc_version": (_i, [C.POINTER(_i), C.POINTER(_i)]),
     "dpia_compile": (_i, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.POINTER(_vp),
                           C.POINTER(_sz), C.c_char_p, _sz]),
     "dpia_module_load": (_i, [_i, _vp, C.POINTER(_vp)]),
@@ -119,9 +120,9 @@ def build_lib(out: str = LIB_PATH, verbose: bool = False) -> str:
     tmp = f"{out}.{os.getpid()}.tmp"
     cmd = ["g++", "-O2", "-shared", "-fPIC", "-std=c++17", "-Wall",
            "-I", os.path.join(root, "include"), "-I", os.path.join(cuda, "include"),
-           os.path.join(PKG, "csrc", "dpia_rt.cpp"),
-           "-L", os.path.join(cuda, "lib64"), "-lnvrtc", "-ldl",
-           "-Wl,-rpath," + os.path.join(cuda, "lib64"), "-o", tmp]
+           "-DDPIA_NVRTC_PATH=\"" + os.path.join(os.path.realpath(os.path.join(cuda, "lib64")),
+                                                  "libnvrtc.so.12") + "\"",
+           os.path.join(PKG, "csrc", "dpia_rt.cpp"), "-ldl", "-o", tmp]
     if verbose:
         print("+", " ".join(cmd[:-1] + [out]), flush=True)
     try:
@@ -184,6 +185,13 @@ def cubin_key(src: str, arch: str = ARCH, opts: Sequence[str] = NVRTC_OPTS) -> s
         h.update(part.encode())
         h.update(b"\0")
     return h.hexdigest()[:32]
+
+
+def nvrtc_version():
+    """(major, minor) of the NVRTC the runtime compiles with."""
+    a, b = C.c_int(), C.c_int()
+    lib().dpia_nvrtc_version(C.byref(a), C.byref(b))
+    return a.value, b.value
 
 
 def nvrtc_compile(src: str, name: str = "dpia.cu", arch: str = ARCH,

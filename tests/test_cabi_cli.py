@@ -246,3 +246,22 @@ def test_cli_fuzz_arguments_and_report(tmp_path):
     root = ET.parse(tmp_path / "r.xml").getroot()
     assert root.get("tests") == "2" and root.get("failures") == "1"
     assert root.findall("testcase")[1].find("failure").get("message").startswith("GPU")
+
+
+def test_nvrtc_is_the_toolkits_even_with_an_older_one_loaded():
+    """The runtime binds NVRTC by the toolkit's absolute path (RTLD_LOCAL):
+    an older libnvrtc.so.12 already in the process (PyTorch's wheel ships
+    12.8) must not capture the calls -- it rejects the sm_100 256-bit loads
+    (ld.global.v8.f32) the emitter's fold queues use."""
+    import ctypes
+    import glob
+    import sys
+    for p in glob.glob(os.path.join(sys.prefix, "lib", "python3*", "site-packages", "nvidia",
+                                    "cuda_nvrtc", "lib", "libnvrtc.so.12")):
+        ctypes.CDLL(p, mode=ctypes.RTLD_GLOBAL)
+    assert RT.nvrtc_version() >= (12, 9)
+    img = RT.nvrtc_compile('extern "C" __global__ void k(float* p) { float a0,a1,a2,a3,a4,a5,a6,a7;\n'
+                           'asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];" : "=f"(a0),'
+                           '"=f"(a1),"=f"(a2),"=f"(a3),"=f"(a4),"=f"(a5),"=f"(a6),"=f"(a7) : "l"(p));\n'
+                           'p[0] = a0+a1+a2+a3+a4+a5+a6+a7; }')
+    assert img[:4] == b"\x7fELF"

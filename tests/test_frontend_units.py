@@ -347,3 +347,44 @@ def test_vectorised_fold_pipelining(monkeypatch):
     assert "+= 128)" in body_s and "+ 4 < 128) pfq_" in body_s
     body0, _ = emit(VEC_PREFETCH=0, TAIL_RING=False)
     assert "pfq_" not in body0 and "ring_" not in body0
+
+
+def test_chain_waits_emission(monkeypatch):
+    """CPU: a program's first kernel triggers its dependent launch at once
+    and waits (once per thread) for the grid it is chained behind right
+    before each line naming a non-input global buffer -- never before a
+    line that only reads inputs, never between a #pragma and its loop;
+    later phases keep their griddepcontrol.wait at the top; DPIA_CHAIN=0
+    emits none of it."""
+    import re
+    from paper_1710_08332_b200 import compile_program
+    from paper_1710_08332_b200.bench_programs import dot_config
+    from paper_1710_08332_b200.cuda import emit as E
+    cfg = dot_config(N=1 << 20)
+    prog = compile_program(cfg.text)
+    outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    src, sig = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    lines = src.split('extern "C"')[1].splitlines()
+    assert "dpia::pdl_trigger();" in lines[3] or any("pdl_trigger" in ln for ln in lines[:8])
+    waits = [i for i, ln in enumerate(lines) if "pdl_wait_once" in ln]
+    assert waits
+    start = next(i for i, ln in enumerate(lines) if "bool dpia_chained" in ln)
+    first_global = min(i for i, ln in enumerate(lines)
+                       if i > start and re.search(r"\b(out|g_tmp\w*|dpia_counter)\b", ln))
+    assert waits[0] == first_global - 1
+    for i in waits:
+        assert not lines[i - 1].lstrip().startswith("#pragma")
+        assert re.search(r"\b(out|g_tmp\w*|dpia_counter)\b", lines[i + 1])
+    # the vectorised loads of the inputs come before the first wait
+    assert any("xs" in ln for ln in lines[:waits[0]])
+    two = compile_program("(nat n)\n(param xs (exp (array n num)))\n"
+                          "(mapGlobal (lam x (+ x 1)) (toGlobal (lam t t) (mapGlobal (lam y (* y 2)) xs)))")
+    s2, sig2 = E.emit_cuda(two.imperative, [("out", two.out_type)], [("xs", two.source.params[0][1].data)],
+                           sigma={"n": 4096}, launch=(16, 256))
+    k1 = s2.split("KERNEL_k1")[1]
+    assert "griddepcontrol.wait" in k1.splitlines()[4] or "griddepcontrol.wait" in "".join(k1.splitlines()[:6])
+    assert "pdl_wait_once" not in k1
+    monkeypatch.setattr(E, "CHAIN", False)
+    s0, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    body0 = s0.split('extern "C"')[1]
+    assert "pdl_" not in body0

@@ -12,6 +12,9 @@ from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 SRC = r"""
 extern "C" __global__ void __launch_bounds__(1024) readsum(const float4* __restrict__ p, long long n4,
                                                            float* out) {
+  // a chained launch (bench.read_sol's steady timing) may start now; the
+  // kernel writes nothing it reads, so it never waits for its predecessor
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long stride = (long long)gridDim.x * blockDim.x;

@@ -27,14 +27,16 @@ from paper_1710_08332_b200.bench_programs import (asum_config, dot_config, dot_l
 L2 = 126 * 1024 * 1024
 
 
-def measure(name, cfg, shapes, st, rng, K=50):
-    """(isolated mean us, steady-state median us) of one config."""
+def measure(name, cfg, shapes, st, rng, K=50, chain=False, R=None):
+    """(isolated mean us, steady-state median us, R, runs) of one config;
+    chain: the steady-state steps are chained (Executable.launch_with(chain=
+    True)); R: input sets (default: enough for 3 x L2)."""
     exe = executable(compile_program(cfg.text, name=name.split("_")[0]), cfg.launch, cfg.sigma,
                      float_mode=True)
     if "alpha" in dict(exe.sig.inputs):
         exe.upload("alpha", np.full(4, 1.5, np.float32), st)
     step_bytes = sum(4 * v for v in shapes.values())
-    R = max(2, -(-3 * L2 // step_bytes))
+    R = R or max(2, -(-3 * L2 // step_bytes))
     sets = []
     for r in range(R):
         bufs = {}
@@ -46,8 +48,8 @@ def measure(name, cfg, shapes, st, rng, K=50):
     st.sync()
     ptrs = [{n: b.ptr for n, b in s.items()} for s in sets]
 
-    def launch(i):
-        exe.launch_with(st, ptrs[i % R])
+    def launch(i, ch=False):
+        exe.launch_with(st, ptrs[i % R], chain=ch)
     iso = []
     for it in range(K + 5):
         RT.lib().dpia_l2_flush(0, st.handle)
@@ -59,14 +61,14 @@ def measure(name, cfg, shapes, st, rng, K=50):
         if it >= 5:
             iso.append(e0.elapsed_ms(e1))
     for i in range(6):
-        launch(i)
+        launch(i, chain)
     st.sync()
     runs = []
     for rep in range(5):
         e0, e1 = RT.Event(0), RT.Event(0)
         e0.record(st)
         for i in range(K):
-            launch(i)
+            launch(i, chain)
         e1.record(st)
         st.sync()
         runs.append(e0.elapsed_ms(e1) / K)
@@ -86,12 +88,16 @@ def main():
             ("gemv", gemv_config(), {"A": 8192 * 8192, "x": 8192}),
             ("gemv_xprivate", gemv_config(x_private=True), {"A": 8192 * 8192, "x": 8192}),
             ("scal", scal_config(), {"xs": 1 << 26})]
+    chains = (False, True) if "--chain" in sys.argv else (False,)
     for name, cfg, shapes in cfgs:
-        iso_us, ss_us, R, runs = measure(name, cfg, shapes, st, rng)
-        print(f"{name:14s} R={R}: isolated {iso_us:7.2f} us ({cfg.bytes / iso_us / 1e3:6.0f} GB/s, "
-              f"frac {cfg.bytes / iso_us / 1e3 / 6554.9:.3f})   steady {ss_us:7.2f} us "
-              f"({cfg.bytes / ss_us / 1e3:6.0f} GB/s, frac {cfg.bytes / ss_us / 1e3 / 6554.9:.3f})  "
-              f"runs {[round(r * 1e3, 2) for r in runs]}", flush=True)
+        for chain in chains:
+            for R in ((None, 2, 4, 8) if "--sets" in sys.argv else (None,)):
+                iso_us, ss_us, R_, runs = measure(name, cfg, shapes, st, rng, chain=chain, R=R)
+                print(f"{name:14s} chain={int(chain)} R={R_}: isolated {iso_us:7.2f} us "
+                      f"({cfg.bytes / iso_us / 1e3:6.0f} GB/s, frac {cfg.bytes / iso_us / 1e3 / 6554.9:.3f})"
+                      f"   steady {ss_us:7.2f} us ({cfg.bytes / ss_us / 1e3:6.0f} GB/s, "
+                      f"frac {cfg.bytes / ss_us / 1e3 / 6554.9:.3f})  runs {[round(r * 1e3, 2) for r in runs]}",
+                      flush=True)
 
 
 if __name__ == "__main__":
