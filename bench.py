@@ -63,6 +63,9 @@ def fp32_peak(device):
 _SOL_CACHE = {}
 
 
+NOMINAL_HBM_GBS = 7700.0     # B200 HBM3e, HGX figure (B200_PROFILING.md)
+
+
 def l2_bytes(device):
     return RT.device_attribute(device, 38) or (126 << 20)     # CU_DEVICE_ATTRIBUTE_L2_CACHE_SIZE
 
@@ -833,6 +836,10 @@ def main():
                     "traffic": None,
                     "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs)",
                     "algorithmic_bytes_per_launch": cfg.bytes, "kernel_ms": round(kmean, 5)}
+            # context for fractions above 1 of the copy peak (reads stream
+            # faster than a read+write copy): the part's nominal HBM3e rate
+            roof["nominal_gbs"] = NOMINAL_HBM_GBS
+            roof["frac_of_nominal"] = round(achieved / NOMINAL_HBM_GBS, 4)
             if workload in ("asum", "dot", "gemv"):
                 sol = read_sol(device, cfg.bytes, stream)
                 roof["size_matched_read_sol_gbs"] = sol["steady"]
