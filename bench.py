@@ -810,6 +810,14 @@ def main():
         # the round-1 method beside it: each launch alone after an L2 scrub
         iso = run_isolated(exe, stream, steps, allreduce)
         iso_ms = statistics.mean(iso)
+        # and the steady state without chaining (the same rotation, each step
+        # launched after the previous one completed)
+        unch_ms = None
+        if rot.chain:
+            rot.chain = False
+            rot.run(stream, 3, allreduce)
+            unch_ms = rot.run(stream, steps, allreduce)
+            rot.chain = True
         rot_desc = {"input_sets": rot.R, "l2_bytes": l2_bytes(device),
                     "bytes_per_step": cfg.bytes, "chained": rot.chain}
         rot.free()
@@ -865,6 +873,13 @@ def main():
                       "(profiles/r01f_tailexp4.txt)"}
         if workload in ("asum", "dot", "gemv"):
             roof["isolated"]["size_matched_read_sol_gbs"] = read_sol(device, cfg.bytes, stream)["isolated"]
+        if unch_ms:
+            ua = work / (unch_ms * 1e-3) / (1e12 if workload == "mm" else 1e9)
+            roof["unchained"] = {
+                "ms_per_step": round(unch_ms, 5), "achieved": round(ua, 2 if workload == "mm" else 1),
+                "frac": round(ua / roof["peak"], 4),
+                "method": "the same rotation back to back, each step launched without chaining "
+                          "(bench.py --no-chain)"}
         res = {"cfg": cfg, "exe": exe, "mean_ms": mean_ms, "wall_s": wall, "clocks": clk.summary(),
                "value": value, "roofline": roof, "rotation": rot_desc}
         if check is not None:
