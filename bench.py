@@ -34,7 +34,7 @@ from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
                                                   dot_literal_config, gemv_config, mm_config,
-                                                  scal_config)
+                                                  mm_tma_config, scal_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
 
@@ -307,8 +307,8 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
     elif name == "scal":
         cfg = scal_config()
         inputs = {"alpha": np.full(4, 1.5, np.float32), "xs": _seeded(1 << 26, 7, -1.0, 1.0)}
-    elif name == "mm":
-        cfg = mm_config()
+    elif name in ("mm", "mm_tma"):
+        cfg = mm_config() if name == "mm" else mm_tma_config()
         inputs = {"A": _seeded((4096, 4096), 5, -1.0, 1.0), "B": _seeded((4096, 4096), 6, -1.0, 1.0)}
     else:
         raise SystemExit(f"unknown workload {name}")
@@ -317,7 +317,7 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
     if allgather is not None and name in ("asum", "dot", "dot_literal"):
         from paper_1710_08332_b200.peer import PeerGroup
         peer = PeerGroup(device, rank, world, 1, allgather)
-    exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device, peer=peer)
+    exe = executable(prog, cfg.launch, cfg.sigma, float_mode=True, device=device, peer=peer, **cfg.emit)
 
     def prepare(stream):
         for n, v in inputs.items():
@@ -545,6 +545,7 @@ REF_STRATEGY = {
 }
 REF_STRATEGY["dot_literal"] = REF_STRATEGY["dot"]
 REF_STRATEGY["gemv_xprivate"] = REF_STRATEGY["gemv"]
+REF_STRATEGY["mm_tma"] = REF_STRATEGY["mm"]
 
 
 def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1):
@@ -555,7 +556,7 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         return None
     vp, ci = ctypes.c_void_p, ctypes.c_int
     out = np.zeros(8192, np.float32)
-    base = workload
+    base = "mm" if workload == "mm_tma" else workload
     note = ""
     if workload.startswith("scaleout"):
         # the reference's emitted C indexes with 32-bit int and keeps the
@@ -637,7 +638,7 @@ def reference_arm(args):
     workload (oracle/_ref, its c-openmp emission, all host threads), on the
     same metric, unit and workload as our arm; each step one call."""
     r = cpu_reference(args.workload, steps=args.steps, warmup=args.warmup)
-    unit = "GFLOP/s" if args.workload == "mm" else "GB/s"
+    unit = "GFLOP/s" if args.workload.startswith("mm") else "GB/s"
     wl, strat = REF_STRATEGY.get(args.workload, (args.workload, "none"))
     line = {"impl": "reference", "metric": METRIC, "unit": unit, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
@@ -821,7 +822,7 @@ def main():
         rot_desc = {"input_sets": rot.R, "l2_bytes": l2_bytes(device),
                     "bytes_per_step": cfg.bytes, "chained": rot.chain}
         rot.free()
-        if workload == "mm":
+        if workload.startswith("mm"):
             fp32 = fp32_peak(device)
             achieved = cfg.flops / (kmean * 1e-3) / 1e12
             value = world * cfg.flops / (mean_ms * 1e-3) / 1e9
@@ -862,21 +863,21 @@ def main():
             roof["traffic_source"] = tsrc
             if t:
                 roof["traffic_over_algorithmic"] = round(t / cfg.bytes, 4)
-        work = cfg.flops if workload == "mm" else cfg.bytes
+        work = cfg.flops if workload.startswith("mm") else cfg.bytes
         roof["isolated"] = {
             "ms_per_launch": round(iso_ms, 5),
-            "achieved": round(work / (iso_ms * 1e-3) / (1e12 if workload == "mm" else 1e9),
-                              2 if workload == "mm" else 1),
-            "frac": round(work / (iso_ms * 1e-3) / (1e12 if workload == "mm" else 1e9) / roof["peak"], 4),
+            "achieved": round(work / (iso_ms * 1e-3) / (1e12 if workload.startswith("mm") else 1e9),
+                              2 if workload.startswith("mm") else 1),
+            "frac": round(work / (iso_ms * 1e-3) / (1e12 if workload.startswith("mm") else 1e9) / roof["peak"], 4),
             "method": "each launch alone between its own event pair, after an L2 scrub (round-1 "
                       "timing): adds the event pair and an unhidden launch, ~6 us "
                       "(profiles/r01f_tailexp4.txt)"}
         if workload in ("asum", "dot", "gemv"):
             roof["isolated"]["size_matched_read_sol_gbs"] = read_sol(device, cfg.bytes, stream)["isolated"]
         if unch_ms:
-            ua = work / (unch_ms * 1e-3) / (1e12 if workload == "mm" else 1e9)
+            ua = work / (unch_ms * 1e-3) / (1e12 if workload.startswith("mm") else 1e9)
             roof["unchained"] = {
-                "ms_per_step": round(unch_ms, 5), "achieved": round(ua, 2 if workload == "mm" else 1),
+                "ms_per_step": round(unch_ms, 5), "achieved": round(ua, 2 if workload.startswith("mm") else 1),
                 "frac": round(ua / roof["peak"], 4),
                 "method": "the same rotation back to back, each step launched without chaining "
                           "(bench.py --no-chain)"}
@@ -890,7 +891,7 @@ def main():
             e2e_ms, h2d, d2h = e2e_measure(exe, inputs, stream, min(steps, 5))
             if dist is not None:   # whole job: every rank's bytes over the slowest rank's time
                 e2e_ms = float(_allreduce(dist, e2e_ms, dist.ReduceOp.MAX, local, share))
-            work, unit = (cfg.flops, "GFLOP/s") if workload == "mm" else (cfg.bytes, "GB/s")
+            work, unit = (cfg.flops, "GFLOP/s") if workload.startswith("mm") else (cfg.bytes, "GB/s")
             res["e2e"] = {"value": round(world * work / (e2e_ms * 1e-3) / 1e9, 3), "unit": unit,
                           "h2d_link_gbs": _LINK_GBS,
                           "h2d_link_note": "pinned H2D of the same input bytes alone, measured in the "
@@ -939,14 +940,14 @@ def main():
     # N = 1: every benchmark program; N > 1: the sharded reductions of
     # BASELINE config 5 (2^31 in total, strong scaling) beside the weak-scaled
     # headline -- gemv / mm / scal would only replicate (no exchange step)
-    names = (("dot", "dot_literal", "asum", "gemv", "gemv_xprivate", "mm", "scal",
+    names = (("dot", "dot_literal", "asum", "gemv", "gemv_xprivate", "mm", "mm_tma", "scal",
               "scaleout_asum", "scaleout_dot") if world == 1 else ("scaleout_asum", "scaleout_dot"))
     if not args.no_suite:
         for w in names:
             if w == args.workload:
                 continue
             r = measure(w, min(args.steps, 20), 3, with_e2e=True)
-            suite[w] = {"value": round(r["value"], 1), "unit": "GFLOP/s" if w == "mm" else "GB/s",
+            suite[w] = {"value": round(r["value"], 1), "unit": "GFLOP/s" if w.startswith("mm") else "GB/s",
                         "ms_per_step": round(r["mean_ms"], 5), "roofline": r["roofline"],
                         "scaling": "strong" if w.startswith("scaleout") else "weak",
                         "e2e": r.get("e2e"), "clocks": r["clocks"],
@@ -972,7 +973,7 @@ def main():
     cfg, exe = head["cfg"], head["exe"]
     strong = args.workload.startswith("scaleout")
     line = {"metric": METRIC, "value": round(head["value"], 2),
-            "unit": "GFLOP/s" if args.workload == "mm" else "GB/s", "n_gpus": world,
+            "unit": "GFLOP/s" if args.workload.startswith("mm") else "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(head["mean_ms"], 5),
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f32",
@@ -1108,6 +1109,9 @@ WORKLOADS = {
     "scal": ("scal N=2^26 fp32 (read + write)", "grid-stride mapGlobal over vec4"),
     "mm": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "128x128 tiles, 8x8 register tiles, toLocal "
            "k-tiles of 16, FFMA2"),
+    "mm_tma": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "the mm strategy with B's toLocal k-tile "
+               "staged by TMA tensor copies (cp.async.bulk.tensor.2d, 3 rotating slices, mbarrier); "
+               "A's transposed k-tile by register prefetch"),
 }
 
 

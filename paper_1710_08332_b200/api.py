@@ -47,9 +47,10 @@ def compile_program(text: str, name: str = "KERNEL", check: bool = True) -> Prog
 
 
 def executable(prog: Program, launch, sigma: Optional[Dict[str, int]] = None,
-               float_mode: bool = True, device: int = 0, peer=None) -> Executable:
+               float_mode: bool = True, device: int = 0, peer=None,
+               tma_tiles: Optional[bool] = None) -> Executable:
     return build(prog.imperative, prog.params, launch, sigma, float_mode, device, prog.name,
-                 peer=peer)
+                 peer=peer, tma_tiles=tma_tiles)
 
 
 def run_program_cuda(prog: Program, inputs: Dict[str, object], sigma=None, launch=(148, 256),

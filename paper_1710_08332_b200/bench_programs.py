@@ -19,7 +19,7 @@ in tests/golden/programs.json and oracle/ref_programs/.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 from typing import Dict, Tuple
 
 
@@ -32,6 +32,7 @@ class Config:
     bytes: int = 0          # algorithmic bytes
     flops: int = 0
     float_mode: bool = True
+    emit: Dict[str, object] = field(default_factory=dict)   # emit_cuda options (tma_tiles)
 
 
 def dot_program(L: int = 256, K: int = 16) -> str:
@@ -368,6 +369,17 @@ def mm_config(M: int = 4096, N: int = 4096, K: int = 4096, T: int = 128, BK: int
                   bytes=4 * (M * K + K * N + M * N), flops=2 * M * N * K)
 
 
+def mm_tma_config(**kw) -> Config:
+    """The mm strategy with B's k-tile staged by TMA tensor copies
+    (cp.async.bulk.tensor.2d into three rotating slices, mbarrier
+    completion) instead of register prefetch + shared stores; A's k-tile is
+    stored transposed (k-major), which a TMA box copy cannot do, so it stays
+    on the register path.  Bit-identical to `mm`."""
+    cfg = mm_config(**kw)
+    cfg.name, cfg.emit = "mm_tma", {"tma_tiles": True}
+    return cfg
+
+
 def scal_program() -> str:
     """y = alpha * x (the paper's fourth BLAS kernel): one
     grid-stride mapGlobal over float4 vectors; alpha arrives as a (vec 4)
@@ -448,7 +460,7 @@ def gemv_xprivate_config(**kw) -> Config:
 
 CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
            "scal": scal_config, "dot_literal": dot_literal_config,
-           "gemv_xprivate": gemv_xprivate_config}
+           "gemv_xprivate": gemv_xprivate_config, "mm_tma": mm_tma_config}
 
 
 def aot_sources():
@@ -462,6 +474,6 @@ def aot_sources():
         outs = [("out", prog.out_type)]
         ins = [(n, t.data) for n, t in prog.source.params]
         src, _ = emit_cuda(prog.imperative, outs, ins, float_mode=cfg.float_mode, name=name,
-                           sigma=cfg.sigma, launch=cfg.launch)
+                           sigma=cfg.sigma, launch=cfg.launch, **cfg.emit)
         out.append((name, src))
     return out

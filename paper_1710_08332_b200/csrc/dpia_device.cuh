@@ -23,6 +23,9 @@
 //                          register queues of a work-item's sequential fold
 // * dpia::ring_*        -- a single thread's shared-memory ring of TMA bulk
 //                          copies (the top-level sequential fold of a tail)
+// * dpia::tma_tile_2d   -- one 2-D box of an input (a toLocal k-tile) as a
+//                          TMA tensor copy (cp.async.bulk.tensor.2d through a
+//                          CUtensorMap kernel parameter, mbarrier complete_tx)
 //
 // Self-contained: NVRTC compiles it without any system header.
 #pragma once
@@ -385,6 +388,39 @@ __device__ __forceinline__ void pdl_wait_once(bool& pending) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     pending = false;
   }
+}
+
+// --------------------------------------------- 2-D TMA tensor tiles
+// The CUtensorMap of an input, passed by value as a __grid_constant__ kernel
+// parameter (runtime: dpia_tensor_map_2d).  tma_tile_2d: the issuing thread
+// announces `bytes` on the slice's mbarrier and copies the box whose
+// innermost coordinate is x and row coordinate y into shared memory
+// (plain row-major box layout); waiters use ring_wait on the same mbarrier.
+// The slice was last read through the generic proxy (the previous use of
+// the rotating buffer), and every such read is ordered before this call by
+// the CTA barrier the caller issues it after -- the same release the
+// consumer arrive of a full/empty mbarrier pipeline gives; no proxy fence.
+struct alignas(64) TensorMap {
+  unsigned long long w[16];
+};
+__device__ __forceinline__ void tile_bar_init(unsigned long long* mb, int slots, unsigned count) {
+  for (int s = 0; s < slots; ++s) {
+    const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb + s));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(count) : "memory");
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_tile_2d(void* dst, const TensorMap* map, int x, int y,
+                                            unsigned bytes, unsigned long long* mb) {
+  const unsigned b = static_cast<unsigned>(__cvta_generic_to_shared(mb));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+        "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(b)
+      : "memory");
 }
 
 __device__ __forceinline__ void grid_reset(unsigned int* counter, int tid) {

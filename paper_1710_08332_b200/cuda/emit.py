@@ -83,6 +83,24 @@ BULK_STAGE = os.environ.get("DPIA_BULK_STAGE", "1") != "0"
 # work-item loops of a pipelined staging may take up to this many iterations
 # per thread (unrolled into guarded copies, one prefetch register set each)
 PF_MAX_COPIES = 4
+# a rotating toLocal k-tile that is a plain 2-D box of an input can be staged
+# by TMA tensor copies (cp.async.bulk.tensor.2d + mbarrier) instead of
+# register prefetch + shared stores: KernelEmitter._tma_plan.  Off unless a
+# program asks (emit_cuda(tma_tiles=True)) or DPIA_TMA_TILES=1: on the mm
+# config it is bit-identical and 1-2% slower than the register path
+# (profiles/r02c_tma_mm.txt)
+TMA_TILES = os.environ.get("DPIA_TMA_TILES", "0") == "1"
+TMA_PROBE_MAX = 1 << 16            # copy statements the box probe may enumerate
+# slices of a TMA-staged tile: 2 -- iteration k+1's box is issued right after
+# iteration k's CTA barrier; 3 -- it is issued at the top of iteration k, into
+# the slice iteration k-2 read (free since iteration k-1's barrier)
+TMA_SLOTS = int(os.environ.get("DPIA_TMA_SLOTS", "3"))
+# row bands a box is issued in (one per warp, lane 0); 1 = thread 0 issues
+TMA_BANDS = int(os.environ.get("DPIA_TMA_BANDS", "1"))
+
+
+class _ProbeFail(Exception):
+    """The staging command is not a plain box copy (KernelEmitter._tma_plan)."""
 # bank-conflict layout of local buffers whose rows are a multiple of 32
 # scalars (see KernelEmitter._declare_local): swizzle | pad | none
 SMEM_LAYOUT = os.environ.get("DPIA_SMEM_LAYOUT", "swizzle")
@@ -190,6 +208,8 @@ class CudaSignature:
     sigma: Optional[Dict[str, int]]
     spaces: Dict[str, str] = field(default_factory=dict, repr=False)   # buffer binder -> space
     align: Dict[str, int] = field(default_factory=dict, repr=False)    # buffer -> bytes (> 16) its loads need
+    # tensor-map parameter -> (input, element bytes, rows, cols, row pitch bytes, box rows, box cols)
+    tmaps: Dict[str, Tuple[str, int, int, int, int, int, int]] = field(default_factory=dict, repr=False)
 
     def params(self) -> List[str]:
         out = [f"{self.scalar} *{n}" for n, _ in self.outputs]
@@ -498,6 +518,11 @@ class KernelEmitter:
         self.vec_vars: Dict[str, int] = {}   # loop counter -> lane width of an unrolled fold
         self.vec_hits = 0
         self.vec_pf: Optional[dict] = None   # the innermost prefetching fold (`_vec_loop`)
+        self.probing = False                 # `_tma_plan`: enumerate and record, emit nothing
+        self.probe_recs: List[tuple] = []
+        self.probe_src: Optional[tuple] = None
+        self.barrier_hooks: List[Tuple[int, List[str]]] = []   # (loop depth, lines after the next barrier)
+        self.tmaps_used: List[str] = []
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -728,7 +753,14 @@ class KernelEmitter:
                             f"{self.r(ref.at)}).v[{self.r(lane)}]")
                 return self.resolve(args[0], [("i", i * w + lane)] + rest)
             if aligned:
+                if self.probing:
+                    self.probe_src = (ref.buf, ref.at, w)
                 return f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, {self.r(ref.at)})"
+            if self.probing:
+                refs = [self.resolve(args[0], [("i", i * w + k)]) for k in range(w)]
+                if all(isinstance(r, Ref) and r.flat is not None and not r.suffix and r.addr is None
+                       and r.buf is refs[0].buf for r in refs):
+                    self.probe_src = (refs[0].buf, [r.flat for r in refs], w)
             lanes = ", ".join(self.exp(args[0], [("i", i * w + k)]) for k in range(w))
             return f"dpia::vec<{self.scalar}, {w}>{{{{{lanes}}}}}"
         if name.startswith("asScalar") and "Acc" not in name:
@@ -846,9 +878,13 @@ class KernelEmitter:
                 for k in range(d.width):
                     self.assign(Num(), a, e, steps + [("i", ix(k))])
                 return
+            if self.probing:
+                return self._probe_record(target, e, steps)
             rhs = self.exp(e, steps)
         else:
             target = self.acc(a, steps)
+            if self.probing:
+                return self._probe_record(target, e, steps)
             rhs = self.exp(e, steps)
         if self.pf is not None:
             mode, regs = self.pf
@@ -880,7 +916,7 @@ class KernelEmitter:
     def comm(self, p: Phrase):
         if id(p) in self.barriers and not self.per_thread and \
                 (self.pf is None or self.pf[0] == "commit"):
-            self.line("__syncthreads();")
+            self._barrier()
         u = unapply(p)
         if u is None:
             raise CudaError(f"not a command: {p!r}")
@@ -889,7 +925,7 @@ class KernelEmitter:
             return
         if name == "barrier":
             if not self.per_thread:
-                self.line("__syncthreads();")
+                self._barrier()
             return
         if name == ";":
             self.comm(args[0].fst)
@@ -1200,12 +1236,53 @@ class KernelEmitter:
             elif SMEM_LAYOUT == "pad":
                 buf.pad = 4
                 n = n // inner * (inner + 4)
-        off = self.alloc_smem(n * self._elem_bytes(split_array(full)[1]))
+        # 128-byte aligned: the bank arithmetic of the swizzle / padding
+        # above assumes each buffer starts in bank 0
+        off = self.alloc_smem(n * self._elem_bytes(split_array(full)[1]), align=128)
         ct = self.types.c_elem(split_array(full)[1])
         self.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
         return buf
 
     def new(self, prim: str, d: DataType, f: Lam, node: Phrase = None):
+        if node is not None and id(node) in self.pipelined and self.pipelined[id(node)][0] == "tma":
+            _, buf, (plan, mb, tm), c1, c2, binder, trip = self.pipelined[id(node)]
+            old = self.env.get(f.binder)
+            self.env[f.binder] = buf
+            k = self.env[binder].ixv
+            S = plan["slots"]
+            wait = (f"dpia::ring_wait({mb} + ({self.r(mod(k, S, self.R))}), "
+                    f"(unsigned)(({self.r(k)} / {S}) & 1));")
+            issue = self._tma_issue(plan, buf, mb, tm, k + 1, f"{self.r(k)} + 1 < {trip}")
+            # this iteration's tile: every thread observes its mbarrier
+            # phase right before the CTA barrier that precedes the first
+            # read of the buffer (the hazard planner always puts one there).
+            # The next tile goes into slice (k+1) % S: with 2 slices right
+            # after that barrier (the slice was read by iteration k-1); with
+            # 3 or more at once -- it was last read by iteration k-2, whose
+            # reads every thread finished before iteration k-1's barrier
+            if S >= 3:
+                self.line(issue)
+                issue = None
+            hook = (len(self.loops), [wait], [issue] if issue else [])
+            mark, ind, smem = len(self.lines), self.ind, self.smem
+            self.barrier_hooks.append(hook)
+            self.comm(c2)
+            if hook in self.barrier_hooks:
+                # no barrier at this level inside c2: every thread waits
+                # first, and the refill follows a barrier after c2
+                self.barrier_hooks.remove(hook)
+                del self.lines[mark:]
+                self.ind, self.smem = ind, smem
+                self.line(wait)
+                self.comm(c2)
+                self.line("__syncthreads();")
+                if issue:
+                    self.line(issue)
+            if old is None:
+                del self.env[f.binder]
+            else:
+                self.env[f.binder] = old
+            return
         if node is not None and id(node) in self.pipelined:
             buf, regs, c1, c2, binder, trip = self.pipelined[id(node)]
             old = self.env.get(f.binder)
@@ -1314,8 +1391,8 @@ class KernelEmitter:
             return n * self._tree_bytes(d.elem)
         return self._elem_bytes(d)
 
-    def alloc_smem(self, nbytes: int) -> int:
-        off = (self.smem + 15) // 16 * 16
+    def alloc_smem(self, nbytes: int, align: int = 16) -> int:
+        off = (self.smem + align - 1) // align * align
         self.smem = off + nbytes
         return off
 
@@ -1354,6 +1431,27 @@ class KernelEmitter:
 
     def loop(self, level: str, dim: int, n: Nat, binder: str, body, bind=None):
         trip = self.nat_int(n)
+        if self.probing:
+            # `_tma_plan`: every iteration of the staging's loops, with the
+            # loop index a constant, so each copy's indices are constants
+            # plus work-group-uniform terms
+            if trip is None or trip * max(1, len(self.probe_recs)) > TMA_PROBE_MAX:
+                raise _ProbeFail("unbounded or too large")
+            names = [binder] + ([bind[0]] if bind else [])
+            old = {nm: self.env.get(nm) for nm in names}
+            for t in range(trip):
+                self.loops.append(Loop(level, dim, "", 1, nat(1), True))
+                self.env[binder] = Val(Idx(n), ixv=ix(t))
+                if bind:
+                    self.env[bind[0]] = bind[1](ix(t))
+                body()
+                self.loops.pop()
+            for nm, ov in old.items():
+                if ov is None:
+                    self.env.pop(nm, None)
+                else:
+                    self.env[nm] = ov
+            return
         start, stride, S = self._geometry(level, dim)
         v = self.fresh(binder)
         # `v += stride` must not overflow either: the last increment reaches
@@ -1596,8 +1694,200 @@ class KernelEmitter:
                         self.for_plans[id(q)] = cands
         walk(body, frozenset())
 
+    # ------------------------------------------- TMA tensor k-tiles
+    def _barrier(self):
+        """A CTA barrier, with the lines waiting for the next barrier at
+        their own loop depth around it (a TMA-staged k-tile, `new`: one
+        thread observes the tile's mbarrier just before the barrier, which
+        then orders the landed tile before every thread's reads; the next
+        tile is issued right after it, when no thread still reads the slice
+        it overwrites)."""
+        now = [h for h in self.barrier_hooks if h[0] == len(self.loops)]
+        self.barrier_hooks = [h for h in self.barrier_hooks if h[0] != len(self.loops)]
+        for _d, pre, _post in now:
+            for ln in pre:
+                self.line(ln)
+        self.line("__syncthreads();")
+        for _d, _pre, post in now:
+            for ln in post:
+                self.line(ln)
+
+    def _probe_record(self, target, e: Phrase, steps):
+        """`_tma_plan`: one copy statement of the staging -- the local
+        destination index and the input source index of a whole vector (or
+        one scalar) -- instead of emitting it."""
+        self.probe_src = None
+        r = self.resolve(e, steps)
+        if isinstance(r, Ref):
+            if r.suffix or r.flat is None or r.addr is not None:
+                raise _ProbeFail("source path")
+            src = (r.buf, r.flat, 1)
+        elif self.probe_src is not None:
+            src = self.probe_src
+        else:
+            raise _ProbeFail("source is not a plain read")
+        if isinstance(target, VStore):
+            dst, w = target.ref, target.width
+        else:
+            dst, w = target, 1
+        if dst.suffix or dst.flat is None or dst.addr is not None or w != src[2]:
+            raise _ProbeFail("destination path")
+        if isinstance(src[1], list):       # a vector gathered lane by lane
+            for lane, flat in enumerate(src[1]):
+                self.probe_recs.append((dst.buf.key, dst.flat + lane, src[0], flat, 1))
+        else:
+            self.probe_recs.append((dst.buf.key, dst.flat, src[0], src[1], w))
+
+    def _tma_no(self, why: int):
+        self.tma_why = why          # which test rejected the last staging (tests, debugging)
+        return None
+
+    def _tma_plan(self, c1: Phrase, fl: Lam, d0: DataType, binder: str, n: Nat, trip: int):
+        """Is the staging command c1 of local buffer fl.binder (type d0) a
+        plain 2-D box copy of one input -- element (r, c) of the tile read
+        from X[origin(k) + r * P + c], origin linear in the staging loop's
+        index k?  Decided by enumerating c1's copies with every work-item
+        index a constant (`loop` in probe mode) and checking the index map
+        element by element.  Returns the box geometry or None."""
+        on = TMA_TILES if self.prog.tma_tiles is None else self.prog.tma_tiles
+        if not on or not self.launch or self.pf is not None:
+            return self._tma_no(1)
+        dims, elem = split_array(d0)
+        E = self._elements(d0)
+        if not isinstance(elem, Num) or E is None or len(dims) < 2:
+            return self._tma_no(2)
+        eb = 4 if self.scalar == "float" else 8
+        K = f"dpia_probe_{self.fresh('k')}"
+        probe_buf = Buffer(fl.binder, "dpia_probe", "local", d0)
+        saved = (len(self.lines), self.ind, self.smem, self.env.get(fl.binder), self.env.get(binder),
+                 list(self.loops), self.R.get(K))
+        self.env[fl.binder] = probe_buf
+        self.env[binder] = Val(Idx(n), ixv=ix(K))
+        self.R[K] = trip
+        self.probing, self.probe_recs = True, []
+        recs = None
+        try:
+            self.comm(c1)
+            recs = self.probe_recs
+        except (_ProbeFail, CudaError, NeedLanes):
+            recs = None
+        finally:
+            mark, self.ind, self.smem, ob, ok, self.loops, _ = saved
+            del self.lines[mark:]
+            self.probing, self.probe_recs, self.probe_src = False, [], None
+            for nm, ov in ((fl.binder, ob), (binder, ok)):
+                if ov is None:
+                    self.env.pop(nm, None)
+                else:
+                    self.env[nm] = ov
+        if not recs:
+            return self._tma_no(3)
+        xs = {id(r[2]) for r in recs}
+        X = recs[0][2]
+        if len(xs) != 1 or X.space != "in" or X.prefix or X.swz or X.pad or \
+                any(r[0] != fl.binder for r in recs):
+            return self._tma_no(4)
+        xdims, xelem = split_array(X.dtype)
+        NX = self._elements(X.dtype)
+        if not isinstance(xelem, Num) or NX is None:
+            return self._tma_no(5)
+        # source = U + c: U the non-constant (work-group-uniform) part, shared by all copies
+        uni = lambda e: Ix([(m, c) for m, c in e.terms if m != ()])  # noqa: E731
+        U = uni(recs[0][3])
+        emap: Dict[int, int] = {}
+        for _key, dflat, _x, sflat, w in recs:
+            dc, sc = dflat.const, (sflat + (U * -1)).const
+            if dc is None or sc is None or uni(sflat) != U:
+                return self._tma_no(6)
+            for lane in range(w):
+                if dc + lane in emap:
+                    return self._tma_no(7)
+                emap[dc + lane] = sc + lane
+        if sorted(emap) != list(range(E)):
+            return self._tma_no(8)
+        c0 = emap[0]
+        C = next((q for q in range(1, E) if emap[q] != c0 + q), E)
+        if C == E:
+            # one contiguous run: any row split of it is a box (P = C)
+            C = max((q for q in range(1, min(E, 256) + 1)
+                     if E % q == 0 and (q * eb) % 16 == 0 and E // q <= 256), default=0)
+            if not C:
+                return self._tma_no(9)
+            P = C
+        elif E % C:
+            return self._tma_no(9)
+        else:
+            P = emap[C] - c0
+        rows = E // C
+        if P < C or any(emap[q] != c0 + (q // C) * P + q % C for q in range(E)):
+            return self._tma_no(10)
+        if C > 256 or rows > 256 or (C * eb) % 16 or (P * eb) % 16 or NX % P:
+            return self._tma_no(11)
+        # origin(k) = U0 + a*k + c0, linear in k and free of other probe atoms
+        a, U0 = 0, []
+        for m, c in U.terms:
+            if K in IX.free_names(Ix([(m, c)])):
+                if len(m) != 1 or IX._ATOMS[m[0]] != ("v", K):
+                    return self._tma_no(12)
+                a = c
+            else:
+                U0.append((m, c))
+        # the box is issued in `parts` row bands, one per warp (lane 0), so
+        # no single warp carries the issue work into every CTA barrier
+        nthreads = self.launch[1][0] * self.launch[1][1]
+        nw = nthreads // 32 if nthreads % 32 == 0 else 1
+        parts = max(q for q in range(1, min(nw, rows, max(1, TMA_BANDS)) + 1) if rows % q == 0)
+        return {"X": X, "C": C, "rows": rows, "P": P, "U0": Ix(U0) + c0, "a": a, "eb": eb, "E": E,
+                "NX": NX, "trip": trip, "parts": parts, "slots": max(2, TMA_SLOTS)}
+
+    def _tma_origin(self, plan, k: Ix):
+        """(x, y) TMA coordinates of iteration k's box: column and row of
+        its first element in X viewed as NX/P rows of P elements."""
+        o = plan["U0"] + k * plan["a"]
+        return self.r(mod(o, plan["P"], self.R)), self.r(div(o, plan["P"], self.R))
+
+    def _tma_issue(self, plan, buf, mb: str, tm: str, k: Ix, cond: str = "") -> str:
+        """Issue iteration k's box into slice k % 2: row band p of `parts`
+        by lane 0 of warp p."""
+        slot = mod(k, plan["slots"], self.R)
+        x, y = self._tma_origin(plan, k)
+        parts = plan["parts"]
+        band = plan["rows"] // parts
+        cond = f" && {cond}" if cond else ""
+        if parts == 1:
+            return (f"if (dpia_tid == 0{cond}) dpia::tma_tile_2d({buf.cname} + {plan['E']} * "
+                    f"({self.r(slot)}), &{tm}, {x}, {y}, {plan['E'] * plan['eb']}u, {mb} + ({self.r(slot)}));")
+        return (f"if ((dpia_tid & 31) == 0 && (dpia_tid >> 5) < {parts}{cond}) dpia::tma_tile_2d("
+                f"{buf.cname} + {plan['E']} * ({self.r(slot)}) + {band * plan['C']} * (dpia_tid >> 5), "
+                f"&{tm}, {x}, {y} + {band} * (dpia_tid >> 5), {band * plan['C'] * plan['eb']}u, "
+                f"{mb} + ({self.r(slot)}));")
+
     def pipeline_prologue(self, cands, binder: str, n: Nat, trip: int, rotate: bool = False):
         for node, d0, fl, c1, c2 in cands:
+            plan = self._tma_plan(c1, fl, d0, binder, n, trip) if rotate else None
+            if plan is not None:
+                # two slices written by TMA in plain row-major box layout
+                S = plan["slots"]
+                full = Array(nat(S), d0)
+                ct = self.types.c_elem(split_array(d0)[1])
+                cname = self.fresh(fl.binder)
+                buf = Buffer(fl.binder, cname, "local", full)
+                off = self.alloc_smem(S * plan["E"] * plan["eb"], align=128)
+                self.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
+                R = self.R
+                buf.prefix = [lambda b=binder, S=S: mod(self.env[b].ixv, S, R)]
+                self.rotated[fl.binder] = binder
+                mb = self.fresh("tmb")
+                moff = self.alloc_smem(8 * S, align=8)
+                tm = self.prog.add_tmap(plan)
+                if tm not in self.tmaps_used:
+                    self.tmaps_used.append(tm)
+                self.line(f"unsigned long long* {mb} = reinterpret_cast<unsigned long long*>(dpia_smem + {moff});")
+                self.line(f"if (dpia_tid == 0) dpia::tile_bar_init({mb}, {S}, {plan['parts']});")
+                self.line("__syncthreads();")
+                self.line(self._tma_issue(plan, buf, mb, tm, ix(0)))
+                self.pipelined[id(node)] = ("tma", buf, (plan, mb, tm), c1, c2, binder, trip)
+                continue
             if rotate:
                 # two slices, iteration k writes and reads slice k % 2
                 buf = self._declare_local(fl.binder, Array(nat(2), d0))
@@ -1717,8 +2007,9 @@ class KernelEmitter:
 
 class ProgramEmitter:
     def __init__(self, outputs, inputs, float_mode=True, name="KERNEL", sigma=None, launch=None,
-                 init_new=False, peer=False):
+                 init_new=False, peer=False, tma_tiles: Optional[bool] = None):
         self.outputs, self.inputs = list(outputs), list(inputs)
+        self.tma_tiles = tma_tiles
         self.peer = peer
         self.peer_kernel = None
         self.scalar = "float" if float_mode else "long long"
@@ -1740,6 +2031,19 @@ class ProgramEmitter:
         self.in_tail = False
         self.size_names: Set[str] = set()
         self.align: Dict[str, int] = {}      # buffer -> byte alignment its loads need (> 16)
+        self.tmaps: Dict[str, Tuple[str, int, int, int, int, int, int]] = {}
+
+    def add_tmap(self, plan) -> str:
+        """The tensor-map kernel parameter of a TMA-staged tile (deduplicated
+        per input and box): (input, element bytes, rows, cols, pitch, box)."""
+        spec = (plan["X"].cname, plan["eb"], plan["NX"] // plan["P"], plan["P"], plan["P"] * plan["eb"],
+                plan["rows"] // plan["parts"], plan["C"])
+        for nm, sp in self.tmaps.items():
+            if sp == spec:
+                return nm
+        nm = f"dpia_tm{len(self.tmaps)}"
+        self.tmaps[nm] = spec
+        return nm
 
     def is_shared(self, name: str) -> bool:
         return self.spaces.get(name, "private") != "private"
@@ -1864,7 +2168,7 @@ class ProgramEmitter:
         sig = CudaSignature(self.outputs, self.inputs,
                             [(b.cname, b.dtype) for b in self.scratch], size_names, infos,
                             self.scalar, self.launch, self.sigma, dict(self.spaces),
-                            dict(self.align))
+                            dict(self.align), dict(self.tmaps))
         src = ["// generated by the DPIA CUDA backend (paper_1710_08332_b200) for sm_100a",
                header, self.types.struct_text()] + bodies
         return "\n".join(s for s in src if s) + "\n", sig
@@ -1891,6 +2195,7 @@ class ProgramEmitter:
             sizes = sorted(self._size_vars())
             self.size_names |= set(sizes)
             args += [("size", s) for s in sizes]
+        args += [("tmap", t) for t in ke.tmaps_used]
         if grid is not None and tail:
             args.append(("counter", "dpia_counter"))
         if self.peer and ki == self.peer_kernel:
@@ -1903,6 +2208,9 @@ class ProgramEmitter:
                 continue
             if kind == "counter":
                 params.append("unsigned int *dpia_counter")
+                continue
+            if kind == "tmap":
+                params.append(f"const __grid_constant__ dpia::TensorMap {n}")
                 continue
             if kind.startswith("peer_"):
                 params.append({"peer_boxes": "const unsigned long long * __restrict__ dpia_peer_boxes",
@@ -1920,7 +2228,7 @@ class ProgramEmitter:
         L = self.launch
         bounds = f"__launch_bounds__({L[1][0] * L[1][1]}) " if L else ""
         head = [f'extern "C" __global__ void {bounds}{kname}({", ".join(params)}) {{',
-                "  extern __shared__ __align__(16) unsigned char dpia_smem[];"]
+                "  extern __shared__ __align__(128) unsigned char dpia_smem[];"]
         head += views
         if L:
             head.append(f"  const int dpia_nthreads = {L[1][0] * L[1][1]};")
@@ -1964,7 +2272,7 @@ class ProgramEmitter:
         or written by the grid this one is chained behind.  The wait runs
         once per thread (a flag), so sites inside loops cost a predicate
         test; a site right after a #pragma is fenced before the pragma."""
-        names = [n for kind, n in args if kind != "in" and kind != "size"]
+        names = [n for kind, n in args if kind not in ("in", "size", "tmap")]
         names = [n for n in names] + [n + "_raw" for n in names]
         if not names:
             return lines
@@ -2120,7 +2428,8 @@ class ProgramEmitter:
 def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple[str, DataType]],
               float_mode: bool = True, name: str = "KERNEL", init_new: bool = False,
               simplify: bool = True, sigma: Optional[Dict[str, int]] = None,
-              launch=None, peer: bool = False) -> Tuple[str, CudaSignature]:
+              launch=None, peer: bool = False,
+              tma_tiles: Optional[bool] = None) -> Tuple[str, CudaSignature]:
     """Render an imperative DPIA command as CUDA C for sm_100a.
 
     Drop-in for the reference's `emit_kernel(p, outputs, inputs, float_mode,
@@ -2128,6 +2437,8 @@ def emit_cuda(p: Phrase, outputs: List[Tuple[str, DataType]], inputs: List[Tuple
     phrase directly or the reference's hoisted form.  `sigma` and `launch`
     optionally specialise sizes and the (G, L) launch geometry into the
     source (run_kernel always does), which enables single-iteration loops,
-    thread slicing and compile-time index arithmetic."""
+    thread slicing and compile-time index arithmetic.  tma_tiles: stage
+    rotating 2-D box k-tiles with TMA tensor copies (None: TMA_TILES)."""
     del simplify  # subscripts are always range-simplified
-    return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new, peer).emit(p)
+    return ProgramEmitter(outputs, inputs, float_mode, name, sigma, launch, init_new, peer,
+                          tma_tiles).emit(p)

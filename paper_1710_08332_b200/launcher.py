@@ -83,10 +83,18 @@ class Executable:
                     vals.append(RT.C.c_int(self.peer.world))
                 elif kind == "peer_epoch":
                     vals.append(self.peer.epoch)       # shared; bumped by every launch
+                elif kind == "tmap":
+                    vals.append(self._tensor_map(n, self.buffers[self.sig.tmaps[n][0]].ptr))
                 else:
                     vals.append(RT.C.c_uint64(self.counters[k.name].ptr))
             self._args.append(vals)
         return self
+
+    def _tensor_map(self, name: str, base: int):
+        """The TMA descriptor of tensor-map parameter `name` over the input
+        at device address `base` (cuda/emit.py KernelEmitter._tma_plan)."""
+        _x, eb, rows, cols, pitch, box_rows, box_cols = self.sig.tmaps[name]
+        return RT.tensor_map_2d(eb, base, rows, cols, pitch, box_rows, box_cols)
 
     def bind(self, name: str, buf: RT.DeviceBuffer):
         """Use an externally owned device buffer for parameter `name`."""
@@ -141,7 +149,9 @@ class Executable:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
         for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
-            vals = [RT.C.c_uint64(ptrs[n]) if kind in ("out", "in") and n in ptrs else v
+            vals = [RT.C.c_uint64(ptrs[n]) if kind in ("out", "in") and n in ptrs
+                    else self._tensor_map(n, ptrs[self.sig.tmaps[n][0]])
+                    if kind == "tmap" and self.sig.tmaps[n][0] in ptrs else v
                     for (kind, n), v in zip(k.args, vals)]
             grid = g if k.grid == "launch" else (1, 1)
             RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream,
@@ -184,18 +194,19 @@ def _split_params(params):
 
 def build(p: Phrase, params: List[Tuple[str, DataType, str]], launch, sigma=None,
           float_mode: bool = False, device: int = 0, name: str = "KERNEL",
-          specialize: bool = True, peer=None) -> Executable:
+          specialize: bool = True, peer=None, tma_tiles: Optional[bool] = None) -> Executable:
     """Emit + compile + allocate (no data movement).  specialize=False keeps
     sizes as kernel arguments and the geometry runtime-only (the source the
     CLI's `compile` writes without --launch).  peer: a peer.PeerGroup -- the
-    program's result is summed over the group's ranks inside the kernel."""
+    program's result is summed over the group's ranks inside the kernel.
+    tma_tiles: TMA tensor staging of 2-D box k-tiles (cuda/emit.py)."""
     sigma = dict(sigma or {})
     outs, ins = _split_params(params)
     geom = normalize_launch(launch)
     check_work_item_races(p)   # the reference simulator's WorkItemRace (SRC/opencl.py:465-470)
     src, sig = emit_cuda(p, outs, ins, float_mode=float_mode, name=name,
                          sigma=sigma if specialize else None, launch=geom if specialize else None,
-                         peer=peer is not None)
+                         peer=peer is not None, tma_tiles=tma_tiles)
     if peer is not None:
         # dpia::peer_sum writes one mailbox slot per output scalar into every
         # peer: the group's mailboxes must have been sized for exactly that

@@ -175,7 +175,7 @@ class TilePipeline:
         prog = compile_program(text_for_tile(self.tm, self.tn), name=name)
         self.exe = executable(prog, launch_for_tile(self.tm, self.tn), {}, float_mode=float_mode,
                               device=device)
-        if compute_streams > 1 and any(kind not in ("out", "in") for k in self.exe.sig.kernels
+        if compute_streams > 1 and any(kind not in ("out", "in", "tmap") for k in self.exe.sig.kernels
                                        for kind, _ in k.args):
             raise ValueError("tile kernels with scratch buffers or grid counters cannot share "
                              "them across concurrent streams; use compute_streams=1")
