@@ -23,6 +23,8 @@
 //                          register queues of a work-item's sequential fold
 // * dpia::ring_*        -- a single thread's shared-memory ring of TMA bulk
 //                          copies (the top-level sequential fold of a tail)
+// * dpia::stream_*      -- per-round publication of a grid phase's partials
+//                          and the streaming tail's wait for them
 // * dpia::tma_tile_2d   -- one 2-D box of an input (a toLocal k-tile) as a
 //                          TMA tensor copy (cp.async.bulk.tensor.2d through a
 //                          CUtensorMap kernel parameter, mbarrier complete_tx)
@@ -388,6 +390,33 @@ __device__ __forceinline__ void pdl_wait_once(bool& pending) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     pending = false;
   }
+}
+
+// --------------------------------------------- streaming tail
+// A grid phase over n work-items (gsize per round, whole warps) publishes
+// each round on its own counter: every warp, once all its lanes wrote their
+// partial of round r, adds 1 to cnt[r] (release).  The tail -- one thread of
+// an extra block, running from the start -- waits before each ring copy of
+// partials [., hi) until every round below hi has all its warps counted
+// (acquire), then orders the async-proxy copy after those writes.
+__device__ __forceinline__ void stream_publish(unsigned int* c) {
+  __threadfence();
+  atomicAdd(c, 1u);
+}
+__device__ __forceinline__ void stream_wait(const unsigned int* cnt, long long& ready, long long hi,
+                                            long long gsize, long long n) {
+  if (hi > n) hi = n;
+  while (ready < hi) {
+    const long long r = ready / gsize;
+    const long long items = n - r * gsize < gsize ? n - r * gsize : gsize;
+    const unsigned want = static_cast<unsigned>(items / 32);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt + r) : "memory");
+    } while (v < want);
+    ready = (r + 1) * gsize < n ? (r + 1) * gsize : n;
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // --------------------------------------------- 2-D TMA tensor tiles

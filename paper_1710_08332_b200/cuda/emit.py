@@ -91,6 +91,13 @@ PF_MAX_COPIES = 4
 # (profiles/r02c_tma_mm.txt)
 TMA_TILES = os.environ.get("DPIA_TMA_TILES", "0") == "1"
 TMA_PROBE_MAX = 1 << 16            # copy statements the box probe may enumerate
+# streaming tail: a kernel whose grid phase is a mapGlobal writing one partial
+# per work-item and whose tail is one thread's in-order fold of the partials
+# through the TMA bulk ring runs the tail in ONE extra block from the start:
+# work-item rounds publish on per-round counters and the tail folds round r
+# while rounds > r still run (ProgramEmitter._stream_plan); DPIA_STREAM_TAIL=0
+# keeps the last-block ticket tail
+STREAM_TAIL = os.environ.get("DPIA_STREAM_TAIL", "1") != "0"
 # slices of a TMA-staged tile: 2 -- iteration k+1's box is issued right after
 # iteration k's CTA barrier; 3 -- it is issued at the top of iteration k, into
 # the slice iteration k-2 read (free since iteration k-1's barrier)
@@ -194,6 +201,8 @@ class KernelInfo:
     hoisted: frozenset = field(default=frozenset(), repr=False)      # ids: LICM-staged newLocal
     rotated: Dict[str, str] = field(default_factory=dict, repr=False)  # buffer -> its loop binder
     decls: List = field(default_factory=list, repr=False)            # kernel-level buffers
+    extra_blocks: int = 0        # blocks launched beyond the user's grid (a streaming tail block)
+    counter_words: int = 4       # 32-bit words of the kernel's counter buffer
 
 
 @dataclass
@@ -523,6 +532,7 @@ class KernelEmitter:
         self.probe_src: Optional[tuple] = None
         self.barrier_hooks: List[Tuple[int, List[str]]] = []   # (loop depth, lines after the next barrier)
         self.tmaps_used: List[str] = []
+        self.stream_unsafe = False           # a streaming tail read the partials outside the ring
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -755,6 +765,8 @@ class KernelEmitter:
             if aligned:
                 if self.probing:
                     self.probe_src = (ref.buf, ref.at, w)
+                if self.prog.stream is not None and self.prog.in_tail and ref.buf.key in self.prog.stream["partials"]:
+                    self.stream_unsafe = True
                 return f"dpia::vload<{self.scalar}, {w}>({ref.buf.cname}, {self.r(ref.at)})"
             if self.probing:
                 refs = [self.resolve(args[0], [("i", i * w + k)]) for k in range(w)]
@@ -772,7 +784,12 @@ class KernelEmitter:
     def exp(self, p: Phrase, steps: List[Step]) -> str:
         r = self.resolve(p, steps)
         if isinstance(r, Ref):
-            return self._lane_read(r) or r.text
+            lr = self._lane_read(r)
+            st = self.prog.stream
+            if st is not None and self.prog.in_tail and r.buf.key in st["partials"] and \
+                    not (lr and lr.startswith("pfv_") and self.vec_pf is not None and self.vec_pf.get("ring")):
+                self.stream_unsafe = True
+            return lr or r.text
         return r
 
     def _lane_read(self, r: Ref) -> Optional[str]:
@@ -1049,7 +1066,8 @@ class KernelEmitter:
             S = min(TAIL_RING_STAGES, T // C)
         if mode != "plain":
             self._k += 1
-            pf = {"j": j, "depth": len(self.loops), "streams": {}, "written": set(), "tag": self._k}
+            pf = {"j": j, "depth": len(self.loops), "streams": {}, "written": set(), "tag": self._k,
+                  "ring": mode == "ring"}
             self.vec_pf = pf
         else:
             self.vec_pf = None
@@ -1141,9 +1159,18 @@ class KernelEmitter:
             f"{pad1}const {self.scalar}* {name}_s = reinterpret_cast<const {self.scalar}*>"
             f"(dpia_smem + {off}) + {rs} * {C * W};" for (name, _b, _base), off in zip(streams, offs)]
 
+        st = self.prog.stream
+
         def fill(p, slot, at_j):
-            out = [f"{p}{{", f"{p}  const int {j} = {at_j};",
-                   f"{p}  dpia::ring_expect({mb} + {slot}, {piece * len(streams)}u);"]
+            out = [f"{p}{{", f"{p}  const int {j} = {at_j};"]
+            for name, b, base in streams:
+                if st is not None and b.key in st["partials"]:
+                    # streaming tail: the rounds that wrote this piece's
+                    # partials have published (ProgramEmitter._stream_plan)
+                    out.append(f"{p}  dpia::stream_wait(dpia_counter, dpia_ready, "
+                               f"(long long)({self.r(base)}) + {C * W}, {st['gsize']}, {st['n']});")
+                    st["waits"] += 1
+            out.append(f"{p}  dpia::ring_expect({mb} + {slot}, {piece * len(streams)}u);")
             for (name, b, base), off in zip(streams, offs):
                 out.append(f"{p}  dpia::ring_copy(dpia_smem + {off} + {slot} * {piece}, "
                            f"{b.cname} + ({self.r(base)}), {piece}u, {mb} + {slot});")
@@ -1477,6 +1504,11 @@ class KernelEmitter:
             if bind:
                 self.env[bind[0]] = bind[1](ix(v))
             body()
+            if level == "global" and self.prog.stream is not None and not self.prog.in_tail:
+                # streaming tail: this warp's partials of the round are written
+                rnd = "0" if is_single else f"({v} - dpia_gid) / dpia_gsize"
+                self.line("__syncwarp();")
+                self.line(f"if ((dpia_tid & 31) == 0) dpia::stream_publish(dpia_counter + {rnd});")
             for nm, ov in old.items():
                 if ov is None:
                     self.env.pop(nm, None)
@@ -2032,6 +2064,7 @@ class ProgramEmitter:
         self.size_names: Set[str] = set()
         self.align: Dict[str, int] = {}      # buffer -> byte alignment its loads need (> 16)
         self.tmaps: Dict[str, Tuple[str, int, int, int, int, int, int]] = {}
+        self.stream: Optional[dict] = None   # the kernel being emitted has a streaming tail
 
     def add_tmap(self, plan) -> str:
         """The tensor-map kernel parameter of a TMA-staged tile (deduplicated
@@ -2173,19 +2206,66 @@ class ProgramEmitter:
                header, self.types.struct_text()] + bodies
         return "\n".join(s for s in src if s) + "\n", sig
 
+    def _stream_plan(self, grid, tail) -> Optional[dict]:
+        """Can this kernel's tail stream?  Its grid phase must be one
+        parforGlobal over n work-items (n a multiple of 32, a 1-D launch of
+        whole warps, so every warp's loop trip is uniform) that writes
+        one-scalar-per-item scratch partials, and its tail single-thread
+        items only.  Whether the tail then reads the partials only through the
+        ring is checked after emission (emit_kernel retries without)."""
+        if not STREAM_TAIL or grid is None or not tail or any(self.is_cooperative(t) for t in tail) \
+                or self.peer or not self.launch or self.sigma is None:
+            return None
+        (gx, gy), (lx, ly) = self.launch
+        u = unapply(grid)
+        if gy != 1 or (lx * ly) % 32 or u is None or u[0] != "parforGlobal":
+            return None
+        try:
+            n = int(u[1][0].evaluate(self.sigma))
+        except Exception:  # noqa: BLE001
+            n = None
+        if not isinstance(n, int) or n <= 0 or n % 32:
+            return None
+        _, W = rw_sets(grid)
+        parts = set()
+        for b in self.scratch:
+            if b.key in W:
+                dims, elem = split_array(b.dtype)
+                try:
+                    count = 1
+                    for x in dims:
+                        count *= int(x.evaluate(self.sigma))
+                except Exception:  # noqa: BLE001
+                    return None
+                if not isinstance(elem, Num) or count != n:
+                    return None
+                parts.add(b.key)
+        if not parts:
+            return None
+        gsize = gx * lx * ly
+        return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0}
+
     def emit_kernel(self, ki, grid, tail, decls):
         kname = f"{self.name}_k{ki}"
-        ke = KernelEmitter(self, kname)
         body_lines = None
-        for attempt in ("record", "final"):
-            ke.reset()
-            ke.recording = attempt == "record"
-            self._kernel_body(ke, grid, tail, decls)
-            if attempt == "record":
-                ke.slices, ke.promote = self._decide_slices(ke)
-                for key in ke.promote:
-                    self.spaces[key] = "local"
-            body_lines = ke.lines
+        plan = self._stream_plan(grid, tail)
+        for stream in ([plan, None] if plan else [None]):
+            self.stream = stream
+            ke = KernelEmitter(self, kname)
+            for attempt in ("record", "final"):
+                ke.reset()
+                if stream is not None:
+                    stream["waits"] = 0
+                ke.recording = attempt == "record"
+                self._kernel_body(ke, grid, tail, decls)
+                if attempt == "record":
+                    ke.slices, ke.promote = self._decide_slices(ke)
+                    for key in ke.promote:
+                        self.spaces[key] = "local"
+                body_lines = ke.lines
+            if stream is None or (stream["waits"] and not ke.stream_unsafe):
+                break
+        stream, self.stream = self.stream, None
         args: List[Tuple[str, str]] = [("out", n) for n, _ in self.outputs]
         args += [("in", n) for n, _ in self.inputs]
         args += [("scratch", b.cname) for b in self.scratch if b.cname in ke.used_scratch
@@ -2250,17 +2330,22 @@ class ProgramEmitter:
             head.append("  dpia::pdl_trigger();")
             head.append("  bool dpia_chained = true;")
             body_lines = self._chain_waits(body_lines, args)
-        if ke.uses_gid:
+        if ke.uses_gid or stream is not None:
             wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
             it = "long long" if wide else "int"
-            head.append(f"  const {it} dpia_gid = ({it})(blockIdx.y * gridDim.x + blockIdx.x) * "
+            # a streaming tail's extra block is the last block of the grid
+            # and takes no work-items
+            gx = "(gridDim.x - 1)" if stream is not None else "gridDim.x"
+            head.append(f"  const {it} dpia_gid = ({it})(blockIdx.y * {gx} + blockIdx.x) * "
                         "dpia_nthreads + dpia_tid;")
-            head.append(f"  const {it} dpia_gsize = ({it})gridDim.x * gridDim.y * dpia_nthreads;")
+            head.append(f"  const {it} dpia_gsize = ({it}){gx} * gridDim.y * dpia_nthreads;")
         text = "\n".join(head + body_lines + ["}"])
         info = KernelInfo(kname, "launch" if grid is not None else "single", args, ke.smem,
                           grid is not None and bool(tail), grid_item=grid, tail_items=list(tail),
                           barriers=frozenset(ke.barriers), hoisted=frozenset(ke.hoisted),
-                          rotated=dict(ke.rotated), decls=list(decls))
+                          rotated=dict(ke.rotated), decls=list(decls),
+                          extra_blocks=1 if stream is not None else 0,
+                          counter_words=max(4, stream["R"]) if stream is not None else 4)
         return text, info
 
     @staticmethod
@@ -2327,14 +2412,24 @@ class ProgramEmitter:
                 ke.line(f"{ct}* {cname} = reinterpret_cast<{ct}*>(dpia_smem + {off});")
                 saved_env[binder] = Buffer(binder, cname, "local", d)
         ke.env.update(saved_env)
+        st = self.stream
         if grid is not None:
             self.in_tail = False
             if not self.is_grid_item(grid):
                 raise CudaError("internal: grid item expected")
+            if st is not None:
+                ke.open("if (blockIdx.x != gridDim.x - 1)")
             ke.comm(grid)
+            if st is not None:
+                ke.close()
         if tail:
             self.in_tail = True
-            if grid is not None:
+            if grid is not None and st is not None:
+                # the streaming tail block: partials [0, dpia_ready) are known
+                # to be published (dpia::stream_wait)
+                ke.open("else")
+                ke.line("long long dpia_ready = 0;")
+            elif grid is not None:
                 ke.line("__shared__ bool dpia_last;")
                 ke.open("if (dpia::grid_arrive(dpia_counter, dpia_tid, &dpia_last))")
             for space, binder, d in decls:
@@ -2369,7 +2464,13 @@ class ProgramEmitter:
                 ke.line(f"if (dpia_tid < 32) dpia::peer_sum<{self.scalar}>("
                         f"reinterpret_cast<{self.scalar}*>({on}), {nsc}, dpia_peer_boxes, dpia_rank, "
                         "dpia_world, dpia_epoch, dpia_tid, dpia_nthreads);")
-            if grid is not None:
+            if grid is not None and st is not None:
+                # every round has been published and consumed: reset the
+                # counters for the next launch
+                ke.line(f"if (dpia_tid == 0) for (int dpia_r = 0; dpia_r < {st['R']}; ++dpia_r) "
+                        "dpia_counter[dpia_r] = 0u;")
+                ke.close()
+            elif grid is not None:
                 ke.line("dpia::grid_reset(dpia_counter, dpia_tid);")
                 ke.close()
             self.in_tail = False

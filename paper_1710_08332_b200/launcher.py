@@ -64,7 +64,7 @@ class Executable:
                 self.buffers[n] = b
         for k in self.sig.kernels:
             if k.fused_tail and k.name not in self.counters:
-                c = RT.DeviceBuffer(16, self.device)
+                c = RT.DeviceBuffer(4 * k.counter_words, self.device)
                 c.zero()
                 self.counters[k.name] = c
         self._args = []
@@ -126,7 +126,7 @@ class Executable:
             self.peer.next_epoch()
         (g, l) = self.sig.launch or self.geometry
         for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
-            grid = g if k.grid == "launch" else (1, 1)
+            grid = (g[0] + k.extra_blocks, g[1]) if k.grid == "launch" else (1, 1)
             fn = self.module.function(k.name)
             # later phases: programmatic dependent launch (their first
             # statement is griddepcontrol.wait), which hides their launch
@@ -153,7 +153,7 @@ class Executable:
                     else self._tensor_map(n, ptrs[self.sig.tmaps[n][0]])
                     if kind == "tmap" and self.sig.tmaps[n][0] in ptrs else v
                     for (kind, n), v in zip(k.args, vals)]
-            grid = g if k.grid == "launch" else (1, 1)
+            grid = (g[0] + k.extra_blocks, g[1]) if k.grid == "launch" else (1, 1)
             RT.launch(self.module.function(k.name), self.device, grid, l, k.smem, vals, stream,
                       pdl=i > 0 or chain)
 

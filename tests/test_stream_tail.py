@@ -1,0 +1,131 @@
+"""Streaming tail (cuda/emit.py ProgramEmitter._stream_plan).
+
+A kernel whose grid phase is a mapGlobal writing one partial per work-item
+and whose tail is one thread's in-order fold of those partials (config 1's
+literal program: reduce (+) 0 (mapGlobal ... (split 1024 (zip xs ys)))) runs
+the tail in one extra block from the start: each warp publishes each round
+of work-items on that round's counter, and the tail waits for a round before
+its TMA ring copies that round's partials.  The fold order is unchanged, so
+results are bit-identical to the last-block ticket tail.
+
+CPU: when the streaming form is chosen and when it falls back.  GPU: int mode
+exact, fp32 bit-identical to the ticket tail over 1..8 rounds, chained
+launches.
+"""
+import numpy as np
+import pytest
+
+from paper_1710_08332_b200 import compile_program
+from paper_1710_08332_b200.bench_programs import dot_literal_program
+from paper_1710_08332_b200.cuda import emit as EM
+
+
+def _emit(chunk, n, launch, float_mode=True):
+    prog = compile_program(dot_literal_program(chunk))
+    outs = [("out", prog.out_type)]
+    ins = [(nm, t.data) for nm, t in prog.source.params]
+    return EM.emit_cuda(prog.imperative, outs, ins, float_mode=float_mode, sigma={"n": n}, launch=launch)
+
+
+def test_literal_dot_streams_its_tail():
+    src, sig = _emit(1024, 16384, (128, 32))
+    k = sig.kernels[0]
+    assert k.extra_blocks == 1 and k.counter_words == 4 and k.fused_tail
+    assert "dpia::stream_wait(dpia_counter, dpia_ready" in src
+    assert "dpia::stream_publish(dpia_counter + (i_" in src      # 4 rounds: a round index
+    assert "dpia::grid_arrive(dpia_counter" not in src
+    assert "(gridDim.x - 1)" in src
+    src, sig = _emit(1024, 16384, (16, 32))                      # 32 rounds
+    assert sig.kernels[0].counter_words == 32
+
+
+def test_stream_tail_falls_back(monkeypatch):
+    # n not a multiple of 32: warps would straddle the end of a round
+    src, sig = _emit(1024, 16384 + 16, (129, 32))
+    assert sig.kernels[0].extra_blocks == 0 and "dpia::grid_arrive(dpia_counter" in src
+    # a short tail (32 partials) is folded by plain loads, not the ring:
+    # it could read partials before they are published
+    src, sig = _emit(1024, 32, (1, 32))
+    assert sig.kernels[0].extra_blocks == 0 and "dpia::grid_arrive(dpia_counter" in src
+    monkeypatch.setattr(EM, "STREAM_TAIL", False)
+    src, sig = _emit(1024, 16384, (128, 32))
+    assert sig.kernels[0].extra_blocks == 0 and "dpia::grid_arrive(dpia_counter" in src
+
+
+# ------------------------------------------------------------------ GPU
+
+def _run(chunk, n, launch, inputs, float_mode, stream=True):
+    from paper_1710_08332_b200 import executable
+    from paper_1710_08332_b200 import runtime as RT
+    old = EM.STREAM_TAIL
+    EM.STREAM_TAIL = stream
+    try:
+        exe = executable(compile_program(dot_literal_program(chunk)), launch, {"n": n}, float_mode=float_mode)
+    finally:
+        EM.STREAM_TAIL = old
+    st = RT.Stream(0)
+    for nm, v in inputs.items():
+        exe.upload(nm, v, st)
+    outs = []
+    for _ in range(3):                    # repeated launches reuse the reset counters
+        exe.launch(st)
+        outs.append(np.asarray(exe.download("out", st)).copy())
+    st.sync()
+    assert all(np.array_equal(o.view(np.uint8), outs[0].view(np.uint8)) for o in outs)
+    return outs[0], exe
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk,n,G,L", [(1024, 1024, 32, 32), (1024, 1024, 16, 32), (256, 4096, 32, 32),
+                                         (256, 4096, 16, 64), (64, 8192, 32, 32), (128, 3072, 32, 32),
+                                         (1024, 16384, 128, 32)])
+def test_stream_tail_int_exact(chunk, n, G, L):
+    rng = np.random.default_rng(n + G)
+    xs = rng.integers(-9, 10, n * chunk)
+    ys = rng.integers(-9, 10, n * chunk)
+    got, exe = _run(chunk, n, (G, L), {"xs": xs, "ys": ys}, False)
+    assert exe.sig.kernels[0].extra_blocks == 1
+    assert int(got[0]) == int(np.dot(xs, ys))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("chunk,n,G,L", [(1024, 16384, 512, 32), (1024, 16384, 256, 32), (1024, 16384, 128, 32),
+                                         (1024, 16384, 64, 32), (512, 8192, 96, 32)])
+def test_stream_tail_bit_identical_fp32(chunk, n, G, L):
+    rng = np.random.default_rng(G)
+    inputs = {"xs": rng.uniform(0, 1, n * chunk).astype(np.float32),
+              "ys": rng.uniform(0, 1, n * chunk).astype(np.float32)}
+    a, exe = _run(chunk, n, (G, L), inputs, True, stream=True)
+    b, ref = _run(chunk, n, (G, L), inputs, True, stream=False)
+    assert exe.sig.kernels[0].extra_blocks == 1 and ref.sig.kernels[0].extra_blocks == 0
+    assert a.view(np.uint32)[0] == b.view(np.uint32)[0]
+
+
+@pytest.mark.gpu
+def test_stream_tail_chained_steps():
+    """Steps chained behind each other (programmatic dependent launch), each
+    on its own inputs and output: every step's bits equal an unchained run."""
+    from paper_1710_08332_b200 import executable
+    from paper_1710_08332_b200 import runtime as RT
+    chunk, n, launch = 256, 4096, (32, 32)          # 4 rounds
+    exe = executable(compile_program(dot_literal_program(chunk)), launch, {"n": n}, float_mode=True)
+    assert exe.sig.kernels[0].extra_blocks == 1
+    st = RT.Stream(0)
+    rng = np.random.default_rng(3)
+    steps = []
+    for _ in range(6):
+        xs = rng.uniform(0, 1, n * chunk).astype(np.float32)
+        ys = rng.uniform(0, 1, n * chunk).astype(np.float32)
+        bx, by, bo = RT.DeviceBuffer(xs.nbytes), RT.DeviceBuffer(ys.nbytes), RT.DeviceBuffer(4)
+        bx.upload(xs, st)
+        by.upload(ys, st)
+        steps.append((xs, ys, bx, by, bo))
+    st.sync()
+    for i, (_, _, bx, by, bo) in enumerate(steps):
+        exe.launch_with(st, {"xs": bx.ptr, "ys": by.ptr, "out": bo.ptr}, chain=i > 0)
+    st.sync()
+    for xs, ys, _, _, bo in steps:
+        got = np.empty(1, np.float32)
+        bo.download(got.view(np.uint8), st)
+        want, _ = _run(chunk, n, launch, {"xs": xs, "ys": ys}, True, stream=False)
+        assert got.view(np.uint32)[0] == want.view(np.uint32)[0]
