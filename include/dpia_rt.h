@@ -69,12 +69,13 @@ int dpia_memcpy2d_dtoh(int device, void* dst, size_t dpitch, uint64_t src, size_
                        size_t width, size_t height, void* stream);
 /* TMA descriptor (CUtensorMap, 128 bytes at out) of a row-major matrix of
  * elem_bytes (4: fp32, 8: int64) elements, rows x cols with a row pitch in
- * bytes, read in boxes of box_rows x box_cols, no swizzle: the kernel
- * parameter of an emitted toLocal k-tile staged by cp.async.bulk.tensor.2d
- * (no reference counterpart: the reference has no device code, SURVEY.md
- * 8b).  _f32: the fp32 form (tools/mmtma.py). */
+ * bytes, read in boxes of box_rows x box_cols; swizzle 0 (plain) or 128
+ * (128-byte rows, 16-byte chunks XOR row % 8): the kernel parameter of an
+ * emitted toLocal k-tile or work-item row fold staged by
+ * cp.async.bulk.tensor.2d (no reference counterpart: the reference has no
+ * device code).  _f32: the plain fp32 form (tools/mmtma.py). */
 int dpia_tensor_map_2d(void* out, int elem_bytes, uint64_t base, uint64_t rows, uint64_t cols,
-                       uint64_t pitch, unsigned box_rows, unsigned box_cols);
+                       uint64_t pitch, unsigned box_rows, unsigned box_cols, int swizzle);
 int dpia_tensor_map_2d_f32(void* out, uint64_t base, uint64_t rows, uint64_t cols, uint64_t pitch,
                            unsigned box_rows, unsigned box_cols);
 int dpia_memset(int device, uint64_t dst, int value, size_t bytes, void* stream);

@@ -422,12 +422,15 @@ def dot_literal_program(chunk: int = 1024) -> str:
 """
 
 
-def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 32) -> Config:
-    """One work-item per chunk: N / chunk work-items in groups of L (one
-    warp per group spreads the 16384 work-items over every SM;
-    profiles/r02_litgeo.txt)."""
+def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 32, rounds: int = 4) -> Config:
+    """N / chunk work-items in groups of L (one warp per group), walking the
+    chunks grid-stride in `rounds` rounds: each work-item's chunk arrives by
+    2-D TMA row boxes, and the top-level fold streams -- one extra block folds
+    round r's partials while rounds > r still run (cuda/emit.py
+    _finish_rows, _stream_plan; profiles/r02c_litstream.txt)."""
     n = N // chunk
-    return Config("dot_literal", dot_literal_program(chunk), {"n": n}, (n // L, L),
+    G = max(1, n // (L * rounds)) if n % (L * rounds) == 0 else max(1, n // L)
+    return Config("dot_literal", dot_literal_program(chunk), {"n": n}, (G, L),
                   bytes=8 * N, flops=2 * N)
 
 

@@ -490,17 +490,21 @@ int dpia_launch_pdl(void* function, int device, unsigned gx, unsigned gy, unsign
 
 // TMA descriptor of a row-major matrix of 4-byte (fp32) or 8-byte (int64)
 // elements (rows x cols, row pitch in bytes) read in boxes of box_rows x
-// box_cols, no swizzle, into the 128-byte CUtensorMap at `out` (passed to
-// kernels by value): the toLocal k-tiles the emitter lowers to
-// cp.async.bulk.tensor.2d (cuda/emit.py KernelEmitter._tma_plan).
+// box_cols into the 128-byte CUtensorMap at `out` (passed to kernels by
+// value); swizzle 0 (plain box layout) or 128 (16-byte chunks of each
+// 128-byte row XOR-permuted by the row index mod 8).  The toLocal k-tiles
+// (cuda/emit.py KernelEmitter._tma_plan) and the work-item row folds
+// (KernelEmitter._finish_rows) the emitter lowers to cp.async.bulk.tensor.2d.
 int dpia_tensor_map_2d(void* out, int elem_bytes, uint64_t base, uint64_t rows, uint64_t cols,
-                       uint64_t pitch, unsigned box_rows, unsigned box_cols) {
+                       uint64_t pitch, unsigned box_rows, unsigned box_cols, int swizzle) {
   if (int e = load_driver()) return e;
   if (!drv::cuTensorMapEncodeTiled) return fail(-1, "CUDA driver lacks cuTensorMapEncodeTiled");
   if (elem_bytes != 4 && elem_bytes != 8) return fail(-1, "tensor map: element size must be 4 or 8");
   if (base % 16 || pitch % 16 || (box_cols * elem_bytes) % 16 || box_cols > 256 || box_rows > 256 ||
       box_cols == 0 || box_rows == 0)
     return fail(-1, "tensor map: base/pitch/box violate the TMA alignment or size rules");
+  if (swizzle != 0 && !(swizzle == 128 && box_cols * elem_bytes <= 128))
+    return fail(-1, "tensor map: swizzle must be 0, or 128 with rows of at most 128 bytes");
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch};
   cuuint32_t box[2] = {box_cols, box_rows};
@@ -509,13 +513,14 @@ int dpia_tensor_map_2d(void* out, int elem_bytes, uint64_t base, uint64_t rows, 
       static_cast<CUtensorMap*>(out),
       elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2,
       reinterpret_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
+      swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE));
   return 0;
 }
 
 int dpia_tensor_map_2d_f32(void* out, uint64_t base, uint64_t rows, uint64_t cols, uint64_t pitch,
                            unsigned box_rows, unsigned box_cols) {
-  return dpia_tensor_map_2d(out, 4, base, rows, cols, pitch, box_rows, box_cols);
+  return dpia_tensor_map_2d(out, 4, base, rows, cols, pitch, box_rows, box_cols, 0);
 }
 
 int dpia_stream_create(int device, void** stream) {

@@ -98,6 +98,15 @@ TMA_PROBE_MAX = 1 << 16            # copy statements the box probe may enumerate
 # while rounds > r still run (ProgramEmitter._stream_plan); DPIA_STREAM_TAIL=0
 # keeps the last-block ticket tail
 STREAM_TAIL = os.environ.get("DPIA_STREAM_TAIL", "1") != "0"
+# work-item row folds: a long sequential fold of each work-item of a
+# mapGlobal over its own contiguous chunk of an input (config 1's literal
+# reduceSeq) reads the chunks of a warp's 32 consecutive work-items as 2-D TMA
+# boxes (32 rows x 128 bytes, 128-byte swizzle) through a per-warp ring of
+# ROW_TMA_STAGES shared-memory slots, each lane folding its own row:
+# KernelEmitter._finish_rows; DPIA_ROW_TMA=0 keeps the register queues
+ROW_TMA = os.environ.get("DPIA_ROW_TMA", "1") != "0"
+ROW_TMA_STAGES = int(os.environ.get("DPIA_ROW_TMA_STAGES", "4"))
+ROW_TMA_BOXES = int(os.environ.get("DPIA_ROW_TMA_BOXES", "2"))    # 128-byte box columns per step
 # slices of a TMA-staged tile: 2 -- iteration k+1's box is issued right after
 # iteration k's CTA barrier; 3 -- it is issued at the top of iteration k, into
 # the slice iteration k-2 read (free since iteration k-1's barrier)
@@ -217,8 +226,9 @@ class CudaSignature:
     sigma: Optional[Dict[str, int]]
     spaces: Dict[str, str] = field(default_factory=dict, repr=False)   # buffer binder -> space
     align: Dict[str, int] = field(default_factory=dict, repr=False)    # buffer -> bytes (> 16) its loads need
-    # tensor-map parameter -> (input, element bytes, rows, cols, row pitch bytes, box rows, box cols)
-    tmaps: Dict[str, Tuple[str, int, int, int, int, int, int]] = field(default_factory=dict, repr=False)
+    # tensor-map parameter -> (input, element bytes, rows, cols, row pitch bytes, box rows, box cols,
+    # swizzle bytes)
+    tmaps: Dict[str, Tuple[str, int, int, int, int, int, int, int]] = field(default_factory=dict, repr=False)
 
     def params(self) -> List[str]:
         out = [f"{self.scalar} *{n}" for n, _ in self.outputs]
@@ -533,6 +543,7 @@ class KernelEmitter:
         self.barrier_hooks: List[Tuple[int, List[str]]] = []   # (loop depth, lines after the next barrier)
         self.tmaps_used: List[str] = []
         self.stream_unsafe = False           # a streaming tail read the partials outside the ring
+        self.smem_1k = False                 # dynamic shared memory must start 1024-byte aligned
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -1005,6 +1016,8 @@ class KernelEmitter:
         modes = []
         if TAIL_RING and self.single_thread and not self.loops and TAIL_RING_STAGES > 0:
             modes.append(("ring", VEC_WIDTH))
+        if ROW_TMA and self._rows_loop() is not None and VEC_WIDTH * sb == 16:
+            modes.append(("rows", VEC_WIDTH))
         if VEC_PREFETCH > 1:
             if VEC_LOAD_BYTES == 32:
                 modes.append(("queue32", 32 // sb))
@@ -1064,6 +1077,18 @@ class KernelEmitter:
             if not C:
                 return False
             S = min(TAIL_RING_STAGES, T // C)
+        elif mode == "rows":
+            # vectors per step: ROW_TMA_BOXES box columns of 128 bytes
+            C = 128 // (W * sb) * max(1, ROW_TMA_BOXES)
+            while C > 128 // (W * sb) and T % C:
+                C //= 2
+            if T % C:
+                return False
+            S = max(2, ROW_TMA_STAGES)
+            # fit the warps' slots (two streams assumed) in shared memory
+            nw = self.launch[1][0] * self.launch[1][1] // 32
+            while S > 2 and nw * S * 2 * C * W * sb * 32 > 200 * 1024:
+                S -= 1
         if mode != "plain":
             self._k += 1
             pf = {"j": j, "depth": len(self.loops), "streams": {}, "written": set(), "tag": self._k,
@@ -1076,6 +1101,18 @@ class KernelEmitter:
             self.open(f"for (int {jo} = 0; {jo} < {T}; {jo} += {D})")
             self.line("#pragma unroll")
             self.open(f"for (int {jd} = 0; {jd} < {D}; {jd} += 1)")
+            self.line(f"const int {j} = {jo} + {jd};")
+            take = len(self.lines)
+        elif mode == "rows":
+            jo, jd, ru, rs, mb = (self.fresh(x) for x in ("jo", "jd", "ru", "rs", "wmb"))
+            u0 = self.fresh("wu0")
+            self.open(f"for (int {jo} = 0; {jo} < {T}; {jo} += {C})")
+            self.line(f"const int {ru} = {u0} + {jo} / {C};")
+            self.line(f"const int {rs} = {ru} % {S};")
+            self.line(f"dpia::ring_wait({mb} + {rs}, (unsigned)(({ru} / {S}) & 1));")
+            slot_at = len(self.lines)
+            self.line("#pragma unroll")
+            self.open(f"for (int {jd} = 0; {jd} < {C}; {jd} += 1)")
             self.line(f"const int {j} = {jo} + {jd};")
             take = len(self.lines)
         elif mode == "ring":
@@ -1115,6 +1152,8 @@ class KernelEmitter:
             return False
         if mode == "ring":
             return self._finish_ring(streams, top, slot_at, take, T, W, C, S, j, jo, jd, rs, mb)
+        if mode == "rows":
+            return self._finish_rows(streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0)
         self.close()
         pad = "  " * self.ind
         pad_in = pad + "    "
@@ -1130,6 +1169,113 @@ class KernelEmitter:
         for name, b, base in streams:
             pro.append(f"{pad}  {name.replace('pfv_', 'pfq_')}[{j}] = {self._vload(mode, b, W, base)};")
         pro.append(f"{pad}}}")
+        self.lines[top:top] = pro
+        return True
+
+    def _rows_loop(self) -> Optional[Loop]:
+        """The enclosing mapGlobal loop when a fold here can use row boxes:
+        the fold is a work-item's (directly inside the global loop), the
+        launch is whole warps and the work-item count a multiple of 32, so
+        each warp's 32 consecutive work-items take every round together."""
+        if not self.per_thread or self.single_thread or len(self.loops) != 1 or not self.launch:
+            return None
+        lp = self.loops[0]
+        (gx, gy), (lx, ly) = self.launch
+        if lp.level != "global" or lp.trip is None or lp.trip % 32 or (lx * ly) % 32:
+            return None
+        return lp
+
+    def _finish_rows(self, streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0) -> bool:
+        """Complete a rows-mode fold (see `_vec_loop`).  Stream s reads
+        X_s[coef * i + c_s + W * j'] for work-item i: X_s viewed as rows of
+        coef elements, the warp's work-items are 32 consecutive rows, and
+        step t of the fold covers columns [c_s + t*C*W, +C*W) as C*W/32
+        boxes of 32 rows x 128 bytes.  Lane 0 keeps S steps in flight
+        through the warp's slots (one mbarrier per slot), running ahead into
+        the warp's next round of work-items; every lane reads its own row of
+        each box (128-byte swizzle: 16-byte chunk q of row r sits at chunk
+        q ^ (r % 8), the slots being 1024-byte aligned)."""
+        lp = self._rows_loop()
+        sb = 4 if self.scalar == "float" else 8
+        VB = 128 // (W * sb)                        # vectors per box row
+        if lp is None or W * sb != 16 or C % VB:
+            return False
+        NB = C // VB                                # boxes per stream per step
+        iv, n = lp.var, lp.trip
+        (gx, gy), (lx, ly) = self.launch
+        nthreads, steps = lx * ly, T // C
+        specs = []
+        for name, b, base in streams:
+            coef = {m: c for m, c in base.terms}
+            if b.space != "in" or b.prefix or not isinstance(b.elem, Num) or \
+                    set(coef) - {(j,), (iv,), ()} or coef.get((j,)) != W or (iv,) not in coef:
+                return False
+            P, c0 = coef[(iv,)], coef.get((), 0)
+            NX = self._elements(b.dtype)
+            if NX is None or P <= 0 or NX % P or (P * sb) % 16 or c0 < 0 or c0 + T * W > P \
+                    or NX // P < n or NX // P > IX.INT32_MAX:
+                return False
+            tm = self.prog.add_tmap({"X": b, "eb": sb, "NX": NX, "P": P, "rows": 32, "parts": 1,
+                                     "C": VB * W, "swizzle": 128})
+            if tm not in self.tmaps_used:
+                self.tmaps_used.append(tm)
+            specs.append((name, tm, c0))
+        NS = len(specs)
+        slot_bytes = NS * NB * 4096
+        nw = nthreads // 32
+        if nw * S * slot_bytes > 200 * 1024:
+            return False
+        soff = self.alloc_smem(nw * S * slot_bytes, align=1024)
+        self.smem_1k = True
+        moff = self.alloc_smem(nw * S * 8, align=8)
+        lane, sw, st, row0, rnd = (self.fresh(x) for x in ("wlane", "wsw", "wst", "wrow0", "wround"))
+        jd = f"({j} % {C})"
+        pad1 = "  " * self.ind                      # the step loop's body
+        pad2 = pad1 + "  "                          # the lane loop's body
+        vt = f"dpia::vec<{self.scalar}, {W}>"
+        box_elems = 4096 // sb
+        self.lines[take:take] = [
+            f"{pad2}const {vt} {name} = dpia::vload<{self.scalar}, {W}>({name}_s + {jd} / {VB} * {box_elems}, "
+            f"{W} * ({jd} % {VB} ^ {sw}));" for name, _tm, _c0 in specs]
+        self.lines[slot_at:slot_at] = [
+            f"{pad1}const {self.scalar}* {name}_s = reinterpret_cast<const {self.scalar}*>"
+            f"({st} + {rs} * {slot_bytes} + {k * NB * 4096} + {lane} * 128);"
+            for k, (name, _tm, _c0) in enumerate(specs)]
+
+        def issue(p, u):
+            """lane 0: fill step u's slot (step u % steps of round u / steps)
+            if that round has work-items for this warp"""
+            out = [f"{p}{{", f"{p}  const long long wr_ = {row0} + (long long)(({u}) / {steps}) * dpia_gsize;",
+                   f"{p}  if (wr_ < {n}) {{",
+                   f"{p}    unsigned char* wd_ = {st} + (({u}) % {S}) * {slot_bytes};",
+                   f"{p}    const int wc_ = (({u}) % {steps}) * {C * W};"]
+            for k, (_name, tm, c0) in enumerate(specs):
+                for bb in range(NB):
+                    out.append(f"{p}    dpia::tma_tile_2d(wd_ + {(k * NB + bb) * 4096}, &{tm}, "
+                               f"{c0 + bb * VB * W} + wc_, (int)wr_, 4096u, {mb} + (({u}) % {S}));")
+            out += [f"{p}  }}", f"{p}}}"]
+            return out
+
+        self.line("__syncwarp();")
+        self.line(f"if ({lane} == 0)")
+        self.lines += issue(pad1, f"{ru} + {S}")
+        self.close()
+        pad = "  " * self.ind
+        rexpr = "0" if lp.single else f"(int)(({iv} - dpia_gid) / dpia_gsize)"
+        warp = "(dpia_tid >> 5)"
+        pro = [f"{pad}const int {lane} = dpia_tid & 31, {sw} = {lane} & 7;",
+               f"{pad}unsigned long long* {mb} = reinterpret_cast<unsigned long long*>(dpia_smem + {moff})"
+               f" + {warp} * {S};",
+               f"{pad}unsigned char* {st} = dpia_smem + {soff} + {warp} * {S * slot_bytes};",
+               f"{pad}const int {rnd} = {rexpr};",
+               f"{pad}const int {u0} = {rnd} * {steps};",
+               f"{pad}const long long {row0} = (long long)dpia_gid - {lane};",
+               f"{pad}if ({rnd} == 0) {{",
+               f"{pad}  if ({lane} == 0) {{",
+               f"{pad}    dpia::tile_bar_init({mb}, {S}, {NS * NB});",
+               f"{pad}    for (int wq_ = 0; wq_ < {S}; ++wq_)"]
+        pro += issue(pad + "    ", "wq_")
+        pro += [f"{pad}  }}", f"{pad}  __syncwarp();", f"{pad}}}"]
         self.lines[top:top] = pro
         return True
 
@@ -2063,14 +2209,14 @@ class ProgramEmitter:
         self.in_tail = False
         self.size_names: Set[str] = set()
         self.align: Dict[str, int] = {}      # buffer -> byte alignment its loads need (> 16)
-        self.tmaps: Dict[str, Tuple[str, int, int, int, int, int, int]] = {}
+        self.tmaps: Dict[str, Tuple[str, int, int, int, int, int, int, int]] = {}
         self.stream: Optional[dict] = None   # the kernel being emitted has a streaming tail
 
     def add_tmap(self, plan) -> str:
         """The tensor-map kernel parameter of a TMA-staged tile (deduplicated
         per input and box): (input, element bytes, rows, cols, pitch, box)."""
         spec = (plan["X"].cname, plan["eb"], plan["NX"] // plan["P"], plan["P"], plan["P"] * plan["eb"],
-                plan["rows"] // plan["parts"], plan["C"])
+                plan["rows"] // plan["parts"], plan["C"], plan.get("swizzle", 0))
         for nm, sp in self.tmaps.items():
             if sp == spec:
                 return nm
@@ -2308,7 +2454,9 @@ class ProgramEmitter:
         L = self.launch
         bounds = f"__launch_bounds__({L[1][0] * L[1][1]}) " if L else ""
         head = [f'extern "C" __global__ void {bounds}{kname}({", ".join(params)}) {{',
-                "  extern __shared__ __align__(128) unsigned char dpia_smem[];"]
+                # 1024: a 128-byte-swizzled TMA box's slots (row folds) must
+                # sit on 1024-byte boundaries, also behind static shared data
+                f"  extern __shared__ __align__({1024 if ke.smem_1k else 128}) unsigned char dpia_smem[];"]
         head += views
         if L:
             head.append(f"  const int dpia_nthreads = {L[1][0] * L[1][1]};")

@@ -93,8 +93,8 @@ class Executable:
     def _tensor_map(self, name: str, base: int):
         """The TMA descriptor of tensor-map parameter `name` over the input
         at device address `base` (cuda/emit.py KernelEmitter._tma_plan)."""
-        _x, eb, rows, cols, pitch, box_rows, box_cols = self.sig.tmaps[name]
-        return RT.tensor_map_2d(eb, base, rows, cols, pitch, box_rows, box_cols)
+        _x, eb, rows, cols, pitch, box_rows, box_cols, swizzle = self.sig.tmaps[name]
+        return RT.tensor_map_2d(eb, base, rows, cols, pitch, box_rows, box_cols, swizzle)
 
     def bind(self, name: str, buf: RT.DeviceBuffer):
         """Use an externally owned device buffer for parameter `name`."""

@@ -53,7 +53,7 @@ _PROTOS = {
     "dpia_launch_pdl": (_i, [_vp, _i, C.c_uint, C.c_uint, C.c_uint, C.c_uint, C.c_uint,
                              C.POINTER(_vp), _vp]),
     "dpia_tensor_map_2d_f32": (_i, [_vp, _u64, _u64, _u64, _u64, C.c_uint, C.c_uint]),
-    "dpia_tensor_map_2d": (_i, [_vp, C.c_int, _u64, _u64, _u64, _u64, C.c_uint, C.c_uint]),
+    "dpia_tensor_map_2d": (_i, [_vp, C.c_int, _u64, _u64, _u64, _u64, C.c_uint, C.c_uint, C.c_int]),
     "dpia_stream_create": (_i, [_i, C.POINTER(_vp)]),
     "dpia_stream_destroy": (_i, [_vp]),
     "dpia_stream_sync": (_i, [_vp]),
@@ -387,11 +387,11 @@ class Event:
 
 
 def tensor_map_2d(elem_bytes: int, base: int, rows: int, cols: int, pitch: int, box_rows: int,
-                  box_cols: int):
+                  box_cols: int, swizzle: int = 0):
     """A CUtensorMap (128 bytes, as a ctypes array passed to a kernel by
     value) of a row-major rows x cols matrix at device address `base`."""
     m = (ctypes.c_uint64 * 16)()
-    lib().dpia_tensor_map_2d(m, elem_bytes, base, rows, cols, pitch, box_rows, box_cols)
+    lib().dpia_tensor_map_2d(m, elem_bytes, base, rows, cols, pitch, box_rows, box_cols, swizzle)
     return m
 
 

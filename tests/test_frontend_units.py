@@ -286,6 +286,7 @@ def test_vectorised_fold_emission(monkeypatch):
     cfg = dot_literal_config()
     prog = compile_program(cfg.text)
     outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    monkeypatch.setattr(E, "ROW_TMA", False)      # the register-path lowering (TMA rows: test_stream_tail)
     monkeypatch.setattr(E, "VEC_PREFETCH", 0)
     monkeypatch.setattr(E, "TAIL_RING", False)
     src, _ = E.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
@@ -320,6 +321,7 @@ def test_vectorised_fold_pipelining(monkeypatch):
     cfg = dot_literal_config()
     prog = compile_program(cfg.text)
     outs, ins = [("out", prog.out_type)], [(n, t.data) for n, t in prog.source.params]
+    monkeypatch.setattr(E, "ROW_TMA", False)      # the register-path lowering (TMA rows: test_stream_tail)
 
     def emit(**kw):
         for k, v in kw.items():

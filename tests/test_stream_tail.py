@@ -54,15 +54,15 @@ def test_stream_tail_falls_back(monkeypatch):
 
 # ------------------------------------------------------------------ GPU
 
-def _run(chunk, n, launch, inputs, float_mode, stream=True):
+def _run(chunk, n, launch, inputs, float_mode, stream=True, rows=True):
     from paper_1710_08332_b200 import executable
     from paper_1710_08332_b200 import runtime as RT
-    old = EM.STREAM_TAIL
-    EM.STREAM_TAIL = stream
+    old = EM.STREAM_TAIL, EM.ROW_TMA
+    EM.STREAM_TAIL, EM.ROW_TMA = stream, rows
     try:
         exe = executable(compile_program(dot_literal_program(chunk)), launch, {"n": n}, float_mode=float_mode)
     finally:
-        EM.STREAM_TAIL = old
+        EM.STREAM_TAIL, EM.ROW_TMA = old
     st = RT.Stream(0)
     for nm, v in inputs.items():
         exe.upload(nm, v, st)
@@ -96,7 +96,7 @@ def test_stream_tail_bit_identical_fp32(chunk, n, G, L):
     inputs = {"xs": rng.uniform(0, 1, n * chunk).astype(np.float32),
               "ys": rng.uniform(0, 1, n * chunk).astype(np.float32)}
     a, exe = _run(chunk, n, (G, L), inputs, True, stream=True)
-    b, ref = _run(chunk, n, (G, L), inputs, True, stream=False)
+    b, ref = _run(chunk, n, (G, L), inputs, True, stream=False, rows=False)
     assert exe.sig.kernels[0].extra_blocks == 1 and ref.sig.kernels[0].extra_blocks == 0
     assert a.view(np.uint32)[0] == b.view(np.uint32)[0]
 
@@ -127,5 +127,23 @@ def test_stream_tail_chained_steps():
     for xs, ys, _, _, bo in steps:
         got = np.empty(1, np.float32)
         bo.download(got.view(np.uint8), st)
-        want, _ = _run(chunk, n, launch, {"xs": xs, "ys": ys}, True, stream=False)
+        want, _ = _run(chunk, n, launch, {"xs": xs, "ys": ys}, True, stream=False, rows=False)
         assert got.view(np.uint32)[0] == want.view(np.uint32)[0]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stream", [True, False])
+@pytest.mark.parametrize("chunk,n,G,L", [(1024, 16384, 512, 32), (1024, 16384, 128, 32), (512, 8192, 32, 128),
+                                         (256, 4096, 8, 64), (128, 3072, 32, 32)])
+def test_row_tma_folds_bit_identical(stream, chunk, n, G, L):
+    """Work-item folds read through 2-D TMA row boxes (128-byte swizzle,
+    per-warp slot ring running ahead across rounds) give the bits of the
+    register-queue folds, with and without the streaming tail (the ticket
+    tail's static shared flag sits in front of the slots)."""
+    rng = np.random.default_rng(n + L)
+    inputs = {"xs": rng.uniform(0, 1, n * chunk).astype(np.float32),
+              "ys": rng.uniform(0, 1, n * chunk).astype(np.float32)}
+    a, exe = _run(chunk, n, (G, L), inputs, True, stream=stream, rows=True)
+    b, _ = _run(chunk, n, (G, L), inputs, True, stream=stream, rows=False)
+    assert "dpia::tma_tile_2d(" in exe.src and exe.sig.tmaps
+    assert a.view(np.uint32)[0] == b.view(np.uint32)[0]

@@ -32,7 +32,7 @@ def test_mm_b_tile_is_a_tma_box_and_a_tile_is_not():
     cfg = mm_tma_config()
     src, sig = _emit(cfg.text, cfg.launch)
     # B (K x N row-major): 16-row x 128-column boxes at (128 * bx, 16 * k)
-    assert sig.tmaps == {"dpia_tm0": ("B", 4, 4096, 4096, 16384, 16, 128)}
+    assert sig.tmaps == {"dpia_tm0": ("B", 4, 4096, 4096, 16384, 16, 128, 0)}
     assert "const __grid_constant__ dpia::TensorMap dpia_tm0" in src
     assert src.count("dpia::tma_tile_2d(") == 2          # prologue + in-loop refill
     assert "dpia::tile_bar_init(" in src and "dpia::ring_wait(" in src
@@ -47,7 +47,7 @@ def test_tma_off_by_default_and_int_mode_geometry():
     assert sig.tmaps == {}
     src, sig = _emit(mm_program(256, 128, 384, 128, 8, 8), ((1, 2), (16, 16)), float_mode=False)
     # N = T: the tile is one contiguous run of B, boxed as 4 rows of 256
-    assert sig.tmaps == {"dpia_tm0": ("B", 8, 192, 256, 2048, 4, 256)}
+    assert sig.tmaps == {"dpia_tm0": ("B", 8, 192, 256, 2048, 4, 256, 0)}
     assert "long long" in src
 
 
@@ -56,7 +56,7 @@ def test_rect_tiles_and_non_multiple_boxes():
     assert len(sig.tmaps) == 1
     # a 16-column tile of 4-byte elements is 64 bytes: a legal box
     src, sig = _emit(mm_program(32, 32, 32, 16, 8, 4), ((2, 2), (4, 4)))
-    assert sig.tmaps == {"dpia_tm0": ("B", 4, 32, 32, 128, 8, 16)}
+    assert sig.tmaps == {"dpia_tm0": ("B", 4, 32, 32, 128, 8, 16, 0)}
 
 
 def test_tma_source_compiles_for_sm100a():

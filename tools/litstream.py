@@ -44,9 +44,9 @@ def main():
     prog = compile_program(dot_literal_program(chunk), name="dot_literal")
     ref = None
     geoms = [(512, 32), (256, 32), (128, 32), (64, 32), (256, 64), (128, 64), (64, 128)]
-    for stream in (False, True):
+    for stream, rows in ((False, False), (True, False), (True, True), (False, True)):
         for G, L in geoms if stream else geoms[:1]:
-            EM.STREAM_TAIL = stream
+            EM.STREAM_TAIL, EM.ROW_TMA = stream, rows
             exe = executable(prog, (G, L), {"n": n}, float_mode=True)
             exe.upload("xs", xs, st)
             exe.upload("ys", ys, st)
@@ -55,7 +55,7 @@ def main():
             st.sync()
             ref = out if ref is None else ref
             R = -(-n // (G * L))
-            print(f"stream={int(stream)} ({G:3d},{L:3d}) rounds={R}: {us:8.2f} us  "
+            print(f"stream={int(stream)} rows={int(rows)} ({G:3d},{L:3d}) rounds={R}: {us:8.2f} us  "
                   f"{8 * n * chunk / us / 1e3:7.1f} GB/s  extra_blocks={exe.sig.kernels[0].extra_blocks}  "
                   f"{'==' if out.view(np.uint32)[0] == ref.view(np.uint32)[0] else '!='} ticket tail",
                   flush=True)
