@@ -419,6 +419,27 @@ __device__ __forceinline__ void stream_wait(const unsigned int* cnt, long long& 
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Parity pipelining of a streaming tail across chained launches: launch e
+// uses partials/counters slice e & 1; rel[p] holds the epoch of the last
+// launch that finished with slice p.  A launch waits (once per thread) for
+// the launch two back to have released its slice before it first touches
+// it; the tail releases it after its last read.  Epochs start at 2 with
+// rel = {0, 1} (launcher.Executable).
+__device__ __forceinline__ void parity_wait_once(bool& pending, const unsigned int* rel,
+                                                 unsigned int epoch) {
+  if (pending) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(rel) : "memory");
+    } while (v + 2u < epoch);
+    pending = false;
+  }
+}
+__device__ __forceinline__ void parity_release(unsigned int* rel, unsigned int epoch) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(rel), "r"(epoch) : "memory");
+}
+
 // --------------------------------------------- 2-D TMA tensor tiles
 // The CUtensorMap of an input, passed by value as a __grid_constant__ kernel
 // parameter (runtime: dpia_tensor_map_2d).  tma_tile_2d: the issuing thread

@@ -98,6 +98,13 @@ TMA_PROBE_MAX = 1 << 16            # copy statements the box probe may enumerate
 # while rounds > r still run (ProgramEmitter._stream_plan); DPIA_STREAM_TAIL=0
 # keeps the last-block ticket tail
 STREAM_TAIL = os.environ.get("DPIA_STREAM_TAIL", "1") != "0"
+# pipelined streaming tail: the partials and round counters are double-
+# buffered by launch parity (an epoch kernel argument), so a launch chained
+# behind the previous one waits only for the launch two back to release its
+# parity, and for the previous grid only before it writes its outputs --
+# consecutive launches' serial tails run concurrently (DPIA_STREAM_PIPE=0:
+# the launch waits for the previous grid before it first writes the partials)
+STREAM_PIPE = os.environ.get("DPIA_STREAM_PIPE", "1") != "0"
 # work-item row folds: a long sequential fold of each work-item of a
 # mapGlobal over its own contiguous chunk of an input (config 1's literal
 # reduceSeq) reads the chunks of a warp's 32 consecutive work-items as 2-D TMA
@@ -212,6 +219,7 @@ class KernelInfo:
     decls: List = field(default_factory=list, repr=False)            # kernel-level buffers
     extra_blocks: int = 0        # blocks launched beyond the user's grid (a streaming tail block)
     counter_words: int = 4       # 32-bit words of the kernel's counter buffer
+    counter_init: List[Tuple[int, int]] = field(default_factory=list, repr=False)  # (word, value) after zeroing
 
 
 @dataclass
@@ -544,6 +552,7 @@ class KernelEmitter:
         self.tmaps_used: List[str] = []
         self.stream_unsafe = False           # a streaming tail read the partials outside the ring
         self.smem_1k = False                 # dynamic shared memory must start 1024-byte aligned
+        self.tail_mark: Optional[int] = None  # first line of a streaming tail block
 
     # ---------------------------------------------------------- helpers
     def fresh(self, base: str) -> str:
@@ -1312,9 +1321,12 @@ class KernelEmitter:
             for name, b, base in streams:
                 if st is not None and b.key in st["partials"]:
                     # streaming tail: the rounds that wrote this piece's
-                    # partials have published (ProgramEmitter._stream_plan)
-                    out.append(f"{p}  dpia::stream_wait(dpia_counter, dpia_ready, "
-                               f"(long long)({self.r(base)}) + {C * W}, {st['gsize']}, {st['n']});")
+                    # partials have published (ProgramEmitter._stream_plan);
+                    # the piece's index within this launch's parity slice
+                    at = Ix([(m, c) for m, c in base.terms if "dpia_par" not in IX.free_names(Ix([(m, c)]))])
+                    cnt = f"dpia_counter + dpia_par * {st['R']}" if st["pipe"] else "dpia_counter"
+                    out.append(f"{p}  dpia::stream_wait({cnt}, dpia_ready, "
+                               f"(long long)({self.r(at)}) + {C * W}, {st['gsize']}, {st['n']});")
                     st["waits"] += 1
             out.append(f"{p}  dpia::ring_expect({mb} + {slot}, {piece * len(streams)}u);")
             for (name, b, base), off in zip(streams, offs):
@@ -1653,8 +1665,9 @@ class KernelEmitter:
             if level == "global" and self.prog.stream is not None and not self.prog.in_tail:
                 # streaming tail: this warp's partials of the round are written
                 rnd = "0" if is_single else f"({v} - dpia_gid) / dpia_gsize"
+                base = f"dpia_par * {self.prog.stream['R']} + " if self.prog.stream["pipe"] else ""
                 self.line("__syncwarp();")
-                self.line(f"if ((dpia_tid & 31) == 0) dpia::stream_publish(dpia_counter + {rnd});")
+                self.line(f"if ((dpia_tid & 31) == 0) dpia::stream_publish(dpia_counter + {base}{rnd});")
             for nm, ov in old.items():
                 if ov is None:
                     self.env.pop(nm, None)
@@ -2211,6 +2224,7 @@ class ProgramEmitter:
         self.align: Dict[str, int] = {}      # buffer -> byte alignment its loads need (> 16)
         self.tmaps: Dict[str, Tuple[str, int, int, int, int, int, int, int]] = {}
         self.stream: Optional[dict] = None   # the kernel being emitted has a streaming tail
+        self.buffer_kernels: Dict[str, Set[int]] = {}   # top-level buffer -> kernels that use it
 
     def add_tmap(self, plan) -> str:
         """The tensor-map kernel parameter of a TMA-staged tile (deduplicated
@@ -2300,6 +2314,7 @@ class ProgramEmitter:
                            for it in ([g] if g is not None else []) + tail
                            if binder in exp_names(it)}
         n_items = {binder: sum(1 for it in items if binder in exp_names(it)) for _, _, binder in top}
+        self.buffer_kernels = use
         top_global: List[Tuple[str, DataType]] = []
         kernel_top: Dict[int, List[Tuple[str, str, DataType]]] = {}
         for b_prim, d, binder in top:
@@ -2352,7 +2367,7 @@ class ProgramEmitter:
                header, self.types.struct_text()] + bodies
         return "\n".join(s for s in src if s) + "\n", sig
 
-    def _stream_plan(self, grid, tail) -> Optional[dict]:
+    def _stream_plan(self, ki, grid, tail) -> Optional[dict]:
         """Can this kernel's tail stream?  Its grid phase must be one
         parforGlobal over n work-items (n a multiple of 32, a 1-D launch of
         whole warps, so every warp's loop trip is uniform) that writes
@@ -2389,14 +2404,27 @@ class ProgramEmitter:
         if not parts:
             return None
         gsize = gx * lx * ly
-        return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0}
+        # parity pipelining: the grid phase writes nothing but the partials,
+        # which no other kernel touches
+        shared = {b.key for b in self.scratch} | {nm for nm, _ in self.outputs}
+        pipe = STREAM_PIPE and (W & shared) <= parts and \
+            all(self.buffer_kernels.get(k) == {ki} for k in parts)
+        return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0, "pipe": pipe}
 
     def emit_kernel(self, ki, grid, tail, decls):
         kname = f"{self.name}_k{ki}"
         body_lines = None
-        plan = self._stream_plan(grid, tail)
+        plan = self._stream_plan(ki, grid, tail)
         for stream in ([plan, None] if plan else [None]):
             self.stream = stream
+            saved = {}
+            if stream is not None and stream["pipe"]:
+                # the partials get one slice per launch parity
+                for b in self.scratch:
+                    if b.key in stream["partials"]:
+                        saved[b.key] = (b.dtype, list(b.prefix))
+                        b.dtype = Array(nat(2), b.dtype)
+                        b.prefix = [ix("dpia_par")] + list(b.prefix)
             ke = KernelEmitter(self, kname)
             for attempt in ("record", "final"):
                 ke.reset()
@@ -2411,7 +2439,11 @@ class ProgramEmitter:
                 body_lines = ke.lines
             if stream is None or (stream["waits"] and not ke.stream_unsafe):
                 break
+            for b in self.scratch:
+                if b.key in saved:
+                    b.dtype, b.prefix = saved[b.key]
         stream, self.stream = self.stream, None
+        pipe = stream is not None and stream["pipe"]
         args: List[Tuple[str, str]] = [("out", n) for n, _ in self.outputs]
         args += [("in", n) for n, _ in self.inputs]
         args += [("scratch", b.cname) for b in self.scratch if b.cname in ke.used_scratch
@@ -2424,6 +2456,8 @@ class ProgramEmitter:
         args += [("tmap", t) for t in ke.tmaps_used]
         if grid is not None and tail:
             args.append(("counter", "dpia_counter"))
+        if pipe:
+            args.append(("epoch", "dpia_epoch"))
         if self.peer and ki == self.peer_kernel:
             args += [("peer_boxes", "dpia_peer_boxes"), ("peer_rank", "dpia_rank"),
                      ("peer_world", "dpia_world"), ("peer_epoch", "dpia_epoch")]
@@ -2437,6 +2471,9 @@ class ProgramEmitter:
                 continue
             if kind == "tmap":
                 params.append(f"const __grid_constant__ dpia::TensorMap {n}")
+                continue
+            if kind == "epoch":
+                params.append("unsigned int dpia_epoch")
                 continue
             if kind.startswith("peer_"):
                 params.append({"peer_boxes": "const unsigned long long * __restrict__ dpia_peer_boxes",
@@ -2463,6 +2500,10 @@ class ProgramEmitter:
         else:
             head.append("  const int dpia_nthreads = (int)(blockDim.x * blockDim.y);")
         head.append("  const int dpia_tid = (int)(threadIdx.y * blockDim.x + threadIdx.x);")
+        if pipe:
+            head.append("  const int dpia_par = (int)(dpia_epoch & 1u);")
+            head.append("  bool dpia_pw = true;")
+            body_lines = self._pipe_waits(body_lines, ke, stream, args, CHAIN and ki == 0)
         if ki > 0:
             # launched with programmatic dependent launch (launcher.Executable):
             # the grid may be scheduled while the previous phase's kernel still
@@ -2477,7 +2518,8 @@ class ProgramEmitter:
             # grid may still use (`_chain_waits`); all no-ops when not chained
             head.append("  dpia::pdl_trigger();")
             head.append("  bool dpia_chained = true;")
-            body_lines = self._chain_waits(body_lines, args)
+            if not pipe:
+                body_lines = self._chain_waits(body_lines, args)
         if ke.uses_gid or stream is not None:
             wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
             it = "long long" if wide else "int"
@@ -2493,7 +2535,9 @@ class ProgramEmitter:
                           barriers=frozenset(ke.barriers), hoisted=frozenset(ke.hoisted),
                           rotated=dict(ke.rotated), decls=list(decls),
                           extra_blocks=1 if stream is not None else 0,
-                          counter_words=max(4, stream["R"]) if stream is not None else 4)
+                          counter_words=(2 * stream["R"] + 2 if pipe else max(4, stream["R"]))
+                          if stream is not None else 4,
+                          counter_init=[(2 * stream["R"] + 1, 1)] if pipe else [])
         return text, info
 
     @staticmethod
@@ -2518,6 +2562,36 @@ class ProgramEmitter:
                 if at and out[-1].lstrip().startswith("#pragma"):
                     at -= 1
                 out.insert(at, f"{ind}dpia::pdl_wait_once(dpia_chained);")
+            out.append(ln)
+        return out
+
+    def _pipe_waits(self, lines: List[str], ke, st, args, chained: bool) -> List[str]:
+        """Waits of a parity-pipelined streaming-tail kernel: before every
+        line that names the partials or the counters, the launch two back
+        (same parity) must have released them (`dpia::parity_wait_once`);
+        in the tail, before every line that names an output, the previous
+        grid must have completed (`dpia::pdl_wait_once`, chained first
+        kernels only) -- launches' outputs are written in launch order."""
+        mine = [b.cname for b in self.scratch if b.key in st["partials"]] + ["dpia_counter"]
+        outs = [n for kind, n in args if kind == "out"]
+        pat_p = re.compile(r"\b(" + "|".join(re.escape(n) for n in mine + [n + "_raw" for n in mine]) + r")\b")
+        pat_o = re.compile(r"\b(" + "|".join(re.escape(n) for n in outs + [n + "_raw" for n in outs]) + r")\b") \
+            if outs else None
+        tail_from = ke.tail_mark if ke.tail_mark is not None else len(lines)
+        rel = f"dpia_counter + {2 * st['R']} + dpia_par"
+        out: List[str] = []
+        for k, ln in enumerate(lines):
+            waits = []
+            if pat_p.search(ln):
+                waits.append(f"dpia::parity_wait_once(dpia_pw, {rel}, dpia_epoch);")
+            if chained and k >= tail_from and pat_o is not None and pat_o.search(ln):
+                waits.append("dpia::pdl_wait_once(dpia_chained);")
+            if waits:
+                ind = ln[:len(ln) - len(ln.lstrip())]
+                at = len(out)
+                if at and out[-1].lstrip().startswith("#pragma"):
+                    at -= 1
+                out[at:at] = [ind + w for w in waits]
             out.append(ln)
         return out
 
@@ -2548,6 +2622,8 @@ class ProgramEmitter:
 
     def _kernel_body(self, ke: KernelEmitter, grid, tail, decls):
         saved_env = {}
+        if self.stream is not None and self.stream["pipe"]:
+            ke.R["dpia_par"] = 2
         for space, binder, d in decls:
             # declare kernel-level buffers (top-level local / private)
             if space == "local":
@@ -2576,6 +2652,7 @@ class ProgramEmitter:
                 # the streaming tail block: partials [0, dpia_ready) are known
                 # to be published (dpia::stream_wait)
                 ke.open("else")
+                ke.tail_mark = len(ke.lines)
                 ke.line("long long dpia_ready = 0;")
             elif grid is not None:
                 ke.line("__shared__ bool dpia_last;")
@@ -2592,7 +2669,8 @@ class ProgramEmitter:
                     ke.env[binder] = Buffer(binder, cname, "private", d)
             ke.plan_uniform(seq_all(list(tail)),
                             opaque={id(it) for it in tail if not self.is_cooperative(it)})
-            for it in tail:
+            released = False
+            for q, it in enumerate(tail):
                 if self.is_cooperative(it):
                     ke.comm(it)
                 else:
@@ -2603,6 +2681,16 @@ class ProgramEmitter:
                     ke.comm(it)
                     ke.single_thread = False
                     ke.close()
+                if grid is not None and st is not None and st["pipe"] and not released and \
+                        not any(exp_names(t2) & st["partials"] for t2 in tail[q + 1:]):
+                    # the partials of this launch's parity are consumed: reset
+                    # its round counters and release the parity to the launch
+                    # two ahead, before this launch waits to write its outputs
+                    R = st["R"]
+                    ke.line(f"if (dpia_tid == 0) {{ for (int dpia_r = 0; dpia_r < {R}; ++dpia_r) "
+                            f"dpia_counter[dpia_par * {R} + dpia_r] = 0u; "
+                            f"dpia::parity_release(dpia_counter + {2 * R} + dpia_par, dpia_epoch); }}")
+                    released = True
             if self.peer and ke.kname == f"{self.name}_k{self.peer_kernel}":
                 on, od = self.outputs[0]
                 from ..layout import shape_of
@@ -2613,10 +2701,11 @@ class ProgramEmitter:
                         f"reinterpret_cast<{self.scalar}*>({on}), {nsc}, dpia_peer_boxes, dpia_rank, "
                         "dpia_world, dpia_epoch, dpia_tid, dpia_nthreads);")
             if grid is not None and st is not None:
-                # every round has been published and consumed: reset the
-                # counters for the next launch
-                ke.line(f"if (dpia_tid == 0) for (int dpia_r = 0; dpia_r < {st['R']}; ++dpia_r) "
-                        "dpia_counter[dpia_r] = 0u;")
+                if not st["pipe"]:
+                    # every round has been published and consumed: reset the
+                    # counters for the next launch
+                    ke.line(f"if (dpia_tid == 0) for (int dpia_r = 0; dpia_r < {st['R']}; ++dpia_r) "
+                            "dpia_counter[dpia_r] = 0u;")
                 ke.close()
             elif grid is not None:
                 ke.line("dpia::grid_reset(dpia_counter, dpia_tid);")

@@ -38,6 +38,9 @@ class Executable:
     counters: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
     peer: object = None             # peer.PeerGroup of the fused cross-GPU combine
     _args: List = field(default_factory=list)
+    # launch epoch of parity-pipelined streaming tails (cuda/emit.py STREAM_PIPE):
+    # bumped before every launch, first launch 2 (the release words start at {0, 1})
+    _epoch: object = field(default_factory=lambda: RT.C.c_uint(1))
 
     @property
     def launch_geom(self):
@@ -66,6 +69,12 @@ class Executable:
             if k.fused_tail and k.name not in self.counters:
                 c = RT.DeviceBuffer(4 * k.counter_words, self.device)
                 c.zero()
+                if k.counter_init:
+                    init = np.zeros(k.counter_words, np.uint32)
+                    for word, value in k.counter_init:
+                        init[word] = value
+                    c.upload(init)
+                    RT.lib().dpia_device_sync(self.device)   # before any launch stream sees it
                 self.counters[k.name] = c
         self._args = []
         for k in self.sig.kernels:
@@ -85,6 +94,8 @@ class Executable:
                     vals.append(self.peer.epoch)       # shared; bumped by every launch
                 elif kind == "tmap":
                     vals.append(self._tensor_map(n, self.buffers[self.sig.tmaps[n][0]].ptr))
+                elif kind == "epoch":
+                    vals.append(self._epoch)           # shared; bumped by every launch
                 else:
                     vals.append(RT.C.c_uint64(self.counters[k.name].ptr))
             self._args.append(vals)
@@ -124,6 +135,7 @@ class Executable:
         inputs, e.g. repeated steps); results are identical either way."""
         if self.peer is not None:
             self.peer.next_epoch()
+        self._epoch.value += 1
         (g, l) = self.sig.launch or self.geometry
         for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
             grid = (g[0] + k.extra_blocks, g[1]) if k.grid == "launch" else (1, 1)
@@ -147,6 +159,7 @@ class Executable:
                              f"{[need[n] for n in bad]} bytes")
         if self.peer is not None:
             self.peer.next_epoch()
+        self._epoch.value += 1
         (g, l) = self.sig.launch or self.geometry
         for i, (k, vals) in enumerate(zip(self.sig.kernels, self._args)):
             vals = [RT.C.c_uint64(ptrs[n]) if kind in ("out", "in") and n in ptrs

@@ -30,13 +30,32 @@ def _emit(chunk, n, launch, float_mode=True):
 def test_literal_dot_streams_its_tail():
     src, sig = _emit(1024, 16384, (128, 32))
     k = sig.kernels[0]
-    assert k.extra_blocks == 1 and k.counter_words == 4 and k.fused_tail
-    assert "dpia::stream_wait(dpia_counter, dpia_ready" in src
-    assert "dpia::stream_publish(dpia_counter + (i_" in src      # 4 rounds: a round index
+    # 4 rounds x 2 launch parities of round counters, 2 parity release words
+    assert k.extra_blocks == 1 and k.counter_words == 10 and k.fused_tail
+    assert k.counter_init == [(9, 1)] and ("epoch", "dpia_epoch") in k.args
+    assert "dpia::stream_wait(dpia_counter + dpia_par * 4, dpia_ready" in src
+    assert "dpia::stream_publish(dpia_counter + dpia_par * 4 + (i_" in src   # a round index
+    assert "g_tmp4[16384 * dpia_par + " in src                   # the partials: one slice per parity
+    assert "dpia::parity_release(dpia_counter + 8 + dpia_par, dpia_epoch)" in src
+    assert "dpia::parity_wait_once(dpia_pw, dpia_counter + 8 + dpia_par, dpia_epoch);" in src
     assert "dpia::grid_arrive(dpia_counter" not in src
     assert "(gridDim.x - 1)" in src
+    # the output is written after the previous grid completed; the partials
+    # are not waited on that way any more
+    body = src.split('extern "C"')[1]
+    assert body.count("dpia::pdl_wait_once(dpia_chained);") == 1
+    assert body.index("dpia::pdl_wait_once(dpia_chained);") < body.index("out[0] =")
     src, sig = _emit(1024, 16384, (16, 32))                      # 32 rounds
-    assert sig.kernels[0].counter_words == 32
+    assert sig.kernels[0].counter_words == 66
+    assert sig.buffers[0][1].size.const == 2                     # doubled partials
+
+
+def test_stream_tail_without_parity_pipelining(monkeypatch):
+    monkeypatch.setattr(EM, "STREAM_PIPE", False)
+    src, sig = _emit(1024, 16384, (128, 32))
+    k = sig.kernels[0]
+    assert k.extra_blocks == 1 and k.counter_words == 4 and not k.counter_init
+    assert "dpia_par" not in src.split('extern "C"')[1] and "dpia::stream_wait(dpia_counter, dpia_ready" in src
 
 
 def test_stream_tail_falls_back(monkeypatch):
