@@ -111,6 +111,37 @@ def main():
         assert vals[0] == vals[1] == vals[2], vals
         run.peer.close()
         print(f"ok peer {kind}", flush=True)
+    # TMA row folds + a parity-pipelined streaming tail (fp32: the row boxes
+    # are 16-byte vectors), several launches chained; TMA k-tiles (mm, int)
+    from paper_1710_08332_b200 import executable
+    from paper_1710_08332_b200.bench_programs import dot_literal_config
+    c = dot_literal_config(N=1 << 18)
+    exe = executable(compile_program(c.text), c.launch, c.sigma, float_mode=True)
+    assert exe.sig.kernels[0].extra_blocks == 1 and exe.sig.tmaps, "streaming tail + row boxes"
+    rng = np.random.default_rng(12)
+    xs = rng.uniform(0, 1, 1 << 18).astype(np.float32)
+    ys = rng.uniform(0, 1, 1 << 18).astype(np.float32)
+    st = RT.Stream(0)
+    exe.upload("xs", xs, st)
+    exe.upload("ys", ys, st)
+    for k in range(4):
+        exe.launch(st, chain=k > 0)
+    got = float(np.asarray(exe.download("out", st))[0])
+    st.sync()
+    want = float(np.dot(xs.astype(np.float64), ys.astype(np.float64)))
+    assert abs(got - want) <= 1e-4 * want, (got, want)
+    print("ok dot_literal streaming tail + TMA row folds", flush=True)
+    c = mm_config(M=256, N=128, K=256, T=128, BK=16, R=8)
+    exe = executable(compile_program(c.text), c.launch, {}, float_mode=False, tma_tiles=True)
+    assert exe.sig.tmaps, "TMA k-tiles"
+    A, B = ints((256, 256), 13), ints((256, 128), 14)
+    exe.upload("A", A, st)
+    exe.upload("B", B, st)
+    exe.launch(st)
+    got = np.asarray(exe.download("out", st))
+    st.sync()
+    assert np.array_equal(got.astype(np.int64).reshape(256, 128), A @ B), "mm tma"
+    print("ok mm TMA k-tiles", flush=True)
     # the reference's golden programs
     from conftest import load_golden
     for case in load_golden("programs.json"):

@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --traffic committed \
     > gpurun_out/launches_bench.json 2>&1
-for w in asum dot dot_literal gemv gemv_xprivate mm scal; do
+for w in asum dot dot_literal gemv gemv_xprivate mm mm_tma scal; do
   ncu --set full --clock-control none --import-source on -k "regex:^${w}_k0$" -s 3 -c 1 \
       -o gpurun_out/prof_${w} python bench.py --workload $w --steps 2 --warmup 3 --no-suite --no-cpu \
       --traffic committed > gpurun_out/ncu_${w}.log 2>&1
