@@ -41,6 +41,7 @@ class Executable:
     # launch epoch of parity-pipelined streaming tails (cuda/emit.py STREAM_PIPE):
     # bumped before every launch, first launch 2 (the release words start at {0, 1})
     _epoch: object = field(default_factory=lambda: RT.C.c_uint(1))
+    _tmap_cache: Dict = field(default_factory=dict)
 
     @property
     def launch_geom(self):
@@ -103,9 +104,17 @@ class Executable:
 
     def _tensor_map(self, name: str, base: int):
         """The TMA descriptor of tensor-map parameter `name` over the input
-        at device address `base` (cuda/emit.py KernelEmitter._tma_plan)."""
-        _x, eb, rows, cols, pitch, box_rows, box_cols, swizzle = self.sig.tmaps[name]
-        return RT.tensor_map_2d(eb, base, rows, cols, pitch, box_rows, box_cols, swizzle)
+        at device address `base` (cuda/emit.py KernelEmitter._tma_plan),
+        encoded once per address (launch_with re-points inputs every step)."""
+        key = (name, base)
+        m = self._tmap_cache.get(key)
+        if m is None:
+            _x, eb, rows, cols, pitch, box_rows, box_cols, swizzle = self.sig.tmaps[name]
+            m = RT.tensor_map_2d(eb, base, rows, cols, pitch, box_rows, box_cols, swizzle)
+            if len(self._tmap_cache) > 256:
+                self._tmap_cache.clear()
+            self._tmap_cache[key] = m
+        return m
 
     def bind(self, name: str, buf: RT.DeviceBuffer):
         """Use an externally owned device buffer for parameter `name`."""
