@@ -148,7 +148,8 @@ def cmd_compile(args) -> int:
     src, _sig = emit_cuda(prog.imperative, [("out", prog.out_type)],
                           [(n, t.data) for n, t in prog.source.params],
                           float_mode=not args.int_mode, name=prog.name, init_new=args.init_new,
-                          simplify=args.simplify_indices != "off", sigma=sigma, launch=args.launch)
+                          simplify=args.simplify_indices != "off", sigma=sigma, launch=args.launch,
+                          tma_tiles=True if args.tma_tiles else None)
     dest = args.output or f"{stem}.cu"
     Path(dest).write_text(src)
     print(f"wrote {dest}")
@@ -317,6 +318,8 @@ def build_parser() -> argparse.ArgumentParser:
     c.add_argument("--sizes", help="`name = value` file with the nat parameters to specialise")
     c.add_argument("--init-new", action="store_true", help="zero-initialize allocations explicitly")
     c.add_argument("--check-only", action="store_true")
+    c.add_argument("--tma-tiles", action="store_true",
+                   help="stage rotating 2-D box k-tiles with TMA tensor copies (needs --launch)")
     c.add_argument("--simplify-indices", choices=["on", "off"], default="on",
                    help="accepted for compatibility: CUDA subscripts are always range-simplified")
     _value_mode(c)

@@ -77,6 +77,19 @@ def test_cli_compile_cuda(tmp_path):
         assert needle in text, needle
 
 
+def test_cli_compile_tma_tiles(tmp_path):
+    """`compile --tma-tiles --launch ...` lowers mm's rotating B k-tile to TMA
+    tensor copies (a CUtensorMap kernel parameter); without the flag the
+    register staging stays."""
+    from paper_1710_08332_b200.bench_programs import mm_program
+    f = _prog(tmp_path, mm_program(256, 256, 128, 128, 16, 8), "mm.dpia")
+    assert main(["compile", f, "--launch", "2,2,16,16", "--tma-tiles", "-o", str(tmp_path / "a.cu")]) == 0
+    assert main(["compile", f, "--launch", "2,2,16,16", "-o", str(tmp_path / "b.cu")]) == 0
+    a, b = (tmp_path / "a.cu").read_text(), (tmp_path / "b.cu").read_text()
+    assert "dpia::TensorMap dpia_tm0" in a and "dpia::tma_tile_2d(" in a
+    assert "dpia::TensorMap dpia_tm0" not in b
+
+
 def test_cli_exit_codes(tmp_path):
     assert main(["compile", _prog(tmp_path, "(param xs (exp (array 4 num))) (map")]) == 2
     assert main(["compile", _prog(tmp_path, "(param xs (exp (array 4 num)))\n(zip xs (split 2 xs))",
