@@ -419,19 +419,19 @@ __device__ __forceinline__ void stream_wait(const unsigned int* cnt, long long& 
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-// Parity pipelining of a streaming tail across chained launches: launch e
-// uses partials/counters slice e & 1; rel[p] holds the epoch of the last
-// launch that finished with slice p.  A launch waits (once per thread) for
-// the launch two back to have released its slice before it first touches
-// it; the tail releases it after its last read.  Epochs start at 2 with
-// rel = {0, 1} (launcher.Executable).
+// Slot pipelining of a streaming tail across chained launches: launch e
+// uses partials/counters slice e % K; rel[s] holds the epoch of the last
+// launch that finished with slice s.  A launch waits (once per thread) for
+// the launch K back to have released its slice before it first touches it;
+// the tail releases it after its last read.  The launcher's epochs start at
+// 16 and each rel word starts at its slot's first epoch minus K.
 __device__ __forceinline__ void parity_wait_once(bool& pending, const unsigned int* rel,
-                                                 unsigned int epoch) {
+                                                 unsigned int epoch, unsigned int slots) {
   if (pending) {
     unsigned v;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(rel) : "memory");
-    } while (v + 2u < epoch);
+    } while (v + slots < epoch);
     pending = false;
   }
 }

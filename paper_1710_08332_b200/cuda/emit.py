@@ -105,6 +105,10 @@ STREAM_TAIL = os.environ.get("DPIA_STREAM_TAIL", "1") != "0"
 # consecutive launches' serial tails run concurrently (DPIA_STREAM_PIPE=0:
 # the launch waits for the previous grid before it first writes the partials)
 STREAM_PIPE = os.environ.get("DPIA_STREAM_PIPE", "1") != "0"
+# slices of a pipelined streaming tail's partials and counters: launch e uses
+# slice e % K and waits for launch e - K to release it
+STREAM_PIPE_SLOTS = max(2, int(os.environ.get("DPIA_STREAM_PIPE_SLOTS", "4")))
+EPOCH_BASE = 16                 # the launcher's first epoch (launcher.Executable._epoch)
 # work-item row folds: a long sequential fold of each work-item of a
 # mapGlobal over its own contiguous chunk of an input (config 1's literal
 # reduceSeq) reads the chunks of a warp's 32 consecutive work-items as 2-D TMA
@@ -2409,7 +2413,8 @@ class ProgramEmitter:
         shared = {b.key for b in self.scratch} | {nm for nm, _ in self.outputs}
         pipe = STREAM_PIPE and (W & shared) <= parts and \
             all(self.buffer_kernels.get(k) == {ki} for k in parts)
-        return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0, "pipe": pipe}
+        return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0, "pipe": pipe,
+                "K": STREAM_PIPE_SLOTS}
 
     def emit_kernel(self, ki, grid, tail, decls):
         kname = f"{self.name}_k{ki}"
@@ -2423,7 +2428,7 @@ class ProgramEmitter:
                 for b in self.scratch:
                     if b.key in stream["partials"]:
                         saved[b.key] = (b.dtype, list(b.prefix))
-                        b.dtype = Array(nat(2), b.dtype)
+                        b.dtype = Array(nat(stream["K"]), b.dtype)
                         b.prefix = [ix("dpia_par")] + list(b.prefix)
             ke = KernelEmitter(self, kname)
             for attempt in ("record", "final"):
@@ -2501,7 +2506,7 @@ class ProgramEmitter:
             head.append("  const int dpia_nthreads = (int)(blockDim.x * blockDim.y);")
         head.append("  const int dpia_tid = (int)(threadIdx.y * blockDim.x + threadIdx.x);")
         if pipe:
-            head.append("  const int dpia_par = (int)(dpia_epoch & 1u);")
+            head.append(f"  const int dpia_par = (int)(dpia_epoch % {stream['K']}u);")
             head.append("  bool dpia_pw = true;")
             body_lines = self._pipe_waits(body_lines, ke, stream, args, CHAIN and ki == 0)
         if ki > 0:
@@ -2535,9 +2540,9 @@ class ProgramEmitter:
                           barriers=frozenset(ke.barriers), hoisted=frozenset(ke.hoisted),
                           rotated=dict(ke.rotated), decls=list(decls),
                           extra_blocks=1 if stream is not None else 0,
-                          counter_words=(2 * stream["R"] + 2 if pipe else max(4, stream["R"]))
+                          counter_words=(stream["K"] * (stream["R"] + 1) if pipe else max(4, stream["R"]))
                           if stream is not None else 4,
-                          counter_init=[(2 * stream["R"] + 1, 1)] if pipe else [])
+                          counter_init=self._release_init(stream) if pipe else [])
         return text, info
 
     @staticmethod
@@ -2565,6 +2570,18 @@ class ProgramEmitter:
             out.append(ln)
         return out
 
+    @staticmethod
+    def _release_init(st) -> List[Tuple[int, int]]:
+        """Release words of a pipelined streaming tail before the first
+        launch: slot s's first launch (the smallest epoch >= EPOCH_BASE with
+        epoch % K == s) must find the slot released by launch epoch - K."""
+        K, R = st["K"], st["R"]
+        out = []
+        for slot in range(K):
+            first = EPOCH_BASE + (slot - EPOCH_BASE) % K
+            out.append((K * R + slot, first - K))
+        return out
+
     def _pipe_waits(self, lines: List[str], ke, st, args, chained: bool) -> List[str]:
         """Waits of a parity-pipelined streaming-tail kernel: before every
         line that names the partials or the counters, the launch two back
@@ -2578,12 +2595,12 @@ class ProgramEmitter:
         pat_o = re.compile(r"\b(" + "|".join(re.escape(n) for n in outs + [n + "_raw" for n in outs]) + r")\b") \
             if outs else None
         tail_from = ke.tail_mark if ke.tail_mark is not None else len(lines)
-        rel = f"dpia_counter + {2 * st['R']} + dpia_par"
+        rel = f"dpia_counter + {st['K'] * st['R']} + dpia_par"
         out: List[str] = []
         for k, ln in enumerate(lines):
             waits = []
             if pat_p.search(ln):
-                waits.append(f"dpia::parity_wait_once(dpia_pw, {rel}, dpia_epoch);")
+                waits.append(f"dpia::parity_wait_once(dpia_pw, {rel}, dpia_epoch, {st['K']}u);")
             if chained and k >= tail_from and pat_o is not None and pat_o.search(ln):
                 waits.append("dpia::pdl_wait_once(dpia_chained);")
             if waits:
@@ -2623,7 +2640,7 @@ class ProgramEmitter:
     def _kernel_body(self, ke: KernelEmitter, grid, tail, decls):
         saved_env = {}
         if self.stream is not None and self.stream["pipe"]:
-            ke.R["dpia_par"] = 2
+            ke.R["dpia_par"] = self.stream["K"]
         for space, binder, d in decls:
             # declare kernel-level buffers (top-level local / private)
             if space == "local":
@@ -2689,7 +2706,7 @@ class ProgramEmitter:
                     R = st["R"]
                     ke.line(f"if (dpia_tid == 0) {{ for (int dpia_r = 0; dpia_r < {R}; ++dpia_r) "
                             f"dpia_counter[dpia_par * {R} + dpia_r] = 0u; "
-                            f"dpia::parity_release(dpia_counter + {2 * R} + dpia_par, dpia_epoch); }}")
+                            f"dpia::parity_release(dpia_counter + {st['K'] * R} + dpia_par, dpia_epoch); }}")
                     released = True
             if self.peer and ke.kname == f"{self.name}_k{self.peer_kernel}":
                 on, od = self.outputs[0]

@@ -19,7 +19,7 @@ import numpy as np
 
 from . import layout as LY
 from . import runtime as RT
-from .cuda.emit import CudaError, CudaSignature, emit_cuda, normalize_launch
+from .cuda.emit import EPOCH_BASE, CudaError, CudaSignature, emit_cuda, normalize_launch
 from .cuda.hierarchy import check_work_item_races
 from .dtypes import DataType
 from .terms import Phrase
@@ -38,9 +38,10 @@ class Executable:
     counters: Dict[str, RT.DeviceBuffer] = field(default_factory=dict)
     peer: object = None             # peer.PeerGroup of the fused cross-GPU combine
     _args: List = field(default_factory=list)
-    # launch epoch of parity-pipelined streaming tails (cuda/emit.py STREAM_PIPE):
-    # bumped before every launch, first launch 2 (the release words start at {0, 1})
-    _epoch: object = field(default_factory=lambda: RT.C.c_uint(1))
+    # launch epoch of slot-pipelined streaming tails (cuda/emit.py STREAM_PIPE):
+    # bumped before every launch, first launch EPOCH_BASE (the kernels' release
+    # words are initialised for it, KernelInfo.counter_init)
+    _epoch: object = field(default_factory=lambda: RT.C.c_uint(EPOCH_BASE - 1))
     _tmap_cache: Dict = field(default_factory=dict)
 
     @property

@@ -30,14 +30,16 @@ def _emit(chunk, n, launch, float_mode=True):
 def test_literal_dot_streams_its_tail():
     src, sig = _emit(1024, 16384, (128, 32))
     k = sig.kernels[0]
-    # 4 rounds x 2 launch parities of round counters, 2 parity release words
-    assert k.extra_blocks == 1 and k.counter_words == 10 and k.fused_tail
-    assert k.counter_init == [(9, 1)] and ("epoch", "dpia_epoch") in k.args
+    # 4 rounds x K = 4 launch slots of round counters, then 4 release words,
+    # initialised for the first epochs 16..19 (slots 0..3)
+    assert k.extra_blocks == 1 and k.counter_words == 20 and k.fused_tail
+    assert k.counter_init == [(16, 12), (17, 13), (18, 14), (19, 15)] and ("epoch", "dpia_epoch") in k.args
+    assert "const int dpia_par = (int)(dpia_epoch % 4u);" in src
     assert "dpia::stream_wait(dpia_counter + dpia_par * 4, dpia_ready" in src
     assert "dpia::stream_publish(dpia_counter + dpia_par * 4 + (i_" in src   # a round index
-    assert "g_tmp4[16384 * dpia_par + " in src                   # the partials: one slice per parity
-    assert "dpia::parity_release(dpia_counter + 8 + dpia_par, dpia_epoch)" in src
-    assert "dpia::parity_wait_once(dpia_pw, dpia_counter + 8 + dpia_par, dpia_epoch);" in src
+    assert "g_tmp4[16384 * dpia_par + " in src                   # the partials: one slice per slot
+    assert "dpia::parity_release(dpia_counter + 16 + dpia_par, dpia_epoch)" in src
+    assert "dpia::parity_wait_once(dpia_pw, dpia_counter + 16 + dpia_par, dpia_epoch, 4u);" in src
     assert "dpia::grid_arrive(dpia_counter" not in src
     assert "(gridDim.x - 1)" in src
     # the output is written after the previous grid completed; the partials
@@ -46,8 +48,8 @@ def test_literal_dot_streams_its_tail():
     assert body.count("dpia::pdl_wait_once(dpia_chained);") == 1
     assert body.index("dpia::pdl_wait_once(dpia_chained);") < body.index("out[0] =")
     src, sig = _emit(1024, 16384, (16, 32))                      # 32 rounds
-    assert sig.kernels[0].counter_words == 66
-    assert sig.buffers[0][1].size.const == 2                     # doubled partials
+    assert sig.kernels[0].counter_words == 132
+    assert sig.buffers[0][1].size.const == 4                     # one partials slice per slot
 
 
 def test_stream_tail_without_parity_pipelining(monkeypatch):
