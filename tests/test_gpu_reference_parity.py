@@ -164,3 +164,43 @@ def test_scaleout_dot_full_2p31_single_gpu():
     got = run_.result()
     want, absterms = blas_np.hashed_dot(1 << 31, SEEDS["x"], SEEDS["y"])
     assert abs(got - want) <= TOL * absterms, (got, want)
+
+
+def test_dot_literal_chained_job_vs_reference_interpreter():
+    """The bench's job form of config 1's literal program: steps chained
+    behind each other (programmatic dependent launch) over alternating input
+    sets, up to 4 launches' streaming tails in flight (K-slot pipelining).
+    Every step on the golden inputs matches eval_phrase within the stated
+    bound and all steps give the bits of an unchained launch."""
+    from paper_1710_08332_b200 import executable
+    from paper_1710_08332_b200 import runtime as RT
+    cfg = CONFIGS["dot_literal"]()
+    exe = executable(compile_program(cfg.text, name="dot_literal"), cfg.launch, cfg.sigma, float_mode=True)
+    assert exe.sig.kernels[0].extra_blocks == 1 and any(k == "epoch" for k, _ in exe.sig.kernels[0].args)
+    st = RT.Stream(0)
+    sets = [dot_inputs(), {"xs": blas_np.seeded(1 << 24, 10, 0.0, 1.0), "ys": blas_np.seeded(1 << 24, 11, 0.0, 1.0)}]
+    bufs, want_bits = [], []
+    for inp in sets:
+        bx, by = RT.DeviceBuffer(inp["xs"].nbytes), RT.DeviceBuffer(inp["ys"].nbytes)
+        bx.upload(inp["xs"], st)
+        by.upload(inp["ys"], st)
+        bufs.append((bx, by))
+        exe.upload("xs", inp["xs"], st)
+        exe.upload("ys", inp["ys"], st)
+        exe.launch(st)
+        want_bits.append(np.asarray(exe.download("out", st)).view(np.uint32)[0])
+        st.sync()
+    outs = [RT.DeviceBuffer(4) for _ in range(10)]
+    for k in range(10):
+        bx, by = bufs[k % 2]
+        exe.launch_with(st, {"xs": bx.ptr, "ys": by.ptr, "out": outs[k].ptr}, chain=True)
+    st.sync()
+    g = golden("dot_literal_f32")
+    _, absterms = blas_np.dot(sets[0]["xs"], sets[0]["ys"])
+    for k in range(10):
+        got = np.empty(1, np.float32)
+        outs[k].download(got.view(np.uint8), st)
+        st.sync()
+        assert got.view(np.uint32)[0] == want_bits[k % 2], k
+        if k % 2 == 0:
+            assert abs(float(got[0]) - g["result"][0]) <= TOL * absterms
