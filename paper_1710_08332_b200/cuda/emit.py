@@ -1933,8 +1933,8 @@ class KernelEmitter:
         else:
             self.probe_recs.append((dst.buf.key, dst.flat, src[0], src[1], w))
 
-    def _tma_no(self, why: int):
-        self.tma_why = why          # which test rejected the last staging (tests, debugging)
+    def _tma_no(self, why: str):
+        self.tma_why = why          # why the last staging was not a TMA box (tests, debugging)
         return None
 
     def _tma_plan(self, c1: Phrase, fl: Lam, d0: DataType, binder: str, n: Nat, trip: int):
@@ -1946,11 +1946,11 @@ class KernelEmitter:
         element by element.  Returns the box geometry or None."""
         on = TMA_TILES if self.prog.tma_tiles is None else self.prog.tma_tiles
         if not on or not self.launch or self.pf is not None:
-            return self._tma_no(1)
+            return self._tma_no("off or unspecialised")
         dims, elem = split_array(d0)
         E = self._elements(d0)
         if not isinstance(elem, Num) or E is None or len(dims) < 2:
-            return self._tma_no(2)
+            return self._tma_no("not a 2-D scalar tile")
         eb = 4 if self.scalar == "float" else 8
         K = f"dpia_probe_{self.fresh('k')}"
         probe_buf = Buffer(fl.binder, "dpia_probe", "local", d0)
@@ -1976,16 +1976,16 @@ class KernelEmitter:
                 else:
                     self.env[nm] = ov
         if not recs:
-            return self._tma_no(3)
+            return self._tma_no("copies not enumerable")
         xs = {id(r[2]) for r in recs}
         X = recs[0][2]
         if len(xs) != 1 or X.space != "in" or X.prefix or X.swz or X.pad or \
                 any(r[0] != fl.binder for r in recs):
-            return self._tma_no(4)
+            return self._tma_no("not one plain input")
         xdims, xelem = split_array(X.dtype)
         NX = self._elements(X.dtype)
         if not isinstance(xelem, Num) or NX is None:
-            return self._tma_no(5)
+            return self._tma_no("input not scalar or unsized")
         # source = U + c: U the non-constant (work-group-uniform) part, shared by all copies
         uni = lambda e: Ix([(m, c) for m, c in e.terms if m != ()])  # noqa: E731
         U = uni(recs[0][3])
@@ -1993,13 +1993,13 @@ class KernelEmitter:
         for _key, dflat, _x, sflat, w in recs:
             dc, sc = dflat.const, (sflat + (U * -1)).const
             if dc is None or sc is None or uni(sflat) != U:
-                return self._tma_no(6)
+                return self._tma_no("source not tile-uniform plus a constant")
             for lane in range(w):
                 if dc + lane in emap:
-                    return self._tma_no(7)
+                    return self._tma_no("element written twice")
                 emap[dc + lane] = sc + lane
         if sorted(emap) != list(range(E)):
-            return self._tma_no(8)
+            return self._tma_no("tile not covered exactly")
         c0 = emap[0]
         C = next((q for q in range(1, E) if emap[q] != c0 + q), E)
         if C == E:
@@ -2007,23 +2007,23 @@ class KernelEmitter:
             C = max((q for q in range(1, min(E, 256) + 1)
                      if E % q == 0 and (q * eb) % 16 == 0 and E // q <= 256), default=0)
             if not C:
-                return self._tma_no(9)
+                return self._tma_no("no legal box width")
             P = C
         elif E % C:
-            return self._tma_no(9)
+            return self._tma_no("no legal box width")
         else:
             P = emap[C] - c0
         rows = E // C
         if P < C or any(emap[q] != c0 + (q // C) * P + q % C for q in range(E)):
-            return self._tma_no(10)
+            return self._tma_no("not a row-strided box")
         if C > 256 or rows > 256 or (C * eb) % 16 or (P * eb) % 16 or NX % P:
-            return self._tma_no(11)
+            return self._tma_no("box violates TMA limits")
         # origin(k) = U0 + a*k + c0, linear in k and free of other probe atoms
         a, U0 = 0, []
         for m, c in U.terms:
             if K in IX.free_names(Ix([(m, c)])):
                 if len(m) != 1 or IX._ATOMS[m[0]] != ("v", K):
-                    return self._tma_no(12)
+                    return self._tma_no("origin not linear in the loop index")
                 a = c
             else:
                 U0.append((m, c))
