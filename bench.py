@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
-from paper_1710_08332_b200.bench_programs import (asum_config, dot_config,  # noqa: E402
+from paper_1710_08332_b200.bench_programs import (asum_config, asum_proxy_config, dot_config,  # noqa: E402
                                                   dot_literal_config, gemv_config, mm_config,
                                                   mm_tma_config, scal_config)
 
@@ -289,8 +289,8 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
         cfg = Config(name, "", {"n": run.shard.chunks}, run.exe.sig.launch, bytes=run.bytes,
                      flops=(2 if kind == "dot" else 1) * run.shard.elems)
         return cfg, run.exe, None, run.fill_inputs, run.prog
-    if name == "asum":
-        cfg = asum_config()
+    if name in ("asum", "asum_proxy"):
+        cfg = asum_config() if name == "asum" else asum_proxy_config()
         inputs = {"xs": _seeded(1 << 26, 2 + 1000 * rank, -1.0, 1.0)}
     elif name == "dot":
         cfg = dot_config()
@@ -546,6 +546,7 @@ REF_STRATEGY = {
 REF_STRATEGY["dot_literal"] = REF_STRATEGY["dot"]
 REF_STRATEGY["gemv_xprivate"] = REF_STRATEGY["gemv"]
 REF_STRATEGY["mm_tma"] = REF_STRATEGY["mm"]
+REF_STRATEGY["asum_proxy"] = REF_STRATEGY["asum"]
 
 
 def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1):
@@ -556,7 +557,7 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         return None
     vp, ci = ctypes.c_void_p, ctypes.c_int
     out = np.zeros(8192, np.float32)
-    base = "mm" if workload == "mm_tma" else workload
+    base = {"mm_tma": "mm", "asum_proxy": "asum"}.get(workload, workload)
     note = ""
     if workload.startswith("scaleout"):
         # the reference's emitted C indexes with 32-bit int and keeps the
@@ -940,7 +941,7 @@ def main():
     # N = 1: every benchmark program; N > 1: the sharded reductions of
     # BASELINE config 5 (2^31 in total, strong scaling) beside the weak-scaled
     # headline -- gemv / mm / scal would only replicate (no exchange step)
-    names = (("dot", "dot_literal", "asum", "gemv", "gemv_xprivate", "mm", "mm_tma", "scal",
+    names = (("dot", "dot_literal", "asum", "asum_proxy", "gemv", "gemv_xprivate", "mm", "mm_tma", "scal",
               "scaleout_asum", "scaleout_dot") if world == 1 else ("scaleout_asum", "scaleout_dot"))
     if not args.no_suite:
         for w in names:
@@ -1109,6 +1110,10 @@ WORKLOADS = {
     "scal": ("scal N=2^26 fp32 (read + write)", "grid-stride mapGlobal over vec4"),
     "mm": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "128x128 tiles, 8x8 register tiles, toLocal "
            "k-tiles of 16, FFMA2"),
+    "asum_proxy": ("asum proxy N=2^26 fp32 (the reference arm's program: sum, no abs)",
+                   "oracle/ref_programs/asum_proxy.dpia as the reference states it: mapGlobal over "
+                   "1024-element chunks, reduceSeq per chunk, top-level sequential reduce of the 65536 "
+                   "partials (TMA row folds, streaming tail over 16 launch slots)"),
     "mm_tma": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "the mm strategy with B's toLocal k-tile "
                "staged by TMA tensor copies (cp.async.bulk.tensor.2d, 3 rotating slices, mbarrier); "
                "A's transposed k-tile by register prefetch"),

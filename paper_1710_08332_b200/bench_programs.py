@@ -434,6 +434,29 @@ def dot_literal_config(N: int = 1 << 24, chunk: int = 1024, L: int = 32, rounds:
                   bytes=8 * N, flops=2 * N)
 
 
+def asum_proxy_program(chunk: int = 1024) -> str:
+    """The program the reference arm times for asum (oracle/ref_programs/
+    asum_proxy.dpia): the reference language has no `abs`, so its asum is
+    the identical-traffic sum -- mapGlobal over `chunk`-element pieces, a
+    sequential reduce per piece, then the top-level sequential reduce of
+    the partials.  The same program on the GPU gives the same-program
+    comparison with the reference's own CPU path."""
+    return f"""
+(nat n)
+(param xs (exp (array (* n {chunk}) num)))
+(reduce (+) 0 (mapGlobal (lam (c (exp (array {chunk} num))) (reduce (+) 0 c)) (split {chunk} xs)))
+"""
+
+
+def asum_proxy_config(N: int = 1 << 26, chunk: int = 1024, L: int = 32, rounds: int = 4) -> Config:
+    """As dot_literal_config: 65536 work-items in 4 rounds of 128 x 32, TMA
+    row folds, a streaming tail pipelined over launch slots (16 here: the
+    65536-add serial tail is 4x config 1's)."""
+    n = N // chunk
+    G = max(1, n // (L * rounds)) if n % (L * rounds) == 0 else max(1, n // L)
+    return Config("asum_proxy", asum_proxy_program(chunk), {"n": n}, (G, L), bytes=4 * N, flops=N)
+
+
 def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -463,7 +486,8 @@ def gemv_xprivate_config(**kw) -> Config:
 
 CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
            "scal": scal_config, "dot_literal": dot_literal_config,
-           "gemv_xprivate": gemv_xprivate_config, "mm_tma": mm_tma_config}
+           "gemv_xprivate": gemv_xprivate_config, "mm_tma": mm_tma_config,
+           "asum_proxy": asum_proxy_config}
 
 
 def aot_sources():

@@ -2413,8 +2413,12 @@ class ProgramEmitter:
         shared = {b.key for b in self.scratch} | {nm for nm, _ in self.outputs}
         pipe = STREAM_PIPE and (W & shared) <= parts and \
             all(self.buffer_kernels.get(k) == {ki} for k in parts)
+        # launch slots: enough that K launches' serial tails (n in-order adds,
+        # ~2.5 ns each) cover the grid phase of one launch; at least
+        # STREAM_PIPE_SLOTS, at most 16
+        K = max(STREAM_PIPE_SLOTS, min(16, -(-n // 4096)))
         return {"n": n, "gsize": gsize, "R": -(-n // gsize), "partials": parts, "waits": 0, "pipe": pipe,
-                "K": STREAM_PIPE_SLOTS}
+                "K": K}
 
     def emit_kernel(self, ki, grid, tail, decls):
         kname = f"{self.name}_k{ki}"

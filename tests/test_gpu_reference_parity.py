@@ -204,3 +204,27 @@ def test_dot_literal_chained_job_vs_reference_interpreter():
         assert got.view(np.uint32)[0] == want_bits[k % 2], k
         if k % 2 == 0:
             assert abs(float(got[0]) - g["result"][0]) <= TOL * absterms
+
+
+@needs_ref
+@pytest.mark.parametrize("workload,slots", [("asum_proxy", 16), ("dot_literal", 4)])
+def test_literal_programs_bit_identical_to_reference_c_path(workload, slots):
+    """The reference-language programs the reference arm times (asum_proxy,
+    config 1's dot), emitted with TMA row folds and a streaming tail, give
+    the bits of the reference compiler's own c-openmp emission of the same
+    program: the same association (per-chunk left folds, then the left fold
+    of the partials) and, for dot, the same contracted multiply-add."""
+    from paper_1710_08332_b200 import executable
+    cfg = CONFIGS[workload]()
+    exe = executable(compile_program(cfg.text, name=workload), cfg.launch, cfg.sigma, float_mode=True)
+    k = exe.sig.kernels[0]
+    assert k.extra_blocks == 1 and exe.sig.tmaps
+    assert k.counter_words == slots * (-(-cfg.sigma["n"] // (cfg.launch[0] * cfg.launch[1])) + 1)
+    if workload == "asum_proxy":
+        inp = {"xs": blas_np.seeded(1 << 26, 2, -1.0, 1.0)}
+        want = ref_cpu.asum_proxy(inp["xs"])
+    else:
+        inp = dot_inputs()
+        want = ref_cpu.dot(inp["xs"], inp["ys"])
+    got = run(workload, inp)
+    assert np.float32(got[0]).view(np.uint32) == np.float32(want).view(np.uint32), (got[0], want)
