@@ -168,3 +168,16 @@ def test_row_tma_folds_bit_identical(stream, chunk, n, G, L):
     b, _ = _run(chunk, n, (G, L), inputs, True, stream=stream, rows=False)
     assert "dpia::tma_tile_2d(" in exe.src and exe.sig.tmaps
     assert a.view(np.uint32)[0] == b.view(np.uint32)[0]
+
+
+def test_slot_count_scales_with_the_serial_tail():
+    """K launch slots cover the grid phase of one launch with K serial tails:
+    config 1 (16384 partials) gets 4, the asum proxy (65536) 16."""
+    from paper_1710_08332_b200.bench_programs import asum_proxy_config, dot_literal_config
+    for cfg, K in ((dot_literal_config(), 4), (asum_proxy_config(), 16)):
+        prog = compile_program(cfg.text)
+        outs = [("out", prog.out_type)]
+        ins = [(nm, t.data) for nm, t in prog.source.params]
+        src, sig = EM.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+        assert f"const int dpia_par = (int)(dpia_epoch % {K}u);" in src
+        assert sig.kernels[0].counter_words == K * (4 + 1)
