@@ -118,6 +118,7 @@ EPOCH_BASE = 16                 # the launcher's first epoch (launcher.Executabl
 ROW_TMA = os.environ.get("DPIA_ROW_TMA", "1") != "0"
 ROW_TMA_STAGES = int(os.environ.get("DPIA_ROW_TMA_STAGES", "4"))
 ROW_TMA_BOXES = int(os.environ.get("DPIA_ROW_TMA_BOXES", "2"))    # 128-byte box columns per step
+ROW_TMA_INFLIGHT = int(os.environ.get("DPIA_ROW_TMA_INFLIGHT", str(32 * 1024)))  # bytes per warp (64 KiB measured slower)
 # slices of a TMA-staged tile: 2 -- iteration k+1's box is issued right after
 # iteration k's CTA barrier; 3 -- it is issued at the top of iteration k, into
 # the slice iteration k-2 read (free since iteration k-1's barrier)
@@ -1097,10 +1098,14 @@ class KernelEmitter:
                 C //= 2
             if T % C:
                 return False
-            S = max(2, ROW_TMA_STAGES)
-            # fit the warps' slots (two streams assumed) in shared memory
+            # slots: about ROW_TMA_INFLIGHT bytes in flight per warp over the
+            # fold's input streams (the inputs its body names), within
+            # 200 KiB of shared memory for the block's warps
+            ns = max(1, len(exp_names(f.body) & {k for k, sp in self.prog.spaces.items() if sp == "in"}))
+            step = ns * C * W * sb * 32
+            S = max(2, ROW_TMA_STAGES, ROW_TMA_INFLIGHT // step)
             nw = self.launch[1][0] * self.launch[1][1] // 32
-            while S > 2 and nw * S * 2 * C * W * sb * 32 > 200 * 1024:
+            while S > 2 and nw * S * step > 200 * 1024:
                 S -= 1
         if mode != "plain":
             self._k += 1
