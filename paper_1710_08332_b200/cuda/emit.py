@@ -945,6 +945,15 @@ class KernelEmitter:
         buf = target.ref.buf if isinstance(target, VStore) else target.buf
         if self.vec_pf is not None:
             self.vec_pf["written"].add(buf.cname)
+        st = self.prog.stream
+        if st is not None and not self.prog.in_tail and buf.key in st["partials"]:
+            # a streaming tail assumes work-item i writes partial i (round
+            # i / gsize publishes it): any other write index falls back
+            lp = self.loops[0] if self.loops and self.loops[0].level == "global" else None
+            at = None if isinstance(target, VStore) or target.flat is None else \
+                Ix([(m, c) for m, c in target.flat.terms if "dpia_par" not in IX.free_names(Ix([(m, c)]))])
+            if lp is None or at is None or at != ix(lp.var):
+                self.stream_unsafe = True
         if isinstance(target, VStore):
             stmt = (f"dpia::vstore<{self.scalar}, {target.width}>({buf.cname}, "
                     f"{self.r(target.ref.at)}, {rhs});")

@@ -73,7 +73,36 @@ def test_stream_tail_falls_back(monkeypatch):
     assert sig.kernels[0].extra_blocks == 0 and "dpia::grid_arrive(dpia_counter" in src
 
 
+PERMUTED = """
+(param xs (exp (array 1048576 num)))
+(reduce (+) 0 (toGlobal (lam t (join (transpose (split 64 t))))
+  (mapGlobal (lam (c (exp (array 256 num))) (reduce (+) 0 c)) (split 256 xs))))
+"""
+
+
+def test_permuted_partials_do_not_stream():
+    """The partials stored through a layout view (work-item i writes partial
+    64 (i mod 64) + i / 64): a round's partials are not a contiguous prefix,
+    so the streaming tail could read one before its round publishes -- the
+    kernel keeps the last-block ticket."""
+    prog = compile_program(PERMUTED)
+    outs = [("out", prog.out_type)]
+    ins = [(nm, t.data) for nm, t in prog.source.params]
+    src, sig = EM.emit_cuda(prog.imperative, outs, ins, sigma={}, launch=(32, 32))
+    assert sig.kernels[0].extra_blocks == 0 and "dpia::grid_arrive(dpia_counter" in src
+    assert "g_tmp4[64 * ((i_3_1) % 64) + ((i_3_1) / 64)]" in src
+
+
 # ------------------------------------------------------------------ GPU
+
+
+@pytest.mark.gpu
+def test_permuted_partials_int_exact():
+    from paper_1710_08332_b200 import run_program_cuda
+    xs = np.random.default_rng(5).integers(-9, 10, 1048576)
+    got = run_program_cuda(compile_program(PERMUTED), {"xs": xs}, sigma={}, launch=(32, 32),
+                           float_mode=False, flat=True)
+    assert int(got[0]) == int(xs.sum())
 
 def _run(chunk, n, launch, inputs, float_mode, stream=True, rows=True):
     from paper_1710_08332_b200 import executable
