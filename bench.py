@@ -33,7 +33,8 @@ sys.path.insert(0, ROOT)
 from paper_1710_08332_b200 import compile_program, executable  # noqa: E402
 from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, asum_proxy_config, dot_config,  # noqa: E402
-                                                  dot_literal_config, gemv_config, mm_config,
+                                                  dot_literal_config, gemv_config, gemv_literal_config,
+                                                  mm_config,
                                                   mm_tma_config, scal_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
@@ -300,8 +301,8 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
         cfg = dot_literal_config()
         inputs = {"xs": _seeded(1 << 24, 0 + 1000 * rank, 0.0, 1.0),
                   "ys": _seeded(1 << 24, 1 + 1000 * rank, 0.0, 1.0)}
-    elif name in ("gemv", "gemv_xprivate"):
-        cfg = gemv_config(x_private=name == "gemv_xprivate")
+    elif name in ("gemv", "gemv_xprivate", "gemv_literal"):
+        cfg = gemv_literal_config() if name == "gemv_literal" else gemv_config(x_private=name == "gemv_xprivate")
         cfg.name = name
         inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
     elif name == "scal":
@@ -545,6 +546,7 @@ REF_STRATEGY = {
 }
 REF_STRATEGY["dot_literal"] = REF_STRATEGY["dot"]
 REF_STRATEGY["gemv_xprivate"] = REF_STRATEGY["gemv"]
+REF_STRATEGY["gemv_literal"] = REF_STRATEGY["gemv"]
 REF_STRATEGY["mm_tma"] = REF_STRATEGY["mm"]
 REF_STRATEGY["asum_proxy"] = REF_STRATEGY["asum"]
 
@@ -557,7 +559,7 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         return None
     vp, ci = ctypes.c_void_p, ctypes.c_int
     out = np.zeros(8192, np.float32)
-    base = {"mm_tma": "mm", "asum_proxy": "asum"}.get(workload, workload)
+    base = {"mm_tma": "mm", "asum_proxy": "asum", "gemv_literal": "gemv"}.get(workload, workload)
     note = ""
     if workload.startswith("scaleout"):
         # the reference's emitted C indexes with 32-bit int and keeps the
@@ -580,7 +582,7 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         fn.argtypes = [vp, vp, vp, ci]
         call = lambda: fn(out.ctypes.data, xs.ctypes.data, ys.ctypes.data, n)  # noqa: E731
         nbytes, sample = 8 << 24, "dot over 2^24 fp32 pairs, full size"
-    elif base in ("gemv", "gemv_xprivate"):
+    elif base in ("gemv", "gemv_xprivate", "gemv_literal"):
         A, x = _seeded((8192, 8192), 3, -1.0, 1.0), _seeded(8192, 4, -1.0, 1.0)
         fn = lib.gemv
         fn.argtypes = [vp, vp, vp]
@@ -941,7 +943,8 @@ def main():
     # N = 1: every benchmark program; N > 1: the sharded reductions of
     # BASELINE config 5 (2^31 in total, strong scaling) beside the weak-scaled
     # headline -- gemv / mm / scal would only replicate (no exchange step)
-    names = (("dot", "dot_literal", "asum", "asum_proxy", "gemv", "gemv_xprivate", "mm", "mm_tma", "scal",
+    names = (("dot", "dot_literal", "asum", "asum_proxy", "gemv", "gemv_xprivate", "gemv_literal", "mm",
+              "mm_tma", "scal",
               "scaleout_asum", "scaleout_dot") if world == 1 else ("scaleout_asum", "scaleout_dot"))
     if not args.no_suite:
         for w in names:
@@ -1107,6 +1110,9 @@ WORKLOADS = {
              "(shared memory), reduceSeq over vec4 column slices, reduceLocal per row"),
     "gemv_xprivate": ("gemv 8192x8192 fp32", "row per work-group, x staged toPrivate in the "
                       "work-items' column layout (registers), reduceSeq + reduceLocal per row"),
+    "gemv_literal": ("gemv 8192x8192 fp32", "BASELINE config 3 as the reference states it "
+                     "(oracle/ref_programs/gemv.dpia): row per work-group, x toLocal, each work-item "
+                     "folds its own 32-element piece, partial sums toLocal, one work-item folds them"),
     "scal": ("scal N=2^26 fp32 (read + write)", "grid-stride mapGlobal over vec4"),
     "mm": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "128x128 tiles, 8x8 register tiles, toLocal "
            "k-tiles of 16, FFMA2"),

@@ -457,6 +457,31 @@ def asum_proxy_config(N: int = 1 << 26, chunk: int = 1024, L: int = 32, rounds: 
     return Config("asum_proxy", asum_proxy_program(chunk), {"n": n}, (G, L), bytes=4 * N, flops=N)
 
 
+def gemv_literal_program(M: int = 8192, N: int = 8192, L: int = 256) -> str:
+    """BASELINE config 3 exactly as the reference states it
+    (oracle/ref_programs/gemv.dpia): one row per
+    work-group, x staged with toLocal, each of the L work-items folds its own
+    contiguous N/L-element piece of the row, the partial sums are staged with
+    toLocal and one work-item folds them in order."""
+    c = N // L
+    return f"""
+(param A (exp (array {M} (array {N} num))))
+(param x (exp (array {N} num)))
+(join (mapWorkgroup (lam (row (exp (array {N} num)))
+  (mapLocal (lam (ps (exp (array {L} num))) (reduce (+) 0 ps))
+   (split {L} (toLocal (mapLocal (lam (c (exp (array {c} (pair num num))))
+     (reduce (lam (p (exp (pair num num))) (lam (a (exp num)) (+ (* (fst p) (snd p)) a))) 0 c)))
+    (split {c} (zip row (toLocal (mapLocal (lam (v (exp num)) v)) x)))))))
+ A))
+"""
+
+
+def gemv_literal_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int = 148 * 4) -> Config:
+    """One wave of 4 work-groups per SM (profiles/r02c_gemv_literal.txt)."""
+    return Config("gemv_literal", gemv_literal_program(M, N, L), {}, (min(blocks, M), L),
+                  bytes=4 * (M * N + M + N), flops=2 * M * N)
+
+
 def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -487,7 +512,7 @@ def gemv_xprivate_config(**kw) -> Config:
 CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
            "scal": scal_config, "dot_literal": dot_literal_config,
            "gemv_xprivate": gemv_xprivate_config, "mm_tma": mm_tma_config,
-           "asum_proxy": asum_proxy_config}
+           "asum_proxy": asum_proxy_config, "gemv_literal": gemv_literal_config}
 
 
 def aot_sources():

@@ -56,6 +56,8 @@ UNROLL_LIMIT = 64
 # VEC_WIDTH-wide vectors (KernelEmitter._vec_loop); DPIA_VEC_LOADS=0 disables
 VEC_LOADS = os.environ.get("DPIA_VEC_LOADS", "1") != "0"
 VEC_WIDTH = 4
+# also vectorise folds of at most UNROLL_LIMIT iterations (DPIA_VEC_SHORT=0: only longer ones)
+VEC_SHORT = os.environ.get("DPIA_VEC_SHORT", "1") != "0"
 # ... and each read stream of a work-item's fold keeps VEC_PREFETCH queue
 # slots in flight (a rotating register queue refilled VEC_PREFETCH slots
 # ahead; 0 disables).  A slot is one VEC_LOAD_BYTES vector: 32 = one sm_100
@@ -132,6 +134,9 @@ class _ProbeFail(Exception):
 # bank-conflict layout of local buffers whose rows are a multiple of 32
 # scalars (see KernelEmitter._declare_local): swizzle | pad | none
 SMEM_LAYOUT = os.environ.get("DPIA_SMEM_LAYOUT", "swizzle")
+# 1-D shared buffers read at a work-item stride that is a multiple of 32
+# scalars get 4 scalars of padding per 32 (KernelEmitter._declare_local)
+SMEM_PAD_1D = os.environ.get("DPIA_SMEM_PAD_1D", "1") != "0"
 
 
 class NeedLanes(Exception):
@@ -150,6 +155,7 @@ class Buffer:
     sliced: int = 0
     pad: int = 0             # scalars added to the innermost row stride (shared-memory banks)
     swz: Optional[Tuple[int, int, int]] = None   # (unit, div, period): inner ^= unit*((outer/div)%period)
+    pad32: int = 0           # 1-D shared buffer: scalars of padding after every 32 (bank-conflict padding)
 
     @property
     def dims(self):
@@ -522,6 +528,7 @@ class KernelEmitter:
         self.sigma = prog.sigma
         self.slices: Dict[str, int] = {}
         self.promote: Set[str] = set()
+        self.pad32: Set[str] = set()         # 1-D shared buffers to pad (decided by the record pass)
         self.reset()
 
     def reset(self):
@@ -531,6 +538,7 @@ class KernelEmitter:
         self.loops: List[Loop] = []
         self.R: Dict[str, Optional[int]] = {}
         self.records: Dict[str, List] = {}
+        self.local_reads: Dict[str, bool] = {}   # 1-D shared buffer -> read at a 32-multiple work-item stride
         self.recording = False
         self.smem = 0
         self.barriers: Set[int] = set()
@@ -629,6 +637,13 @@ class KernelEmitter:
             self.records.setdefault(buf.key, []).append(
                 (idxs, list(self.loops), self.single_thread, self.decl_depth.get(buf.key, 0)))
         idxs, dims = idxs[buf.sliced:], dims[buf.sliced:]
+        if self.recording and buf.space == "local" and len(dims) == 1 and isinstance(elem, Num):
+            # a work-item index with a coefficient that is a multiple of 32
+            # puts every work-item of a warp in the same bank
+            work = {lp.var for lp in self.loops if lp.level in ("local", "lin") and lp.var}
+            hit = any(len(m) == 1 and IX._ATOMS[m[0]][0] == "v" and IX._ATOMS[m[0]][1] in work
+                      and c % 32 == 0 for m, c in ix(idxs[0]).terms)
+            self.local_reads[buf.key] = self.local_reads.get(buf.key, False) or hit
         flat = addr = None
         if dims:
             flat = Ix()
@@ -640,6 +655,8 @@ class KernelEmitter:
                     mask = mod(div(idxs[last - 1], dv, self.R), per, self.R) * unit
                     addr = flat * ext + self._swizzled(i, mask, unit, per)
                 flat = flat * ext + i
+            if buf.pad32:
+                addr = flat + div(flat, 32, self.R) * buf.pad32
             base = f"{buf.cname}[{self.r(addr if addr is not None else flat)}]"
         else:
             base = buf.cname if buf.space == "private" else f"{buf.cname}[0]"
@@ -826,7 +843,7 @@ class KernelEmitter:
         vector comes from the stream's queue or ring when A mentions no loop
         variable bound inside the fold."""
         if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global") \
-                or r.buf.swz or r.buf.pad or not isinstance(r.buf.elem, Num):
+                or r.buf.swz or r.buf.pad or r.buf.pad32 or not isinstance(r.buf.elem, Num):
             return None
         coef = dict((m, c) for m, c in r.flat.terms)
         js = [v for v, w in self.vec_vars.items() if coef.get((v,)) == w]
@@ -1032,8 +1049,11 @@ class KernelEmitter:
         variant is tried on a scratch copy of the output; False (nothing
         emitted) when no read qualifies."""
         trip = self.nat_int(n)
+        # short folds too (down to 2 vectors): a work-item walking its own
+        # 32-element piece issues 8 LDG.128 instead of 32 scalar loads that
+        # each touch a different cache line of the warp (the reference's gemv)
         if not VEC_LOADS or not self.per_thread or self.pf is not None or trip is None \
-                or trip <= UNROLL_LIMIT:
+                or trip < (2 * VEC_WIDTH if VEC_SHORT else UNROLL_LIMIT + 1):
             return False
         sb = 4 if self.scalar == "float" else 8
         modes = []
@@ -1049,11 +1069,11 @@ class KernelEmitter:
         for mode, W in modes:
             if trip % W:
                 continue
-            mark, ind, hits, smem = len(self.lines), self.ind, self.vec_hits, self.smem
+            mark, ind, hits, smem, k0 = len(self.lines), self.ind, self.vec_hits, self.smem, self._k
             if self._emit_vec_loop(n, f, trip // W, W, mode) and self.vec_hits > hits:
                 return True
             del self.lines[mark:]
-            self.ind, self.smem = ind, smem
+            self.ind, self.smem, self._k = ind, smem, k0   # a failed attempt leaves no trace
         return False
 
     @staticmethod
@@ -1439,6 +1459,13 @@ class KernelEmitter:
             elif SMEM_LAYOUT == "pad":
                 buf.pad = 4
                 n = n // inner * (inner + 4)
+        elif isinstance(elem, Num) and len(dims) == 1 and inner and inner % 32 == 0 and binder in self.pad32:
+            # a 1-D buffer that work-items read at a stride of a multiple of
+            # 32 scalars (each folding its own contiguous piece): 4 scalars of
+            # padding after every 32 put the warp's work-items in distinct
+            # banks, also for 16-byte vectors (element i lives at i + 4 (i / 32))
+            buf.pad32 = 4
+            n = n // 32 * 36
         # 128-byte aligned: the bank arithmetic of the swizzle / padding
         # above assumes each buffer starts in bank 0
         off = self.alloc_smem(n * self._elem_bytes(split_array(full)[1]), align=128)
@@ -1760,7 +1787,7 @@ class KernelEmitter:
         a copy loop over the work-items.  Used for the block-invariant
         stagings (hoisted out of the work-group loop).  False when the
         pattern, the sizes or the alignment do not fit (the loop is emitted)."""
-        if not BULK_STAGE or buf.swz is not None or buf.pad or buf.prefix:
+        if not BULK_STAGE or buf.swz is not None or buf.pad or buf.pad32 or buf.prefix:
             return False
         u = unapply(c1)
         if u is None or u[0] not in ("parforLocal", "parfor") or len(u[2]) != 2:
@@ -2459,6 +2486,7 @@ class ProgramEmitter:
                     ke.slices, ke.promote = self._decide_slices(ke)
                     for key in ke.promote:
                         self.spaces[key] = "local"
+                    ke.pad32 = {k for k, hit in ke.local_reads.items() if hit} if SMEM_PAD_1D else set()
                 body_lines = ke.lines
             if stream is None or (stream["waits"] and not ke.stream_unsafe):
                 break

@@ -83,7 +83,7 @@ def test_asum_fp32_vs_reference_interpreter():
     assert abs(got[0] - want) <= TOL * want, (got[0], want)
 
 
-@pytest.mark.parametrize("workload", ["gemv", "gemv_xprivate"])
+@pytest.mark.parametrize("workload", ["gemv", "gemv_xprivate", "gemv_literal"])
 def test_gemv_fp32_vs_reference_interpreter(workload):
     """config 3 (toLocal x) and the toPrivate variant: all 8192 rows."""
     g = golden("gemv_f32")
@@ -118,7 +118,7 @@ def test_asum_vs_reference_c_path():
 
 
 @needs_ref
-@pytest.mark.parametrize("workload", ["gemv", "gemv_xprivate"])
+@pytest.mark.parametrize("workload", ["gemv", "gemv_xprivate", "gemv_literal"])
 def test_gemv_vs_reference_c_path(workload):
     A, x = blas_np.seeded((8192, 8192), 3, -1.0, 1.0), blas_np.seeded(8192, 4, -1.0, 1.0)
     got = run(workload, {"A": A, "x": x})

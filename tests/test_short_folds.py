@@ -1,0 +1,46 @@
+"""Two general emitter choices that the reference's own gemv program
+(BASELINE config 3 as the reference states it, oracle/ref_programs/gemv.dpia)
+exposed: each of its work-items folds its own contiguous 32-element piece of
+a row against the shared copy of x.
+
+* 1-D shared buffers read at a work-item stride that is a multiple of 32
+  scalars are padded by 4 scalars per 32 (`SMEM_PAD_1D`): work-item t's
+  element j sits at 36 t + j instead of 32 t + j, so a warp's 32 work-items
+  hit 32 different banks (scalar loads) or 8 different 16-byte bank groups
+  per quarter warp (vector loads);
+* short folds (down to 2 vectors) over unit-stride global data read whole
+  vectors (`VEC_SHORT`): 4 32-byte loads per work-item piece instead of 32
+  scalar loads each touching a different cache line of the warp.
+
+CPU: the emitted indices; the B200 gemv (coalesced reads of x) keeps its
+unpadded buffer and its TMA bulk copy.  GPU (test_gpu_reference_parity):
+the reference program's results against the reference's interpreter and C.
+"""
+from paper_1710_08332_b200 import compile_program
+from paper_1710_08332_b200.bench_programs import gemv_config, gemv_literal_config
+from paper_1710_08332_b200.cuda import emit as EM
+
+
+def _emit(cfg):
+    prog = compile_program(cfg.text)
+    outs = [("out", prog.out_type)]
+    ins = [(nm, t.data) for nm, t in prog.source.params]
+    src, sig = EM.emit_cuda(prog.imperative, outs, ins, sigma=cfg.sigma, launch=cfg.launch)
+    return src.split('extern "C"')[1], sig
+
+
+def test_reference_gemv_pads_x_and_vectorises_the_pieces():
+    body, _ = _emit(gemv_literal_config())
+    assert "[4 * ((i_1_2) / 32) + i_1_2] = x[i_1_2];" in body        # padded staging copy
+    assert "tmp16_1[36 * i_5_6 + 8 * j_9]" in body                     # work-item stride 36
+    assert "dpia::vload32<true>(A, 8192 * i_11_3 + 32 * i_5_6 + 8 * j_9)" in body
+    assert "dpia::bulk_stage(" not in body                             # a padded buffer is copied by the work-items
+
+
+def test_switches_and_the_b200_gemv_unchanged(monkeypatch):
+    body, _ = _emit(gemv_config())
+    assert "dpia::bulk_stage(" in body and "36 *" not in body
+    monkeypatch.setattr(EM, "SMEM_PAD_1D", False)
+    monkeypatch.setattr(EM, "VEC_SHORT", False)
+    body, _ = _emit(gemv_literal_config())
+    assert "36 * i_5_6" not in body and "vload32" not in body and "dpia::bulk_stage(" in body
