@@ -558,6 +558,7 @@ class KernelEmitter:
         self.vec_vars: Dict[str, int] = {}   # loop counter -> lane width of an unrolled fold
         self.vec_hits = 0
         self.vec_pf: Optional[dict] = None   # the innermost prefetching fold (`_vec_loop`)
+        self.lane_stores: Optional[list] = None   # scalar stores of the current vectorised lane
         self.probing = False                 # `_tma_plan`: enumerate and record, emit nothing
         self.probe_recs: List[tuple] = []
         self.probe_src: Optional[tuple] = None
@@ -978,6 +979,9 @@ class KernelEmitter:
             stmt = f"{target.text} = {rhs};"
         if buf.space != "private" and not self.per_thread:
             stmt = f"if (dpia_tid == 0) {stmt}"
+        if self.lane_stores is not None and not isinstance(target, VStore) and target.flat is not None \
+                and not target.suffix and target.addr is None:
+            self.lane_stores.append((buf, target.flat, rhs, stmt))
         self.line(stmt)
 
     # --------------------------------------------------------- commands
@@ -1178,11 +1182,17 @@ class KernelEmitter:
         self.loops.append(Loop("seq", 0, j, T, nat(T), False))
         old = self.env.get(f.binder)
         try:
+            lanes, outer_stores = [], self.lane_stores
             for k in range(W):
+                self.lane_stores = []
+                at = len(self.lines)
                 self.open("")
                 self.env[f.binder] = Val(Idx(n), ixv=ix(j) * W + k)
                 self.comm(f.body)
                 self.close()
+                lanes.append((at, len(self.lines), self.lane_stores))
+            self.lane_stores = outer_stores
+            self._merge_lane_stores(lanes, W)
         finally:
             self.loops.pop()
             self.vec_vars.pop(j, None)
@@ -1218,6 +1228,34 @@ class KernelEmitter:
         pro.append(f"{pad}}}")
         self.lines[top:top] = pro
         return True
+
+    def _merge_lane_stores(self, lanes, W: int):
+        """The W lanes of a vectorised fold iteration that each store one
+        scalar to W consecutive elements of a global buffer (a work-item
+        writing its own contiguous piece: the reference's scal) become one
+        W-wide vector store, when each lane's code is nothing but that
+        store and the first element is W-aligned."""
+        recs = []
+        for at, end, stores in lanes:
+            body = [ln.strip() for ln in self.lines[at:end]]
+            if len(stores) != 1 or len(body) != 3 or body[0] != "{" or body[2] != "}":
+                return
+            buf, flat, rhs, text = stores[0]
+            if body[1] != text:
+                return
+            recs.append((buf, flat, rhs))
+        buf0, f0, _ = recs[0]
+        if buf0.space not in ("out", "global") or buf0.swz or buf0.pad or buf0.pad32 or \
+                not isinstance(buf0.elem, Num) or any(c % W for _, c in f0.terms):
+            return
+        for k, (buf, flat, _) in enumerate(recs):
+            if buf is not buf0 or flat != f0 + k:
+                return
+        vals = ", ".join(rhs for _, _, rhs in recs)
+        stmt = (f"dpia::vstore<{self.scalar}, {W}>({buf0.cname}, {self.r(f0)}, "
+                f"dpia::vec<{self.scalar}, {W}>{{{{{vals}}}}});")
+        pad = "  " * self.ind
+        self.lines[lanes[0][0]:lanes[-1][1]] = [pad + stmt]
 
     def _rows_loop(self) -> Optional[Loop]:
         """The enclosing mapGlobal loop when a fold here can use row boxes:
