@@ -35,7 +35,7 @@ from paper_1710_08332_b200 import runtime as RT  # noqa: E402
 from paper_1710_08332_b200.bench_programs import (asum_config, asum_proxy_config, dot_config,  # noqa: E402
                                                   dot_literal_config, gemv_config, gemv_literal_config,
                                                   mm_config,
-                                                  mm_tma_config, scal_config)
+                                                  mm_tma_config, scal_config, scal_literal_config)
 
 METRIC = "achieved HBM GB/s (dot/asum/gemv), GFLOP/s (mm) vs roofline, at 1-8 B200"
 
@@ -305,9 +305,11 @@ def make_workload(name, device, rank=0, world=1, combine="nccl"):
         cfg = gemv_literal_config() if name == "gemv_literal" else gemv_config(x_private=name == "gemv_xprivate")
         cfg.name = name
         inputs = {"A": _seeded((8192, 8192), 3, -1.0, 1.0), "x": _seeded(8192, 4, -1.0, 1.0)}
-    elif name == "scal":
-        cfg = scal_config()
-        inputs = {"alpha": np.full(4, 1.5, np.float32), "xs": _seeded(1 << 26, 7, -1.0, 1.0)}
+    elif name in ("scal", "scal_literal"):
+        cfg = scal_config() if name == "scal" else scal_literal_config()
+        # alpha: a splat vec4 in the B200 program, a scalar in the reference's
+        inputs = {"alpha": np.full(4 if name == "scal" else 1, 1.5, np.float32),
+                  "xs": _seeded(1 << 26, 7, -1.0, 1.0)}
     elif name in ("mm", "mm_tma"):
         cfg = mm_config() if name == "mm" else mm_tma_config()
         inputs = {"A": _seeded((4096, 4096), 5, -1.0, 1.0), "B": _seeded((4096, 4096), 6, -1.0, 1.0)}
@@ -547,6 +549,7 @@ REF_STRATEGY = {
 REF_STRATEGY["dot_literal"] = REF_STRATEGY["dot"]
 REF_STRATEGY["gemv_xprivate"] = REF_STRATEGY["gemv"]
 REF_STRATEGY["gemv_literal"] = REF_STRATEGY["gemv"]
+REF_STRATEGY["scal_literal"] = REF_STRATEGY["scal"]
 REF_STRATEGY["mm_tma"] = REF_STRATEGY["mm"]
 REF_STRATEGY["asum_proxy"] = REF_STRATEGY["asum"]
 
@@ -559,7 +562,8 @@ def cpu_reference(workload, min_seconds=2.0, max_reps=200, steps=None, warmup=1)
         return None
     vp, ci = ctypes.c_void_p, ctypes.c_int
     out = np.zeros(8192, np.float32)
-    base = {"mm_tma": "mm", "asum_proxy": "asum", "gemv_literal": "gemv"}.get(workload, workload)
+    base = {"mm_tma": "mm", "asum_proxy": "asum", "gemv_literal": "gemv",
+            "scal_literal": "scal"}.get(workload, workload)
     note = ""
     if workload.startswith("scaleout"):
         # the reference's emitted C indexes with 32-bit int and keeps the
@@ -944,7 +948,7 @@ def main():
     # BASELINE config 5 (2^31 in total, strong scaling) beside the weak-scaled
     # headline -- gemv / mm / scal would only replicate (no exchange step)
     names = (("dot", "dot_literal", "asum", "asum_proxy", "gemv", "gemv_xprivate", "gemv_literal", "mm",
-              "mm_tma", "scal",
+              "mm_tma", "scal", "scal_literal",
               "scaleout_asum", "scaleout_dot") if world == 1 else ("scaleout_asum", "scaleout_dot"))
     if not args.no_suite:
         for w in names:
@@ -1114,6 +1118,9 @@ WORKLOADS = {
                      "(oracle/ref_programs/gemv.dpia): row per work-group, x toLocal, each work-item "
                      "folds its own 32-element piece, partial sums toLocal, one work-item folds them"),
     "scal": ("scal N=2^26 fp32 (read + write)", "grid-stride mapGlobal over vec4"),
+    "scal_literal": ("scal N=2^26 fp32 (read + write)", "the paper's scal as the reference states it "
+                     "(oracle/ref_programs/scal.dpia): mapGlobal over 1024-element chunks, each work-item "
+                     "scaling its own chunk (TMA row reads, vector stores)"),
     "mm": ("mm 4096^3 fp32 (FFMA, no tensor cores)", "128x128 tiles, 8x8 register tiles, toLocal "
            "k-tiles of 16, FFMA2"),
     "asum_proxy": ("asum proxy N=2^26 fp32 (the reference arm's program: sum, no abs)",

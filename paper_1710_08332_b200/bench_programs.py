@@ -482,6 +482,26 @@ def gemv_literal_config(M: int = 8192, N: int = 8192, L: int = 256, blocks: int 
                   bytes=4 * (M * N + M + N), flops=2 * M * N)
 
 
+def scal_literal_program(chunk: int = 1024) -> str:
+    """The paper's fourth BLAS kernel as the reference states it
+    (oracle/ref_programs/scal.dpia): a mapGlobal over `chunk`-element pieces,
+    each work-item scaling its own piece sequentially (read + write)."""
+    return f"""
+(nat n)
+(param alpha (exp num))
+(param xs (exp (array (* n {chunk}) num)))
+(join (mapGlobal (lam (c (exp (array {chunk} num))) (mapSeq (lam x (* alpha x)) c)) (split {chunk} xs)))
+"""
+
+
+def scal_literal_config(N: int = 1 << 26, chunk: int = 1024, L: int = 32, rounds: int = 8) -> Config:
+    """Work-items read their pieces through TMA row boxes and write them with
+    vector stores (profiles/r02c_scal_literal.txt)."""
+    n = N // chunk
+    G = max(1, n // (L * rounds)) if n % (L * rounds) == 0 else max(1, n // L)
+    return Config("scal_literal", scal_literal_program(chunk), {"n": n}, (G, L), bytes=8 * N, flops=N)
+
+
 def asum_config(N: int = 1 << 26, L: int = 1024, K: int = 64, blocks=None) -> Config:
     per_wg = 4 * K * L
     assert N % per_wg == 0
@@ -512,7 +532,8 @@ def gemv_xprivate_config(**kw) -> Config:
 CONFIGS = {"dot": dot_config, "asum": asum_config, "gemv": gemv_config, "mm": mm_config,
            "scal": scal_config, "dot_literal": dot_literal_config,
            "gemv_xprivate": gemv_xprivate_config, "mm_tma": mm_tma_config,
-           "asum_proxy": asum_proxy_config, "gemv_literal": gemv_literal_config}
+           "asum_proxy": asum_proxy_config, "gemv_literal": gemv_literal_config,
+           "scal_literal": scal_literal_config}
 
 
 def aot_sources():

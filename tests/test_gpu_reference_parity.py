@@ -234,3 +234,14 @@ def test_literal_programs_vs_reference_c_path(workload, slots):
         want = ref_cpu.dot(inp["xs"], inp["ys"])
         _, absterms = blas_np.dot(inp["xs"], inp["ys"])
         assert abs(got[0] - want) <= TOL * absterms, (got[0], want)
+
+
+@needs_ref
+def test_scal_literal_bit_identical_to_reference_c_path():
+    """The paper's scal as the reference states it (one work-item per
+    1024-element chunk): TMA row reads and merged vector stores give the
+    reference C path's bits (one multiply per element)."""
+    xs = blas_np.seeded(1 << 26, 7, -1.0, 1.0)
+    got = run("scal_literal", {"alpha": np.float32([1.5]), "xs": xs})
+    want = ref_cpu.scal(1.5, xs)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -44,3 +44,15 @@ def test_switches_and_the_b200_gemv_unchanged(monkeypatch):
     monkeypatch.setattr(EM, "VEC_SHORT", False)
     body, _ = _emit(gemv_literal_config())
     assert "36 * i_5_6" not in body and "vload32" not in body and "dpia::bulk_stage(" in body
+
+
+def test_reference_scal_stores_whole_vectors(monkeypatch):
+    """A work-item writing its own contiguous piece: the W lanes' scalar
+    stores of one vectorised iteration are one W-wide vector store."""
+    from paper_1710_08332_b200.bench_programs import scal_literal_config
+    body, _ = _emit(scal_literal_config())
+    assert "dpia::vstore<float, 4>(out, 1024 * i_" in body and "out[1024 *" not in body
+    assert "dpia::tma_tile_2d(" in body                                # row-box reads
+    monkeypatch.setattr(EM, "VEC_LOADS", False)
+    body, _ = _emit(scal_literal_config())
+    assert "dpia::vstore<float, 4>(out" not in body
