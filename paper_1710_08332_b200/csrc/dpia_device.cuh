@@ -385,9 +385,14 @@ __device__ __forceinline__ void ring_wait(unsigned long long* mb, unsigned parit
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// TRIGGER: let the dependent launch once the previous grid has completed
+// (at most two launches resident; the kernel did not trigger at its top).
+// A block that never waits triggers when it exits.
+template <bool TRIGGER = false>
 __device__ __forceinline__ void pdl_wait_once(bool& pending) {
   if (pending) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     pending = false;
   }
 }

@@ -75,6 +75,10 @@ TAIL_RING = os.environ.get("DPIA_TAIL_RING", "1") != "0"
 # it waits for that grid only before touching non-input global memory
 # (ProgramEmitter._chain_waits); DPIA_CHAIN=0 emits no chaining code.
 CHAIN = os.environ.get("DPIA_CHAIN", "1") != "0"
+# where a chained first kernel lets its dependent launch: "top" (at once),
+# "wait" (after its first wait for the previous grid) or "auto" (ProgramEmitter
+# .emit_kernel: "wait" for small grids that store outputs, else "top")
+CHAIN_TRIGGER = os.environ.get("DPIA_CHAIN_TRIGGER", "auto")
 TAIL_RING_STAGES = int(os.environ.get("DPIA_TAIL_RING_STAGES", "4"))
 TAIL_RING_BYTES = int(os.environ.get("DPIA_TAIL_RING_BYTES", "2048"))
 TAIL_RING_UNROLL = int(os.environ.get("DPIA_TAIL_RING_UNROLL", "16"))
@@ -2605,10 +2609,28 @@ class ProgramEmitter:
             # lets its own dependent launch early, streams its inputs at once
             # and waits for that grid only before it first touches memory the
             # grid may still use (`_chain_waits`); all no-ops when not chained
-            head.append("  dpia::pdl_trigger();")
+            # Trigger placement.  At once by default: the dependent launch is
+            # scheduled while this one drains.  A small grid (under half the
+            # B200's 148 x 2048 resident threads) whose grid phase writes an
+            # output instead triggers right after its first wait for the
+            # previous grid (`dpia::pdl_wait_once<true>`), so at most two
+            # launches are resident: otherwise the SMs fill with blocks of
+            # later launches waiting to store (the reference's scal: chained
+            # 2.4x slower than unchained; the large grids and the reductions
+            # lose 1-10 % with the late trigger, `profiles/r02c_chain_trigger.txt`).
+            # A slot-pipelined streaming tail always triggers at once.
+            L_ = self.launch
+            small = L_ is not None and L_[0][0] * L_[0][1] * L_[1][0] * L_[1][1] < 148 * 1024
+            writes_out = grid is not None and bool(rw_sets(grid)[1] & {nm for nm, _ in self.outputs})
+            late = not pipe and (CHAIN_TRIGGER == "wait" or (CHAIN_TRIGGER == "auto" and small and writes_out))
+            if not late:
+                head.append("  dpia::pdl_trigger();")
             head.append("  bool dpia_chained = true;")
             if not pipe:
                 body_lines = self._chain_waits(body_lines, args)
+                if late:
+                    body_lines = [ln.replace("dpia::pdl_wait_once(dpia_chained);",
+                                             "dpia::pdl_wait_once<true>(dpia_chained);") for ln in body_lines]
         if ke.uses_gid or stream is not None:
             wide = not L or L[0][0] * L[0][1] * L[1][0] * L[1][1] > IX.INT32_MAX
             it = "long long" if wide else "int"
