@@ -11,7 +11,8 @@ import pytest
 from paper_1710_08332_b200 import compile_program, executable
 from paper_1710_08332_b200 import runtime as RT
 from paper_1710_08332_b200.bench_programs import (asum_config, dot_config, dot_literal_config,
-                                                  gemv_config, mm_config, scal_config)
+                                                  gemv_config, mm_config, scal_config,
+                                                  scal_literal_config)
 
 pytestmark = pytest.mark.gpu
 
@@ -27,6 +28,7 @@ def _cases():
         ("gemv", gemv_config(M=512, N=1024), {"A": 512 * 1024, "x": 1024}),
         ("gemv_xprivate", gemv_config(M=512, N=1024, x_private=True), {"A": 512 * 1024, "x": 1024}),
         ("scal", scal_config(N=1 << 20), {"xs": 1 << 20}),
+        ("scal_literal", scal_literal_config(N=1 << 22), {"xs": 1 << 22}),
         ("mm", mm_config(M=256, N=256, K=256), {"A": 256 * 256, "B": 256 * 256}),
     ]
 
@@ -83,7 +85,7 @@ def test_chained_steps_match_unchained_launches(name, cfg, shapes):
     exe = executable(compile_program(cfg.text, name=name.split("_")[0]), cfg.launch, cfg.sigma,
                      float_mode=True)
     if "alpha" in dict(exe.sig.inputs):
-        shapes = dict(shapes, alpha=4)
+        shapes = dict(shapes, alpha=4 if name == "scal" else 1)
     _run_chained(exe, shapes, 12, np.random.default_rng(7))
 
 

@@ -56,3 +56,15 @@ def test_reference_scal_stores_whole_vectors(monkeypatch):
     monkeypatch.setattr(EM, "VEC_LOADS", False)
     body, _ = _emit(scal_literal_config())
     assert "dpia::vstore<float, 4>(out" not in body
+
+
+def test_chain_trigger_placement():
+    """A small grid whose grid phase stores outputs (the reference's scal)
+    lets its dependent launch only after its first wait for the previous
+    grid; the large grids and the reductions trigger at once."""
+    from paper_1710_08332_b200.bench_programs import dot_config, mm_config, scal_literal_config
+    body, _ = _emit(scal_literal_config())
+    assert "dpia::pdl_trigger();" not in body and "dpia::pdl_wait_once<true>(dpia_chained);" in body
+    for cfg in (dot_config(), mm_config()):
+        body, _ = _emit(cfg)
+        assert "dpia::pdl_trigger();" in body and "pdl_wait_once<true>" not in body
