@@ -494,9 +494,10 @@ def scal_literal_program(chunk: int = 1024) -> str:
 """
 
 
-def scal_literal_config(N: int = 1 << 26, chunk: int = 1024, L: int = 32, rounds: int = 8) -> Config:
-    """Work-items read their pieces through TMA row boxes and write them with
-    vector stores (profiles/r02c_scal_literal.txt)."""
+def scal_literal_config(N: int = 1 << 26, chunk: int = 1024, L: int = 32, rounds: int = 1) -> Config:
+    """Work-items read their pieces through TMA row boxes and write them
+    through TMA row stores; one work-item per chunk (2048 x 32) is fastest
+    with the stores (profiles/r02c_scal_literal.txt)."""
     n = N // chunk
     G = max(1, n // (L * rounds)) if n % (L * rounds) == 0 else max(1, n // L)
     return Config("scal_literal", scal_literal_program(chunk), {"n": n}, (G, L), bytes=8 * N, flops=N)

@@ -478,6 +478,33 @@ __device__ __forceinline__ void tma_tile_2d(void* dst, const TensorMap* map, int
       : "memory");
 }
 
+// TMA tensor store of a 2-D box from shared memory (the work-item row
+// stores of `_finish_rows`): the writers fence their generic-proxy stores to
+// the slot for the async proxy and sync; one thread issues the copy into the
+// bulk async-group, commits, and waits on the group (.read: the slot may be
+// rewritten; plain: the global writes are complete) before the slot is reused
+// or the block ends.
+__device__ __forceinline__ void tma_store_2d(const TensorMap* map, int x, int y, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+      ::"l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y),
+        "r"(static_cast<unsigned>(__cvta_generic_to_shared(src)))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_shared() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void grid_reset(unsigned int* counter, int tid) {
   if (tid == 0) *counter = 0u;
 }

@@ -125,6 +125,9 @@ ROW_TMA = os.environ.get("DPIA_ROW_TMA", "1") != "0"
 ROW_TMA_STAGES = int(os.environ.get("DPIA_ROW_TMA_STAGES", "4"))
 ROW_TMA_BOXES = int(os.environ.get("DPIA_ROW_TMA_BOXES", "2"))    # 128-byte box columns per step
 ROW_TMA_INFLIGHT = int(os.environ.get("DPIA_ROW_TMA_INFLIGHT", str(32 * 1024)))  # bytes per warp (64 KiB measured slower)
+# a row fold's merged vector stores to an output leave through TMA tensor
+# stores of the warp's rows (KernelEmitter._finish_rows)
+ROW_TMA_STORE = os.environ.get("DPIA_ROW_TMA_STORE", "1") != "0"
 # slices of a TMA-staged tile: 2 -- iteration k+1's box is issued right after
 # iteration k's CTA barrier; 3 -- it is issued at the top of iteration k, into
 # the slice iteration k-2 read (free since iteration k-1's barrier)
@@ -1214,7 +1217,7 @@ class KernelEmitter:
         if mode == "ring":
             return self._finish_ring(streams, top, slot_at, take, T, W, C, S, j, jo, jd, rs, mb)
         if mode == "rows":
-            return self._finish_rows(streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0)
+            return self._finish_rows(streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0, pf)
         self.close()
         pad = "  " * self.ind
         pad_in = pad + "    "
@@ -1260,6 +1263,9 @@ class KernelEmitter:
                 f"dpia::vec<{self.scalar}, {W}>{{{{{vals}}}}});")
         pad = "  " * self.ind
         self.lines[lanes[0][0]:lanes[-1][1]] = [pad + stmt]
+        if self.vec_pf is not None:
+            # a rows-mode fold may turn it into a TMA row store (`_finish_rows`)
+            self.vec_pf.setdefault("stores", []).append((buf0, f0, vals, stmt))
 
     def _rows_loop(self) -> Optional[Loop]:
         """The enclosing mapGlobal loop when a fold here can use row boxes:
@@ -1274,7 +1280,7 @@ class KernelEmitter:
             return None
         return lp
 
-    def _finish_rows(self, streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0) -> bool:
+    def _finish_rows(self, streams, top, slot_at, take, T, W, C, S, j, ru, rs, mb, u0, pf=None) -> bool:
         """Complete a rows-mode fold (see `_vec_loop`).  Stream s reads
         X_s[coef * i + c_s + W * j'] for work-item i: X_s viewed as rows of
         coef elements, the warp's work-items are 32 consecutive rows, and
@@ -1312,10 +1318,39 @@ class KernelEmitter:
         NS = len(specs)
         slot_bytes = NS * NB * 4096
         nw = nthreads // 32
-        if nw * S * slot_bytes > 200 * 1024:
-            return False
+        # row stores: the fold's merged vector stores to an output at
+        # coef * i + c + W * j' (a work-item writing its own contiguous piece)
+        # go through SO shared-memory slots and leave as TMA tensor stores of
+        # the warp's 32 rows
+        SO = 2
+        pf = pf or {}
+        stores = []
+        for buf, f0, vals, stmt in pf.get("stores", []) if ROW_TMA_STORE else []:
+            coef = {m: c for m, c in f0.terms}
+            NX = self._elements(buf.dtype)
+            if buf.space != "out" or buf.prefix or buf.swz or buf.pad or buf.pad32 or \
+                    not isinstance(buf.elem, Num) or set(coef) - {(j,), (iv,), ()} or \
+                    coef.get((j,)) != W or (iv,) not in coef or NX is None:
+                stores = None
+                break
+            P, c0 = coef[(iv,)], coef.get((), 0)
+            if P <= 0 or NX % P or (P * sb) % 16 or c0 < 0 or c0 + T * W > P or NX // P < n:
+                stores = None
+                break
+            tm = self.prog.add_tmap({"X": buf, "eb": sb, "NX": NX, "P": P, "rows": 32, "parts": 1,
+                                     "C": VB * W, "swizzle": 128})
+            if tm not in self.tmaps_used:
+                self.tmaps_used.append(tm)
+            stores.append((buf, tm, c0, vals, stmt))
+        so_bytes = len(stores or []) * NB * 4096
+        if nw * (S * slot_bytes + SO * so_bytes) > 200 * 1024:
+            if nw * S * slot_bytes > 200 * 1024:
+                return False
+            stores = None
+        stores = stores or []
         soff = self.alloc_smem(nw * S * slot_bytes, align=1024)
         self.smem_1k = True
+        ooff = self.alloc_smem(nw * SO * so_bytes, align=1024) if stores else 0
         moff = self.alloc_smem(nw * S * 8, align=8)
         lane, sw, st, row0, rnd = (self.fresh(x) for x in ("wlane", "wsw", "wst", "wrow0", "wround"))
         jd = f"({j} % {C})"
@@ -1326,10 +1361,23 @@ class KernelEmitter:
         self.lines[take:take] = [
             f"{pad2}const {vt} {name} = dpia::vload<{self.scalar}, {W}>({name}_s + {jd} / {VB} * {box_elems}, "
             f"{W} * ({jd} % {VB} ^ {sw}));" for name, _tm, _c0 in specs]
+        ost = self.fresh("wos") if stores else None
+        for k, (buf, tm, c0, vals, stmt) in enumerate(stores):
+            at = next(q for q in range(take, len(self.lines)) if self.lines[q].strip() == stmt)
+            ind = self.lines[at][:len(self.lines[at]) - len(self.lines[at].lstrip())]
+            self.lines[at] = (f"{ind}dpia::vstore<{self.scalar}, {W}>(reinterpret_cast<{self.scalar}*>"
+                              f"({ost} + ({ru} % {SO}) * {so_bytes} + {k * NB * 4096} + {lane} * 128) + "
+                              f"{jd} / {VB} * {box_elems}, {W} * ({jd} % {VB} ^ {sw}), "
+                              f"dpia::vec<{self.scalar}, {W}>{{{{{vals}}}}});")
         self.lines[slot_at:slot_at] = [
             f"{pad1}const {self.scalar}* {name}_s = reinterpret_cast<const {self.scalar}*>"
             f"({st} + {rs} * {slot_bytes} + {k * NB * 4096} + {lane} * 128);"
             for k, (name, _tm, _c0) in enumerate(specs)]
+        if stores:
+            # the store slot this step fills was last read by the TMA store
+            # of step ru - SO
+            self.lines[slot_at:slot_at] = [f"{pad1}if ({lane} == 0) dpia::bulk_wait_read<{SO - 1}>();",
+                                           f"{pad1}__syncwarp();"]
 
         def issue(p, u):
             """lane 0: fill step u's slot (step u % steps of round u / steps)
@@ -1345,10 +1393,28 @@ class KernelEmitter:
             out += [f"{p}  }}", f"{p}}}"]
             return out
 
+        if stores:
+            self.line("dpia::fence_async_shared();")
         self.line("__syncwarp();")
+        if stores:
+            # lane 0 writes the step's rows of each stored output (the line
+            # names the output, so a chained kernel waits for its previous
+            # grid first: `_chain_waits`)
+            self.open(f"if ({lane} == 0)")
+            self.line(f"const int wc_ = ({ru} % {steps}) * {C * W};")
+            self.line(f"const int wr_ = (int)({row0} + (long long)({ru} / {steps}) * dpia_gsize);")
+            for k, (buf, tm, c0, vals, stmt) in enumerate(stores):
+                for bb in range(NB):
+                    self.line(f"dpia::tma_store_2d(&{tm}, {c0 + bb * VB * W} + wc_, wr_, {ost} + ({ru} % {SO}) * "
+                              f"{so_bytes} + {(k * NB + bb) * 4096});  /* {buf.cname} */")
+            self.line("dpia::bulk_commit();")
+            self.close()
         self.line(f"if ({lane} == 0)")
         self.lines += issue(pad1, f"{ru} + {S}")
         self.close()
+        if stores:
+            # the fold's last row stores are complete before the warp moves on
+            self.line(f"if ({lane} == 0) dpia::bulk_wait_all();")
         pad = "  " * self.ind
         rexpr = "0" if lp.single else f"(int)(({iv} - dpia_gid) / dpia_gsize)"
         warp = "(dpia_tid >> 5)"
@@ -1356,6 +1422,7 @@ class KernelEmitter:
                f"{pad}unsigned long long* {mb} = reinterpret_cast<unsigned long long*>(dpia_smem + {moff})"
                f" + {warp} * {S};",
                f"{pad}unsigned char* {st} = dpia_smem + {soff} + {warp} * {S * slot_bytes};",
+               *([f"{pad}unsigned char* {ost} = dpia_smem + {ooff} + {warp} * {SO * so_bytes};"] if stores else []),
                f"{pad}const int {rnd} = {rexpr};",
                f"{pad}const int {u0} = {rnd} * {steps};",
                f"{pad}const long long {row0} = (long long)dpia_gid - {lane};",

@@ -46,13 +46,20 @@ def test_switches_and_the_b200_gemv_unchanged(monkeypatch):
     assert "36 * i_5_6" not in body and "vload32" not in body and "dpia::bulk_stage(" in body
 
 
-def test_reference_scal_stores_whole_vectors(monkeypatch):
+def test_reference_scal_stores_whole_vectors_and_tma_rows(monkeypatch):
     """A work-item writing its own contiguous piece: the W lanes' scalar
-    stores of one vectorised iteration are one W-wide vector store."""
+    stores of one vectorised iteration are one W-wide vector store; inside a
+    row fold those go to a shared-memory slot that leaves as TMA tensor
+    stores of the warp's 32 rows (a tensor map over the output)."""
     from paper_1710_08332_b200.bench_programs import scal_literal_config
+    body, sig = _emit(scal_literal_config())
+    assert "dpia::tma_tile_2d(" in body and "dpia::tma_store_2d(&dpia_tm1" in body
+    assert "dpia::fence_async_shared();" in body and "dpia::bulk_wait_read<1>();" in body
+    assert sig.tmaps["dpia_tm1"] == ("out", 4, 65536, 1024, 4096, 32, 32, 128)
+    assert "out[1024 *" not in body
+    monkeypatch.setattr(EM, "ROW_TMA_STORE", False)
     body, _ = _emit(scal_literal_config())
-    assert "dpia::vstore<float, 4>(out, 1024 * i_" in body and "out[1024 *" not in body
-    assert "dpia::tma_tile_2d(" in body                                # row-box reads
+    assert "dpia::vstore<float, 4>(out, 1024 * i_" in body and "tma_store_2d(&" not in body
     monkeypatch.setattr(EM, "VEC_LOADS", False)
     body, _ = _emit(scal_literal_config())
     assert "dpia::vstore<float, 4>(out" not in body
