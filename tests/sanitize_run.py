@@ -131,6 +131,18 @@ def main():
     want = float(np.dot(xs.astype(np.float64), ys.astype(np.float64)))
     assert abs(got - want) <= 1e-4 * want, (got, want)
     print("ok dot_literal streaming tail + TMA row folds", flush=True)
+    from paper_1710_08332_b200.bench_programs import scal_literal_config
+    c = scal_literal_config(N=1 << 20)
+    exe = executable(compile_program(c.text), c.launch, c.sigma, float_mode=True)
+    xs = rng.uniform(-1, 1, 1 << 20).astype(np.float32)
+    exe.upload("alpha", np.float32([1.5]), st)
+    exe.upload("xs", xs, st)
+    for k in range(3):
+        exe.launch(st, chain=k > 0)
+    got = np.asarray(exe.download("out", st))
+    st.sync()
+    assert np.array_equal(got, np.float32(1.5) * xs), "scal_literal"
+    print("ok scal_literal TMA row reads + row stores", flush=True)
     c = mm_config(M=256, N=128, K=256, T=128, BK=16, R=8)
     exe = executable(compile_program(c.text), c.launch, {}, float_mode=False, tma_tiles=True)
     assert exe.sig.tmaps, "TMA k-tiles"
