@@ -58,6 +58,9 @@ VEC_LOADS = os.environ.get("DPIA_VEC_LOADS", "1") != "0"
 VEC_WIDTH = 4
 # also vectorise folds of at most UNROLL_LIMIT iterations (DPIA_VEC_SHORT=0: only longer ones)
 VEC_SHORT = os.environ.get("DPIA_VEC_SHORT", "1") != "0"
+# ... and read shared-memory operands of such folds as whole vectors too
+# (LDS.128: the single-thread fold of a work-group's staged partials)
+VEC_LOCAL = os.environ.get("DPIA_VEC_LOCAL", "0") == "1"   # (off: no measured gain, the compiler merges them)
 # ... and each read stream of a work-item's fold keeps VEC_PREFETCH queue
 # slots in flight (a rotating register queue refilled VEC_PREFETCH slots
 # ahead; 0 disables).  A slot is one VEC_LOAD_BYTES vector: 32 = one sm_100
@@ -144,6 +147,11 @@ SMEM_LAYOUT = os.environ.get("DPIA_SMEM_LAYOUT", "swizzle")
 # 1-D shared buffers read at a work-item stride that is a multiple of 32
 # scalars get 4 scalars of padding per 32 (KernelEmitter._declare_local)
 SMEM_PAD_1D = os.environ.get("DPIA_SMEM_PAD_1D", "1") != "0"
+# count reads by a one-item work-item loop too (the single work-item that
+# folds a work-group's staged partials): padding that buffer measured
+# 66.6 against 93.2 us on the reference's gemv (same SASS shape, the padded
+# layout schedules better); DPIA_PAD_SINGLE=0 skips them
+PAD_SINGLE = os.environ.get("DPIA_PAD_SINGLE", "1") == "1"
 
 
 class NeedLanes(Exception):
@@ -648,7 +656,8 @@ class KernelEmitter:
         if self.recording and buf.space == "local" and len(dims) == 1 and isinstance(elem, Num):
             # a work-item index with a coefficient that is a multiple of 32
             # puts every work-item of a warp in the same bank
-            work = {lp.var for lp in self.loops if lp.level in ("local", "lin") and lp.var}
+            work = {lp.var for lp in self.loops if lp.level in ("local", "lin") and lp.var
+                    and (lp.trip is None or lp.trip > 1 or PAD_SINGLE)}
             hit = any(len(m) == 1 and IX._ATOMS[m[0]][0] == "v" and IX._ATOMS[m[0]][1] in work
                       and c % 32 == 0 for m, c in ix(idxs[0]).terms)
             self.local_reads[buf.key] = self.local_reads.get(buf.key, False) or hit
@@ -850,8 +859,9 @@ class KernelEmitter:
         vector, which the compiler loads once.  In a prefetching fold the
         vector comes from the stream's queue or ring when A mentions no loop
         variable bound inside the fold."""
-        if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global") \
-                or r.buf.swz or r.buf.pad or r.buf.pad32 or not isinstance(r.buf.elem, Num):
+        if not self.vec_vars or r.suffix or r.flat is None or r.buf.space not in ("in", "global", "local") \
+                or r.buf.swz or r.buf.pad or r.buf.pad32 or not isinstance(r.buf.elem, Num) \
+                or (r.buf.space == "local" and not VEC_LOCAL):
             return None
         coef = dict((m, c) for m, c in r.flat.terms)
         js = [v for v, w in self.vec_vars.items() if coef.get((v,)) == w]
@@ -865,7 +875,8 @@ class KernelEmitter:
         self.vec_hits += 1
         text = self.r(base)
         pf = self.vec_pf
-        if pf is not None and js[0] == pf["j"]:
+        if pf is not None and js[0] == pf["j"] and r.buf.space != "local":
+            # (shared-memory data is read in place: LDS.128, never queued)
             inner = {lp.var for lp in self.loops[pf["depth"]:]} - {pf["j"]}
             if not any(re.search(rf"\b{re.escape(v)}\b", text) for v in inner):
                 key = (r.buf.cname, text)
@@ -1184,6 +1195,8 @@ class KernelEmitter:
             self.line(f"const int {j} = {jo} + {jd};")
             take = len(self.lines)
         else:
+            if T > 8:
+                self.line("#pragma unroll 8")       # loads of later iterations issue ahead
             self.open(f"for (int {j} = 0; {j} < {T}; {j} += 1)")
         self.vec_vars[j] = W
         self.loops.append(Loop("seq", 0, j, T, nat(T), False))
