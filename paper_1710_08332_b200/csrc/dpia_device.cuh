@@ -309,6 +309,12 @@ __device__ __forceinline__ void bulk_stage(void* smem_dst, const void* gsrc, uns
 // One 256-bit global load (sm_100: LDG.E.ENL2.256) of W = 32 / sizeof(T)
 // consecutive scalars at p + i, 32-byte aligned.  NC: the buffer is read-only
 // for the whole kernel (a const __restrict__ input): the non-coherent path.
+// L2 prefetch of the 128-byte line at p (a later iteration's operands)
+template <class T>
+__device__ __forceinline__ void prefetch_l2(const T* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <bool NC>
 __device__ __forceinline__ vec<float, 8> vload32(const float* p, long long i) {
   vec<float, 8> r;

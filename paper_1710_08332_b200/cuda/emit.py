@@ -61,6 +61,8 @@ VEC_SHORT = os.environ.get("DPIA_VEC_SHORT", "1") != "0"
 # ... and read shared-memory operands of such folds as whole vectors too
 # (LDS.128: the single-thread fold of a work-group's staged partials)
 VEC_LOCAL = os.environ.get("DPIA_VEC_LOCAL", "0") == "1"   # (off: no measured gain, the compiler merges them)
+# L2 prefetch of a work-item fold's next work-group iteration (`_prefetch_next_group`)
+PREFETCH_NEXT = os.environ.get("DPIA_PREFETCH_NEXT", "1") != "0"
 # ... and each read stream of a work-item's fold keeps VEC_PREFETCH queue
 # slots in flight (a rotating register queue refilled VEC_PREFETCH slots
 # ahead; 0 disables).  A slot is one VEC_LOAD_BYTES vector: 32 = one sm_100
@@ -1247,7 +1249,31 @@ class KernelEmitter:
             pro.append(f"{pad}  {name.replace('pfv_', 'pfq_')}[{j}] = {self._vload(mode, b, W, base)};")
         pro.append(f"{pad}}}")
         self.lines[top:top] = pro
+        self._prefetch_next_group(streams, j, T * W * sb)
         return True
+
+    def _prefetch_next_group(self, streams, j: str, piece_bytes: int):
+        """A work-item fold inside a work-group loop (the reference's gemv:
+        a row per work-group, each work-item folding its own piece): once
+        the fold is done, prefetch into L2 the piece this work-item folds in
+        the work-group loop's next iteration, so its loads there hit L2
+        while this iteration's barrier and single-thread tail run."""
+        wg = [lp for lp in self.loops if lp.level == "workgroup"]
+        if not PREFETCH_NEXT or len(wg) != 1 or wg[0].single or not self.launch or wg[0].trip is None \
+                or piece_bytes > 8 * 128:
+            return
+        lp = wg[0]
+        G = self.launch[0][lp.dim]
+        sb = 4 if self.scalar == "float" else 8
+        for _name, b, base in streams:
+            coef = {m: c for m, c in base.terms}
+            if b.space != "in" or coef.get((lp.var,)) is None:
+                continue
+            at0 = Ix([(m, c) for m, c in base.terms if j not in IX.free_names(Ix([(m, c)]))])
+            nxt = at0 + ix(coef[(lp.var,)] * G)
+            for q in range(-(-piece_bytes // 128)):
+                self.line(f"if ({lp.var} + {G} < {lp.trip}) dpia::prefetch_l2({b.cname} + "
+                          f"({self.r(nxt)}) + {q * 128 // sb});")
 
     def _merge_lane_stores(self, lanes, W: int):
         """The W lanes of a vectorised fold iteration that each store one
