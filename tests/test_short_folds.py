@@ -75,3 +75,17 @@ def test_chain_trigger_placement():
     for cfg in (dot_config(), mm_config()):
         body, _ = _emit(cfg)
         assert "dpia::pdl_trigger();" in body and "pdl_wait_once<true>" not in body
+
+
+def test_next_work_group_piece_is_prefetched(monkeypatch):
+    """The reference's gemv: after its fold, a work-item prefetches into L2
+    the 128-byte piece it folds for the next row of its work-group loop
+    (row + gridDim), guarded by the loop bound; other kernels unchanged."""
+    body, _ = _emit(gemv_literal_config())
+    assert ("if (i_11_3 + 592 < 8192) dpia::prefetch_l2(A + (8192 * i_11_3 + 32 * i_5_6 + 4849664) + 0);"
+            in body)
+    body, _ = _emit(gemv_config())
+    assert "prefetch_l2" not in body
+    monkeypatch.setattr(EM, "PREFETCH_NEXT", False)
+    body, _ = _emit(gemv_literal_config())
+    assert "prefetch_l2" not in body
