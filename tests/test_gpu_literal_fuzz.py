@@ -108,3 +108,52 @@ def test_literal_shape_int_exact(seed, body, chunk, n, launch):
     vals = _run(exe, inputs)
     want = int(np.sum(ref(inputs["xs"], inputs.get("ys"))))
     assert all(int(v[0]) == want for v in vals)
+
+
+MAPS = {
+    # name: (fold body over element x, numpy of it): a work-item writes its own piece
+    "scale": ("(* alpha x)", lambda x, a: np.float32(a) * x),
+    "double": ("(+ x x)", lambda x, a: x + x),
+    # contracted to one FMA on the GPU: one rounding of the exact a x + x
+    "axpx": ("(+ (* alpha x) x)", lambda x, a: (np.float64(a) * x.astype(np.float64) + x)),
+}
+
+
+def map_program(body: str, chunk: int) -> str:
+    return (f"(nat n)\n(param alpha (exp num))\n(param xs (exp (array (* n {chunk}) num)))\n"
+            f"(join (mapGlobal (lam (c (exp (array {chunk} num))) (mapSeq (lam x {MAPS[body][0]}) c))"
+            f" (split {chunk} xs)))")
+
+
+def map_cases():
+    rng = np.random.default_rng(77)
+    out = []
+    for seed in range(18):
+        body = list(MAPS)[seed % len(MAPS)]
+        chunk = int(rng.choice([128, 256, 1024, 2048]))
+        L = int(rng.choice([32, 64]))
+        rounds = int(rng.choice([1, 2, 4]))
+        G = int(rng.integers(1, 9))
+        out.append((seed, body, chunk, G * L * rounds, (G, L)))
+    return out
+
+
+@pytest.mark.parametrize("seed,body,chunk,n,launch", map_cases())
+def test_literal_map_shape_fp32_exact(seed, body, chunk, n, launch):
+    """Work-items writing their own contiguous pieces (the reference's scal
+    shape): TMA row reads, merged vector stores leaving as TMA row stores,
+    several launches chained -- exact against numpy (one rounding per element
+    and the same operation order)."""
+    rng = np.random.default_rng(seed)
+    xs = rng.uniform(-1, 1, n * chunk).astype(np.float32)
+    exe = executable(compile_program(map_program(body, chunk)), launch, {"n": n}, float_mode=True)
+    from paper_1710_08332_b200 import runtime as RT
+    st = RT.Stream(0)
+    exe.upload("alpha", np.float32([1.25]), st)
+    exe.upload("xs", xs, st)
+    for k in range(3):
+        exe.launch(st, chain=k > 0)
+    got = np.asarray(exe.download("out", st))
+    st.sync()
+    want = MAPS[body][1](xs, 1.25).astype(np.float32)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
