@@ -1400,9 +1400,13 @@ class KernelEmitter:
         self.lines[take:take] = [
             f"{pad2}const {vt} {name} = dpia::vload<{self.scalar}, {W}>({name}_s + {jd} / {VB} * {box_elems}, "
             f"{W} * ({jd} % {VB} ^ {sw}));" for name, _tm, _c0 in specs]
+        where = [next((q for q in range(take, len(self.lines)) if self.lines[q].strip() == stmt), None)
+                 for _b, _t, _c, _v, stmt in stores]
+        if None in where:
+            stores = []              # (each store line is found before any is rewritten)
         ost = self.fresh("wos") if stores else None
         for k, (buf, tm, c0, vals, stmt) in enumerate(stores):
-            at = next(q for q in range(take, len(self.lines)) if self.lines[q].strip() == stmt)
+            at = where[k]
             ind = self.lines[at][:len(self.lines[at]) - len(self.lines[at].lstrip())]
             self.lines[at] = (f"{ind}dpia::vstore<{self.scalar}, {W}>(reinterpret_cast<{self.scalar}*>"
                               f"({ost} + ({ru} % {SO}) * {so_bytes} + {k * NB * 4096} + {lane} * 128) + "
@@ -2153,7 +2157,7 @@ class KernelEmitter:
         try:
             self.comm(c1)
             recs = self.probe_recs
-        except (_ProbeFail, CudaError, NeedLanes):
+        except Exception:  # noqa: BLE001 -- a probe that cannot follow the staging just declines
             recs = None
         finally:
             mark, self.ind, self.smem, ob, ok, self.loops, _ = saved
