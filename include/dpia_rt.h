@@ -71,7 +71,7 @@ int dpia_memcpy2d_dtoh(int device, void* dst, size_t dpitch, uint64_t src, size_
  * elem_bytes (4: fp32, 8: int64) elements, rows x cols with a row pitch in
  * bytes, read in boxes of box_rows x box_cols; swizzle 0 (plain) or 128
  * (128-byte rows, 16-byte chunks XOR row % 8): the kernel parameter of an
- * emitted toLocal k-tile or work-item row fold staged by
+ * emitted toLocal k-tile, work-item row fold or row store moved by
  * cp.async.bulk.tensor.2d (no reference counterpart: the reference has no
  * device code).  _f32: the plain fp32 form (tools/mmtma.py). */
 int dpia_tensor_map_2d(void* out, int elem_bytes, uint64_t base, uint64_t rows, uint64_t cols,
