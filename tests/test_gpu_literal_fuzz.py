@@ -157,3 +157,21 @@ def test_literal_map_shape_fp32_exact(seed, body, chunk, n, launch):
     st.sync()
     want = MAPS[body][1](xs, 1.25).astype(np.float32)
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_strided_piece_stores_exact():
+    """A work-item writing its piece through a layout view (every second
+    element): scalar stores, exact against numpy."""
+    text = ("(nat n)\n(param xs (exp (array (* n 256) num)))\n"
+            "(join (mapGlobal (lam (c (exp (array 256 num)))"
+            " (join (transpose (split 128 (mapSeq (lam x (* x x)) c))))) (split 256 xs)))")
+    xs = np.random.default_rng(9).uniform(-1, 1, 64 * 256).astype(np.float32)
+    exe = executable(compile_program(text), (2, 32), {"n": 64}, float_mode=True)
+    from paper_1710_08332_b200 import runtime as RT
+    st = RT.Stream(0)
+    exe.upload("xs", xs, st)
+    exe.launch(st)
+    got = np.asarray(exe.download("out", st))
+    st.sync()
+    want = (xs * xs).reshape(64, 2, 128).transpose(0, 2, 1).reshape(-1)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -89,3 +89,18 @@ def test_next_work_group_piece_is_prefetched(monkeypatch):
     monkeypatch.setattr(EM, "PREFETCH_NEXT", False)
     body, _ = _emit(gemv_literal_config())
     assert "prefetch_l2" not in body
+
+
+def test_strided_piece_stores_stay_scalar():
+    """Lanes that store non-consecutive elements (a work-item writing every
+    second element of its piece) are not merged into a vector store."""
+    from paper_1710_08332_b200 import compile_program
+    text = ("(nat n)\n(param xs (exp (array (* n 256) num)))\n"
+            "(join (mapGlobal (lam (c (exp (array 256 num)))"
+            " (join (transpose (split 128 (mapSeq (lam x (* x x)) c))))) (split 256 xs)))")
+    prog = compile_program(text)
+    outs = [("out", prog.out_type)]
+    ins = [(nm, t.data) for nm, t in prog.source.params]
+    src, _ = EM.emit_cuda(prog.imperative, outs, ins, sigma={"n": 64}, launch=(2, 32))
+    body = src.split('extern "C"')[1]
+    assert "dpia::vstore<float, 4>(out" not in body and "tma_store_2d(&" not in body
